@@ -1,0 +1,514 @@
+// fa_api.cu -- the C ABI declared in include/rf_fa.h: validation with the reference's error
+// behaviour, TMA tensor-map construction, kernel selection, workspace layout, the host-buffer
+// entry point and the FusedFlashAttention op dispatch (reference interpreter.cpp:308-318).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/rf_fa.h"
+#include "fa_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(RF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// Resolved once through the runtime (no link-time dependency on libcuda).
+EncodeTiledFn encode_tiled_fn() {
+    static EncodeTiledFn fn = [] {
+        void* sym = nullptr;
+        cudaDriverEntryPointQueryResult qres;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &sym, cudaEnableDefault, &qres) != cudaSuccess ||
+            qres != cudaDriverEntryPointSuccess)
+            sym = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(sym);
+    }();
+    return fn;
+}
+
+struct Resolved {
+    int64_t qs[3], ks[3], vs[3], os[3];
+    double scale;  // effective
+    int64_t kv_begin, kv_end;
+    bool partial;
+};
+
+void resolve_strides(const int64_t in[3], int64_t out[3], int64_t H, int64_t S, int64_t d) {
+    if (in[2] == 0) {  // contiguous [B,H,S,d]
+        out[0] = H * S * d;
+        out[1] = S * d;
+        out[2] = d;
+    } else {
+        out[0] = in[0];
+        out[1] = in[1];
+        out[2] = in[2];
+    }
+}
+
+// Checks in the reference's order (attention.cpp:14-21 rank/shape are structural here;
+// pad_bias shape is checked by the host-tensor entry points), then this build's own.
+int validate(const rf_fa_params* p, Resolved* r) {
+    if (p == nullptr) return fail(RF_ERR_ARG, "params is null");
+    if (p->B < 0 || p->H < 0 || p->S < 0 || p->d < 0) return fail(RF_ERR_SHAPE, "negative dimension");
+    if (p->d != 32 && p->d != 64 && p->d != 128)
+        return fail(RF_ERR_HEAD_DIM, "head_dim must be one of {32, 64, 128}, got " + std::to_string(p->d));
+    if (p->dtype != RF_DTYPE_BF16 && p->dtype != RF_DTYPE_F16)
+        return fail(RF_ERR_ARG, "dtype must be bf16 or f16");
+    if (p->out_dtype < RF_DTYPE_BF16 || p->out_dtype > RF_DTYPE_F32) return fail(RF_ERR_ARG, "bad out_dtype");
+    if (p->kernel < RF_KERNEL_AUTO || p->kernel > RF_KERNEL_SIMT) return fail(RF_ERR_ARG, "bad kernel selector");
+    // any negative window bound means "unbounded", as in attention.cpp:132-136
+    if (p->S > (1ll << 30) || p->B * p->H > (1ll << 30)) return fail(RF_ERR_ARG, "dimension too large");
+    r->partial = p->o_partial != nullptr;
+    if (r->partial && (p->m_partial == nullptr || p->l_partial == nullptr))
+        return fail(RF_ERR_ARG, "split-KV needs o_partial, m_partial and l_partial");
+    const bool empty = p->B == 0 || p->H == 0 || p->S == 0;
+    if (!empty) {
+        if (p->q == nullptr || p->k == nullptr || p->v == nullptr) return fail(RF_ERR_ARG, "q/k/v is null");
+        if (!r->partial && p->out == nullptr) return fail(RF_ERR_ARG, "out is null");
+    }
+    resolve_strides(p->q_stride, r->qs, p->H, p->S, p->d);
+    resolve_strides(p->k_stride, r->ks, p->H, p->S, p->d);
+    resolve_strides(p->v_stride, r->vs, p->H, p->S, p->d);
+    resolve_strides(p->o_stride, r->os, p->H, p->S, p->d);
+    r->scale = p->scale != 0.0 ? p->scale : 1.0 / std::sqrt(static_cast<double>(p->d));  // attention.cpp:34-36
+    if (!std::isfinite(r->scale)) return fail(RF_ERR_ARG, "scale is not finite");
+    r->kv_begin = p->kv_begin;
+    r->kv_end = p->kv_end;
+    if (r->kv_begin == 0 && r->kv_end == 0) r->kv_end = p->S;
+    if (r->kv_begin < 0 || r->kv_end > p->S || r->kv_begin > r->kv_end)
+        return fail(RF_ERR_ARG, "kv range must satisfy 0 <= kv_begin <= kv_end <= S");
+    return RF_OK;
+}
+
+bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
+bool strides_ok_tma(const int64_t s[3]) { return s[0] > 0 && s[1] > 0 && s[2] > 0 && s[0] % 8 == 0 && s[1] % 8 == 0 && s[2] % 8 == 0; }
+
+// Can the tcgen05 kernel take this call?  (head_dim 64, scale > 0, TMA-compatible layout.)
+bool tcgen05_eligible(const rf_fa_params* p, const Resolved& r, std::string* why) {
+    if (p->d != 64) {
+        *why = "tcgen05 kernel covers head_dim 64";
+        return false;
+    }
+    if (!(r.scale > 0.0)) {
+        *why = "tcgen05 kernel needs scale > 0";
+        return false;
+    }
+    if (!aligned16(p->q) || !aligned16(p->k) || !aligned16(p->v) || !strides_ok_tma(r.qs) ||
+        !strides_ok_tma(r.ks) || !strides_ok_tma(r.vs)) {
+        *why = "q/k/v must be 16-byte aligned with strides that are multiples of 8 elements";
+        return false;
+    }
+    if (!r.partial) {
+        const int64_t al = p->out_dtype == RF_DTYPE_F32 ? 4 : 8;
+        if (!aligned16(p->out) || r.os[0] % al || r.os[1] % al || r.os[2] % al) {
+            *why = "out rows must be 16-byte aligned";
+            return false;
+        }
+    } else if (!aligned16(p->o_partial)) {
+        *why = "o_partial must be 16-byte aligned";
+        return false;
+    }
+    return true;
+}
+
+int select_kernel(const rf_fa_params* p, const Resolved& r, int* kernel) {
+    std::string why;
+    const bool ok = tcgen05_eligible(p, r, &why);
+    if (p->kernel == RF_KERNEL_TCGEN05 && !ok) return fail(RF_ERR_UNSUPPORTED, why);
+    *kernel = (p->kernel == RF_KERNEL_SIMT || !ok) ? RF_KERNEL_SIMT : RF_KERNEL_TCGEN05;
+    return RF_OK;
+}
+
+int64_t n_kv_tiles(int64_t S) { return (S + rf::kBlockN - 1) / rf::kBlockN; }
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+size_t workspace_bytes_for(const rf_fa_params* p, int kernel) {
+    if (kernel != RF_KERNEL_TCGEN05 || p->pad_bias == nullptr || p->B == 0 || p->S == 0) return 0;
+    const size_t nt = static_cast<size_t>(n_kv_tiles(p->S));
+    return align_up(static_cast<size_t>(p->B) * nt * rf::kBlockN * sizeof(float), 256) +
+           align_up(static_cast<size_t>(p->B) * nt, 256);
+}
+
+int make_tmap(CUtensorMap* tm, const void* base, int dtype, int64_t d, int64_t S, int64_t H, int64_t B,
+              const int64_t st[3]) {
+    EncodeTiledFn enc = encode_tiled_fn();
+    if (enc == nullptr) return fail(RF_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable (driver too old?)");
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(H),
+                                static_cast<cuuint64_t>(B)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(st[2]) * 2, static_cast<cuuint64_t>(st[1]) * 2,
+                                   static_cast<cuuint64_t>(st[0]) * 2};
+    const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(rf::kBlockN), 1, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult res =
+        enc(tm, dtype == RF_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+            const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) return fail(RF_ERR_CUDA, "cuTensorMapEncodeTiled failed, CUresult " + std::to_string(res));
+    return RF_OK;
+}
+
+void fill_fa_params(const rf_fa_params* p, const Resolved& r, rf::FaParams* f) {
+    std::memset(f, 0, sizeof(*f));
+    f->B = static_cast<int>(p->B);
+    f->H = static_cast<int>(p->H);
+    f->S = static_cast<int>(p->S);
+    f->kv_begin = static_cast<int>(r.kv_begin);
+    f->kv_end = static_cast<int>(r.kv_end);
+    f->wl = static_cast<int>(p->window_left < 0 ? -1 : (p->window_left > (1 << 30) ? (1 << 30) : p->window_left));
+    f->wr = static_cast<int>(p->window_right < 0 ? -1 : (p->window_right > (1 << 30) ? (1 << 30) : p->window_right));
+    f->scale_log2 = static_cast<float>(r.scale * 1.4426950408889634);
+    f->n_kv_tiles = static_cast<int>(n_kv_tiles(p->S));
+    f->bias_stride = f->n_kv_tiles * rf::kBlockN;
+    f->out = p->out;
+    f->o_sb = r.os[0];
+    f->o_sh = r.os[1];
+    f->o_ss = r.os[2];
+    f->out_dtype = p->out_dtype;
+    f->o_partial = p->o_partial;
+    f->m_partial = p->m_partial;
+    f->l_partial = p->l_partial;
+    f->debug_scores = p->debug_scores;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rf_last_error(void) { return g_last_error.c_str(); }
+int rf_abi_version(void) { return RF_FA_ABI_VERSION; }
+
+void rf_fa_params_init(rf_fa_params* p) {
+    if (p == nullptr) return;
+    std::memset(p, 0, sizeof(*p));
+    p->window_left = -1;
+    p->window_right = -1;
+    p->dtype = RF_DTYPE_BF16;
+    p->out_dtype = RF_DTYPE_BF16;
+    p->kernel = RF_KERNEL_AUTO;
+}
+
+int rf_fa_validate(const rf_fa_params* p) {
+    Resolved r;
+    int rc = validate(p, &r);
+    if (rc != RF_OK) return rc;
+    int kernel;
+    return select_kernel(p, r, &kernel);
+}
+
+int rf_fa_fwd_workspace_bytes(const rf_fa_params* p, size_t* bytes) {
+    if (bytes == nullptr) return fail(RF_ERR_ARG, "bytes is null");
+    Resolved r;
+    int rc = validate(p, &r);
+    if (rc != RF_OK) return rc;
+    int kernel;
+    rc = select_kernel(p, r, &kernel);
+    if (rc != RF_OK) return rc;
+    *bytes = workspace_bytes_for(p, kernel);
+    return RF_OK;
+}
+
+int rf_fa_stats_query(const rf_fa_params* p, rf_fa_stats* st) {
+    if (st == nullptr) return fail(RF_ERR_ARG, "stats is null");
+    Resolved r;
+    int rc = validate(p, &r);
+    if (rc != RF_OK) return rc;
+    int kernel;
+    rc = select_kernel(p, r, &kernel);
+    if (rc != RF_OK) return rc;
+    std::memset(st, 0, sizeof(*st));
+    st->kernel = kernel;
+    st->workspace_bytes = workspace_bytes_for(p, kernel);
+    const bool p_tmem = !(p->flags & RF_FA_FLAG_P_SMEM);
+    st->tile_scratch_bytes = kernel == RF_KERNEL_TCGEN05
+                                 ? rf::fa_fwd_sm100_smem_bytes(p_tmem) + 512ull * 128 * 4  // smem + TMEM
+                                 : (2ull * 32 * p->d + 32) * sizeof(float);
+    st->row_state_bytes = 2ull * sizeof(float) * static_cast<uint64_t>(p->S);
+    const uint64_t esz = p->out_dtype == RF_DTYPE_F32 ? 4 : 2;
+    st->output_bytes = static_cast<uint64_t>(p->B) * p->H * p->S * p->d * (r.partial ? 4 : esz);
+    st->score_matrix_bytes = 0;
+    const int64_t rows_per_cta = kernel == RF_KERNEL_TCGEN05 ? rf::kRowsPerCta : 32;
+    st->grid_ctas = static_cast<int32_t>(((p->S + rows_per_cta - 1) / rows_per_cta) * p->H * p->B);
+    return RF_OK;
+}
+
+int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, void* stream_v) {
+    Resolved r;
+    int rc = validate(p, &r);
+    if (rc != RF_OK) return rc;
+    int kernel;
+    rc = select_kernel(p, r, &kernel);
+    if (rc != RF_OK) return rc;
+    if (p->B == 0 || p->H == 0 || p->S == 0) return RF_OK;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+
+    rf::FaParams f;
+    fill_fa_params(p, r, &f);
+    int grid = 0;
+
+    if (kernel == RF_KERNEL_SIMT) {
+        rf::SimtParams sp;
+        std::memset(&sp, 0, sizeof(sp));
+        sp.q = p->q;
+        sp.k = p->k;
+        sp.v = p->v;
+        sp.q_sb = r.qs[0]; sp.q_sh = r.qs[1]; sp.q_ss = r.qs[2];
+        sp.k_sb = r.ks[0]; sp.k_sh = r.ks[1]; sp.k_ss = r.ks[2];
+        sp.v_sb = r.vs[0]; sp.v_sh = r.vs[1]; sp.v_ss = r.vs[2];
+        sp.in_dtype = p->dtype;
+        sp.d = static_cast<int>(p->d);
+        sp.f = f;
+        sp.f.bias2 = p->pad_bias;  // raw [B,S] bias; see launch_fa_fwd_simt
+        cudaError_t e = rf::launch_fa_fwd_simt(sp, stream, &grid);
+        if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_simt launch");
+        return RF_OK;
+    }
+
+    // ---- tcgen05 path ----
+    const size_t need = workspace_bytes_for(p, kernel);
+    if (need > 0) {
+        if (workspace == nullptr || workspace_bytes < need)
+            return fail(RF_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+        if (!aligned16(workspace)) return fail(RF_ERR_WORKSPACE, "workspace must be 16-byte aligned");
+        const size_t nt = static_cast<size_t>(f.n_kv_tiles);
+        float* bias2 = static_cast<float*>(workspace);
+        uint8_t* flags = static_cast<uint8_t*>(workspace) +
+                         align_up(static_cast<size_t>(p->B) * nt * rf::kBlockN * sizeof(float), 256);
+        cudaError_t e = rf::launch_bias_prepare(p->pad_bias, f.B, f.S, bias2, flags, f.n_kv_tiles, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "bias_prepare launch");
+        f.bias2 = bias2;
+        f.tile_flags = flags;
+    }
+    CUtensorMap tmq, tmk, tmv;
+    if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
+    if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
+    if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
+    const bool p_tmem = !(p->flags & RF_FA_FLAG_P_SMEM);
+    cudaError_t e = rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, p_tmem, stream, &grid);
+    if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100 launch");
+    return RF_OK;
+}
+
+int rf_fa_merge(const float* const* o_parts, const float* const* m_parts, const float* const* l_parts, int32_t G,
+                int64_t rows, int64_t d, void* out, int32_t out_dtype, void* stream) {
+    if (o_parts == nullptr || m_parts == nullptr || l_parts == nullptr || out == nullptr)
+        return fail(RF_ERR_ARG, "null pointer");
+    if (G < 1 || G > 16) return fail(RF_ERR_ARG, "G must be in [1,16]");
+    if (d <= 0 || d % 4) return fail(RF_ERR_ARG, "d must be a positive multiple of 4");
+    cudaError_t e = rf::launch_merge(o_parts, m_parts, l_parts, G, rows, static_cast<int>(d), out, out_dtype,
+                                     static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+    return RF_OK;
+}
+
+int rf_fa_rescale_partial(float* o_part, float* l_part, const float* m_part, const float* m_star, int64_t rows,
+                          int64_t d, void* stream) {
+    if (o_part == nullptr || l_part == nullptr || m_part == nullptr || m_star == nullptr)
+        return fail(RF_ERR_ARG, "null pointer");
+    cudaError_t e = rf::launch_rescale_partial(o_part, l_part, m_part, m_star, rows, static_cast<int>(d),
+                                               static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "rescale_partial launch");
+    return RF_OK;
+}
+
+int rf_fa_normalize(const float* o_sum, const float* l_sum, int64_t rows, int64_t d, void* out, int32_t out_dtype,
+                    void* stream) {
+    if (o_sum == nullptr || l_sum == nullptr || out == nullptr) return fail(RF_ERR_ARG, "null pointer");
+    cudaError_t e = rf::launch_normalize(o_sum, l_sum, rows, static_cast<int>(d), out, out_dtype,
+                                         static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "normalize launch");
+    return RF_OK;
+}
+
+int rf_pad_bias_from_mask(const float* mask, float* pad_bias, int64_t n, void* stream) {
+    if (n < 0 || (n > 0 && (mask == nullptr || pad_bias == nullptr))) return fail(RF_ERR_ARG, "null pointer");
+    cudaError_t e = rf::launch_pad_bias_from_mask(mask, pad_bias, n, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "pad_bias_from_mask launch");
+    return RF_OK;
+}
+
+int rf_cast_f32_to(const float* src, void* dst, int64_t n, int32_t dst_dtype, void* stream) {
+    if (dst_dtype != RF_DTYPE_BF16 && dst_dtype != RF_DTYPE_F16) return fail(RF_ERR_ARG, "bad dtype");
+    cudaError_t e = rf::launch_cast_from_f32(src, dst, n, dst_dtype, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "cast launch");
+    return RF_OK;
+}
+
+int rf_cast_to_f32(const void* src, float* dst, int64_t n, int32_t src_dtype, void* stream) {
+    if (src_dtype != RF_DTYPE_BF16 && src_dtype != RF_DTYPE_F16) return fail(RF_ERR_ARG, "bad dtype");
+    cudaError_t e = rf::launch_cast_to_f32(src, dst, n, src_dtype, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "cast launch");
+    return RF_OK;
+}
+
+int rf_device_check(int32_t device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (device < 0 || device >= n) return fail(RF_ERR_CUDA, "no CUDA device " + std::to_string(device));
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (sm_count) *sm_count = prop.multiProcessorCount;
+    if (cc_major) *cc_major = prop.major;
+    if (cc_minor) *cc_minor = prop.minor;
+    if (prop.major != 10) return fail(RF_ERR_CUDA, "device is not sm_100 (Blackwell B200)");
+    return RF_OK;
+}
+
+uint64_t rf_mask_memory_bytes(uint64_t batch, uint64_t heads, uint64_t seq_len, uint64_t bpe) {
+    return batch * heads * seq_len * seq_len * bpe;  // attention.cpp:244-247
+}
+uint64_t rf_fa_memory_bytes(uint64_t batch, uint64_t heads, uint64_t seq_len, uint64_t head_dim, uint64_t tile,
+                            uint64_t bpe) {
+    return batch * heads * (2 * tile * head_dim + seq_len * head_dim) * bpe;  // attention.cpp:249-252
+}
+
+// ---------------------------------------------------------------------------------------------
+// Host-tensor entry points (the reference's calling convention)
+// ---------------------------------------------------------------------------------------------
+int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, int64_t B, int64_t H, int64_t S,
+                   int64_t d, double scale, int64_t window_left, int64_t window_right, const float* pad_bias,
+                   const int64_t* pad_bias_dims, int64_t tile, int32_t compute_dtype, int32_t device,
+                   rf_fa_stats* stats) {
+    // reference check order: check_qkv (structural here), tile, pad_bias shape (attention.cpp:107-116)
+    if (B < 0 || H < 0 || S < 0 || d < 0) return fail(RF_ERR_SHAPE, "negative dimension");
+    if (tile < 1) return fail(RF_ERR_SHAPE, "tile must be >= 1");
+    if (pad_bias != nullptr) {
+        if (pad_bias_dims == nullptr || pad_bias_dims[0] != B || pad_bias_dims[1] != 1 || pad_bias_dims[2] != 1 ||
+            pad_bias_dims[3] != S)
+            return fail(RF_ERR_SHAPE, "pad_bias must be [B,1,1,S]");
+    }
+    rf_fa_params p;
+    rf_fa_params_init(&p);
+    p.B = B; p.H = H; p.S = S; p.d = d;
+    p.scale = scale;
+    p.window_left = window_left;
+    p.window_right = window_right;
+    p.dtype = compute_dtype;
+    p.out_dtype = RF_DTYPE_F32;
+    const int64_t n = B * H * S * d;
+    if (n == 0) {
+        Resolved r;
+        int rc0 = validate(&p, &r);
+        if (rc0 != RF_OK) return rc0;
+        if (stats) std::memset(stats, 0, sizeof(*stats));
+        return RF_OK;
+    }
+    if (q == nullptr || k == nullptr || v == nullptr || out == nullptr) return fail(RF_ERR_ARG, "null host pointer");
+
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    cudaStream_t stream = nullptr;
+    e = cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+
+    float* d_f32 = nullptr;   // staging for one f32 input at a time, then reused as the f32 output
+    uint16_t* d_qkv = nullptr;
+    float* d_bias = nullptr;
+    void* d_ws = nullptr;
+    int rc = RF_OK;
+    auto cleanup = [&]() {
+        if (d_f32) cudaFreeAsync(d_f32, stream);
+        if (d_qkv) cudaFreeAsync(d_qkv, stream);
+        if (d_bias) cudaFreeAsync(d_bias, stream);
+        if (d_ws) cudaFreeAsync(d_ws, stream);
+        cudaStreamSynchronize(stream);
+        cudaStreamDestroy(stream);
+    };
+#define RF_TRY_CUDA(call, what)            \
+    do {                                   \
+        cudaError_t _e = (call);           \
+        if (_e != cudaSuccess) {           \
+            rc = cuda_fail(_e, what);      \
+            cleanup();                     \
+            return rc;                     \
+        }                                  \
+    } while (0)
+
+    const size_t nb32 = static_cast<size_t>(n) * sizeof(float);
+    RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_f32), 3 * nb32, stream), "cudaMallocAsync");
+    RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_qkv), 3 * static_cast<size_t>(n) * 2, stream),
+                "cudaMallocAsync");
+    const float* host_in[3] = {q, k, v};
+    for (int t = 0; t < 3; ++t) {
+        RF_TRY_CUDA(cudaMemcpyAsync(d_f32 + static_cast<size_t>(t) * n, host_in[t], nb32, cudaMemcpyHostToDevice, stream),
+                    "H2D copy");
+    }
+    RF_TRY_CUDA(rf::launch_cast_from_f32(d_f32, d_qkv, 3 * n, compute_dtype, stream), "cast launch");
+    if (pad_bias != nullptr) {
+        RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bias), static_cast<size_t>(B) * S * sizeof(float), stream),
+                    "cudaMallocAsync");
+        RF_TRY_CUDA(cudaMemcpyAsync(d_bias, pad_bias, static_cast<size_t>(B) * S * sizeof(float),
+                                    cudaMemcpyHostToDevice, stream),
+                    "H2D copy");
+    }
+    p.q = d_qkv;
+    p.k = d_qkv + n;
+    p.v = d_qkv + 2 * n;
+    p.out = d_f32;  // inputs are already cast; reuse the first staging slab for O (f32)
+    p.pad_bias = d_bias;
+    size_t ws = 0;
+    rc = rf_fa_fwd_workspace_bytes(&p, &ws);
+    if (rc != RF_OK) {
+        cleanup();
+        return rc;
+    }
+    if (ws > 0) RF_TRY_CUDA(cudaMallocAsync(&d_ws, ws, stream), "cudaMallocAsync");
+    if (stats) rf_fa_stats_query(&p, stats);
+    rc = rf_fa_fwd(&p, d_ws, ws, stream);
+    if (rc != RF_OK) {
+        cleanup();
+        return rc;
+    }
+    RF_TRY_CUDA(cudaMemcpyAsync(out, d_f32, nb32, cudaMemcpyDeviceToHost, stream), "D2H copy");
+    RF_TRY_CUDA(cudaStreamSynchronize(stream), "stream sync");
+#undef RF_TRY_CUDA
+    cleanup();
+    return RF_OK;
+}
+
+int rf_fused_flash_attention_op(const float* const* inputs, const int64_t* const* input_dims,
+                                const int32_t* input_ranks, int32_t n_inputs, int32_t has_scale, double scale,
+                                int32_t has_window_left, int64_t window_left, int32_t has_window_right,
+                                int64_t window_right, float* output, int32_t device) {
+    if (inputs == nullptr || input_dims == nullptr || input_ranks == nullptr) return fail(RF_ERR_ARG, "null pointer");
+    if (n_inputs < 3) return fail(RF_ERR_SHAPE, "FusedFlashAttention: missing input tensor");  // interpreter.cpp:209-214
+    // check_qkv (attention.cpp:14-21)
+    for (int t = 0; t < 3; ++t)
+        if (input_ranks[t] != 4) return fail(RF_ERR_SHAPE, "attention inputs must be [B,H,S,d]");
+    for (int t = 1; t < 3; ++t)
+        for (int a = 0; a < 4; ++a)
+            if (input_dims[t][a] != input_dims[0][a]) return fail(RF_ERR_SHAPE, "Q, K, V must have identical shapes");
+    const int64_t* qd = input_dims[0];
+    const float* bias = nullptr;
+    int64_t bias_dims[4] = {0, 0, 0, 0};
+    if (n_inputs > 3) {  // interpreter.cpp:313-315
+        bias = inputs[3];
+        if (input_ranks[3] != 4) return fail(RF_ERR_SHAPE, "pad_bias must be [B,1,1,S]");
+        for (int a = 0; a < 4; ++a) bias_dims[a] = input_dims[3][a];
+        if (bias == nullptr) return fail(RF_ERR_ARG, "pad_bias input is null");
+    }
+    // attrs default exactly like node.attr_real("scale", 0.0) / attr_int("window_*", -1)
+    return rf_fa_fwd_host(inputs[0], inputs[1], inputs[2], output, qd[0], qd[1], qd[2], qd[3],
+                          has_scale ? scale : 0.0, has_window_left ? window_left : -1,
+                          has_window_right ? window_right : -1, bias, bias ? bias_dims : nullptr, 64,
+                          RF_DTYPE_BF16, device, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,474 @@
+// fa_fwd_sm100.cu -- FusedFlashAttention forward for sm_100a (B200), head_dim 64.
+//
+// Semantics: reference routefast::flash_attention (proj/core/src/attention.cpp:106-213):
+// non-causal, additive padding bias (masked at <= -30000), optional two-sided sliding window,
+// online softmax, rows without a live key -> 0.  No S x S tensor is ever materialised.
+//
+// Hardware mapping (one CTA per SM, 320 threads, two 128-row query tiles "A"/"B" ping-pong):
+//   warp 8      TMA producer: Q once, then K/V 128-key tiles through two 3-deep smem rings
+//               (cp.async.bulk.tensor, 128B swizzle, mbarrier complete_tx)
+//   warp 9      UMMA issuer (one elected lane): S_X = Q_X K^T  (tcgen05.mma SS, M128 N128 K16 x4)
+//                                               O_X += P_X V   (tcgen05.mma TS, M128 N64  K16 x8)
+//               accumulators in TMEM: S_A cols [0,128) S_B [128,256) O_A [256,320) O_B [320,384);
+//               P_X (bf16) aliases the first 64 columns of S_X.
+//   warps 0-3   softmax for tile A, warps 4-7 for tile B: one thread owns one query row
+//               (tcgen05.ld 32x32b), so row max / row sum need no shuffles; exp2 with the scale
+//               folded in; lazy rescale of O (only when the running max grows by > 2^8).
+// K/V are loaded once per 256 query rows; the tensor pipe and the MUFU pipe overlap because
+// tile A's softmax runs while tile B's MMAs execute and vice versa.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "fa_internal.h"
+#include "ptx.cuh"
+
+namespace rf {
+namespace {
+
+using namespace rfptx;
+
+constexpr int kHeadDim = 64;
+constexpr int kStages = 3;                          // ring depth for K and for V
+constexpr int kTileBytes = kBlockN * kHeadDim * 2;  // 16 KiB: one 128 x 64 16-bit tile
+constexpr int kNumSoftmaxWarps = 8;
+constexpr int kProducerWarp = 8;
+constexpr int kMmaWarp = 9;
+constexpr int kThreads = 320;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColS = 0;    // + 128 * X
+constexpr uint32_t kColO = 256;  // + 64 * X
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: P <= 2^8 before a rescale is forced
+
+// dynamic shared memory map (offsets from a 1024B-aligned base)
+struct Smem {
+    static constexpr uint32_t q = 0;                                   // 2 tiles
+    static constexpr uint32_t k = q + 2 * kTileBytes;                  // kStages tiles
+    static constexpr uint32_t v = k + kStages * kTileBytes;            // kStages tiles
+    static constexpr uint32_t p = v + kStages * kTileBytes;            // SS mode only: 2 x 32 KiB
+    static constexpr uint32_t bars_tmem = p;                           // barrier block (TS mode)
+    static constexpr uint32_t bars_ss = p + 2 * 2 * kTileBytes;        // barrier block (SS mode)
+    static constexpr uint32_t bar_bytes = 256;
+};
+// barrier indices inside the barrier block (8 bytes each)
+enum : uint32_t {
+    kBarQFull = 0,
+    kBarKFull = 1,                      // [kStages]
+    kBarKEmpty = kBarKFull + kStages,   // [kStages]
+    kBarVFull = kBarKEmpty + kStages,   // [kStages]
+    kBarVEmpty = kBarVFull + kStages,   // [kStages]
+    kBarSFull = kBarVEmpty + kStages,   // [2]
+    kBarPFull = kBarSFull + 2,          // [2]
+    kBarOFull = kBarPFull + 2,          // [2]
+    kNumBars = kBarOFull + 2,
+};
+static_assert(kNumBars * 8 + 8 <= Smem::bar_bytes, "barrier block too small");
+
+__device__ __forceinline__ bool tile_live(const FaParams& p, int b, int n) {
+    return p.tile_flags == nullptr || p.tile_flags[b * p.n_kv_tiles + n] != kTileSkip;
+}
+
+template <bool kBf16, bool kPTmem>
+__global__ void __launch_bounds__(kThreads, 1)
+fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const FaParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
+    const uint32_t bars = smem_base + (kPTmem ? Smem::bars_tmem : Smem::bars_ss);
+    auto bar = [&](uint32_t i) { return bars + 8u * i; };
+    volatile uint32_t* tmem_slot =
+        reinterpret_cast<volatile uint32_t*>(smem_gen + (kPTmem ? Smem::bars_tmem : Smem::bars_ss) + 8 * kNumBars);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int q0 = blockIdx.x * kRowsPerCta;
+    const int h = blockIdx.y;
+    const int b = blockIdx.z;
+    const bool has_b = q0 + kBlockM < p.S;
+    const int rows_end = min(q0 + kRowsPerCta, p.S);
+
+    // key-tile range of this CTA (union over its rows of window and split range)
+    int j_lo = p.kv_begin, j_hi = p.kv_end;
+    if (p.wl >= 0) j_lo = max(j_lo, q0 - p.wl);
+    if (p.wr >= 0) j_hi = min(j_hi, rows_end + p.wr);
+    const int n0 = j_lo >> 7;
+    const int n1 = (j_hi > j_lo) ? ((j_hi + kBlockN - 1) >> 7) : n0;
+    int num_live = 0;
+    for (int n = n0; n < n1; ++n) num_live += tile_live(p, b, n) ? 1 : 0;
+
+    // ---------------- prologue ----------------
+    if (warp == kProducerWarp && lane == 0) {
+        prefetch_tensormap(&tm_q);
+        prefetch_tensormap(&tm_k);
+        prefetch_tensormap(&tm_v);
+        mbar_init(bar(kBarQFull), 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(bar(kBarKFull + s), 1);
+            mbar_init(bar(kBarKEmpty + s), 1);
+            mbar_init(bar(kBarVFull + s), 1);
+            mbar_init(bar(kBarVEmpty + s), 1);
+        }
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(bar(kBarSFull + x), 1);
+            mbar_init(bar(kBarPFull + x), kBlockM);
+            mbar_init(bar(kBarOFull + x), 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == kMmaWarp) {
+        tmem_alloc(smem_u32(const_cast<uint32_t*>(tmem_slot)), kTmemCols);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == kProducerWarp) {
+        // =============================== TMA producer ===============================
+        if (lane == 0 && num_live > 0) {
+            mbar_arrive_expect_tx(bar(kBarQFull), has_b ? 2 * kTileBytes : kTileBytes);
+            tma_load_4d(smem_base + Smem::q, &tm_q, bar(kBarQFull), 0, q0, h, b);
+            if (has_b) tma_load_4d(smem_base + Smem::q + kTileBytes, &tm_q, bar(kBarQFull), 0, q0 + kBlockM, h, b);
+            int it = 0;
+            for (int n = n0; n < n1; ++n) {
+                if (!tile_live(p, b, n)) continue;
+                const int st = it % kStages;
+                const uint32_t ph = (it / kStages) & 1;
+                mbar_wait(bar(kBarKEmpty + st), ph ^ 1);
+                mbar_arrive_expect_tx(bar(kBarKFull + st), kTileBytes);
+                tma_load_4d(smem_base + Smem::k + st * kTileBytes, &tm_k, bar(kBarKFull + st), 0, n * kBlockN, h, b);
+                mbar_wait(bar(kBarVEmpty + st), ph ^ 1);
+                mbar_arrive_expect_tx(bar(kBarVFull + st), kTileBytes);
+                tma_load_4d(smem_base + Smem::v + st * kTileBytes, &tm_v, bar(kBarVFull + st), 0, n * kBlockN, h, b);
+                ++it;
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // =============================== UMMA issuer ===============================
+        if (lane == 0 && num_live > 0) {
+            constexpr uint32_t fmt = kBf16 ? 1u : 0u;
+            constexpr uint32_t idesc_qk = make_idesc_f16(fmt, 0, 0, kBlockM, kBlockN);
+            constexpr uint32_t idesc_pv = make_idesc_f16(fmt, 0, 1, kBlockM, kHeadDim);
+
+            // S_X = Q_X * K^T : both operands K-major (head dim contiguous), 128B swizzle,
+            // 8-row core-matrix groups 1024 B apart; a K=16 step advances 32 B inside the atom.
+            auto issue_qk = [&](int x, int st) {
+                const uint32_t qa = smem_base + Smem::q + x * kTileBytes;
+                const uint32_t ka = smem_base + Smem::k + st * kTileBytes;
+#pragma unroll
+                for (int kk = 0; kk < kHeadDim / 16; ++kk) {
+                    const uint64_t ad = make_smem_desc(qa + kk * 32, 16, 1024, kSwizzle128B);
+                    const uint64_t bd = make_smem_desc(ka + kk * 32, 16, 1024, kSwizzle128B);
+                    mma_ss(tmem_base + kColS + x * kBlockN, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+                }
+            };
+            // O_X += P_X * V : B operand V is [key][d] with d contiguous = MN-major, 128B swizzle;
+            // 8-key groups 1024 B apart (SBO); a K=16 step advances 16 keys = 2048 B.
+            auto issue_pv = [&](int x, int st, bool accumulate) {
+                const uint32_t va = smem_base + Smem::v + st * kTileBytes;
+#pragma unroll
+                for (int kk = 0; kk < kBlockN / 16; ++kk) {
+                    const uint64_t bd = make_smem_desc(va + kk * 2048, kTileBytes, 1024, kSwizzle128B);
+                    const uint32_t acc = (accumulate || kk > 0) ? 1u : 0u;
+                    if (kPTmem) {
+                        // A = P from TMEM: 16 bf16 per row per step = 8 packed 32-bit columns
+                        mma_ts(tmem_base + kColO + x * kHeadDim, tmem_base + kColS + x * kBlockN + kk * 8, bd,
+                               idesc_pv, acc);
+                    } else {
+                        // A = P from smem, K-major 128B swizzle, two 64-key sub-tiles of 16 KiB
+                        const uint32_t pa = smem_base + Smem::p + x * 2 * kTileBytes + (kk >> 2) * kTileBytes +
+                                            (kk & 3) * 32;
+                        const uint64_t ad = make_smem_desc(pa, 16, 1024, kSwizzle128B);
+                        mma_ss(tmem_base + kColO + x * kHeadDim, ad, bd, idesc_pv, acc);
+                    }
+                }
+            };
+
+            mbar_wait(bar(kBarQFull), 0);
+            mbar_wait(bar(kBarKFull + 0), 0);
+            tc_fence_after();
+            issue_qk(0, 0);
+            tc_commit(bar(kBarSFull + 0));
+            if (has_b) {
+                issue_qk(1, 0);
+                tc_commit(bar(kBarSFull + 1));
+            }
+            tc_commit(bar(kBarKEmpty + 0));
+
+            for (int it = 0; it < num_live; ++it) {
+                const int st = it % kStages;
+                const uint32_t ph = (it / kStages) & 1;
+                const bool has_next = it + 1 < num_live;
+                const int st_n = (it + 1) % kStages;
+                const uint32_t ph_n = ((it + 1) / kStages) & 1;
+
+                mbar_wait(bar(kBarVFull + st), ph);
+                // ---- tile A ----
+                mbar_wait(bar(kBarPFull + 0), it & 1);
+                tc_fence_after();
+                issue_pv(0, st, it > 0);
+                if (has_next) {
+                    mbar_wait(bar(kBarKFull + st_n), ph_n);
+                    tc_fence_after();
+                    issue_qk(0, st_n);
+                    tc_commit(bar(kBarSFull + 0));
+                } else {
+                    tc_commit(bar(kBarOFull + 0));
+                }
+                // ---- tile B ----
+                if (has_b) {
+                    mbar_wait(bar(kBarPFull + 1), it & 1);
+                    tc_fence_after();
+                    issue_pv(1, st, it > 0);
+                }
+                tc_commit(bar(kBarVEmpty + st));
+                if (has_b) {
+                    if (has_next) {
+                        issue_qk(1, st_n);
+                        tc_commit(bar(kBarSFull + 1));
+                    } else {
+                        tc_commit(bar(kBarOFull + 1));
+                    }
+                }
+                if (has_next) tc_commit(bar(kBarKEmpty + st_n));
+            }
+        }
+    } else {
+        // =============================== softmax / epilogue ===============================
+        const int x = warp >> 2;            // 0 = tile A, 1 = tile B
+        const int r = threadIdx.x & 127;    // row inside the tile == TMEM lane
+        const int row = q0 + x * kBlockM + r;
+        const bool active = (x == 0) || has_b;
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint32_t t_s = tmem_base + lane_base + kColS + x * kBlockN;
+        const uint32_t t_o = tmem_base + lane_base + kColO + x * kHeadDim;
+        const int kv_end_eff = min(p.kv_end, p.S);
+        const int tile_r_lo = q0 + x * kBlockM;
+        const int tile_r_hi = tile_r_lo + kBlockM - 1;
+        const float c = p.scale_log2;
+
+        float m_ref = -CUDART_INF_F;
+        float l_run = 0.f;
+
+        if (active) {
+            int it = 0;
+            for (int n = n0; n < n1; ++n) {
+                if (!tile_live(p, b, n)) continue;
+                const int kv0 = n * kBlockN;
+                mbar_wait(bar(kBarSFull + x), it & 1);
+                tc_fence_after();
+
+                float s[kBlockN];
+                {
+                    uint32_t(&su)[kBlockN] = reinterpret_cast<uint32_t(&)[kBlockN]>(s);
+#pragma unroll
+                    for (int cb = 0; cb < kBlockN / 32; ++cb)
+                        tmem_ld32(t_s + cb * 32, reinterpret_cast<uint32_t(&)[32]>(su[cb * 32]));
+                    tc_wait_ld();
+                }
+                if (p.debug_scores != nullptr && it == 0) {
+                    const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+                    float* dst = p.debug_scores + ((cta * 2 + x) * kBlockM + r) * kBlockN;
+#pragma unroll
+                    for (int j = 0; j < kBlockN; ++j) dst[j] = s[j];
+                }
+
+                // tile class (warp-uniform): "full" tiles need no per-element predicate
+                uint8_t flag = kTileFull;
+                if (p.tile_flags != nullptr) flag = p.tile_flags[b * p.n_kv_tiles + n];
+                const bool full = flag == kTileFull && kv0 >= p.kv_begin && kv0 + kBlockN <= kv_end_eff &&
+                                  (p.wl < 0 || tile_r_hi - kv0 <= p.wl) &&
+                                  (p.wr < 0 || kv0 + kBlockN - 1 - tile_r_lo <= p.wr);
+
+                float tile_max;
+                float mul;
+                if (full) {
+                    float mx0 = s[0], mx1 = s[1];
+#pragma unroll
+                    for (int j = 2; j < kBlockN; j += 4) {
+                        mx0 = max3(mx0, s[j], s[j + 1]);
+                        if (j + 3 < kBlockN) mx1 = max3(mx1, s[j + 2], s[j + 3]);
+                    }
+                    tile_max = fmaxf(mx0, mx1) * c;  // scale > 0 (validated on the host)
+                    mul = c;
+                } else {
+                    // live columns of this row inside the tile: [lo, hi]
+                    int lo = p.kv_begin, hi = kv_end_eff - 1;
+                    if (p.wl >= 0) lo = max(lo, row - p.wl);
+                    if (p.wr >= 0) hi = min(hi, row + p.wr);
+                    lo -= kv0;
+                    hi -= kv0;
+                    const float* brow = (flag == kTileMixed && p.bias2 != nullptr)
+                                            ? p.bias2 + static_cast<size_t>(b) * p.bias_stride + kv0
+                                            : nullptr;
+                    float mx = -CUDART_INF_F;
+#pragma unroll
+                    for (int j4 = 0; j4 < kBlockN; j4 += 4) {
+                        float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (brow != nullptr) bb = __ldg(reinterpret_cast<const float4*>(brow + j4));
+                        const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = j4 + u;
+                            const float xs = fmaf(s[j], c, bv[u]);  // bias -inf => masked key
+                            s[j] = (j >= lo && j <= hi) ? xs : -CUDART_INF_F;
+                            mx = fmaxf(mx, s[j]);
+                        }
+                    }
+                    tile_max = mx;
+                    mul = 1.0f;
+                }
+
+                // lazy running max: move the reference only when it would grow by > 2^8
+                const float m_new = (tile_max > m_ref + kRescaleThreshold) ? tile_max : m_ref;
+                const float alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
+                const float neg_m = (m_new == -CUDART_INF_F) ? 0.f : -m_new;
+
+                float sum0 = 0.f, sum1 = 0.f;
+                if (kPTmem) {
+#pragma unroll
+                    for (int cb = 0; cb < kBlockN / 32; ++cb) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            const float p0 = ex2(fmaf(s[cb * 32 + 2 * u], mul, neg_m));
+                            const float p1 = ex2(fmaf(s[cb * 32 + 2 * u + 1], mul, neg_m));
+                            sum0 += p0;
+                            sum1 += p1;
+                            pk[u] = pack2<kBf16>(p0, p1);
+                        }
+                        tmem_st16(t_s + cb * 16, pk);
+                    }
+                } else {
+                    uint8_t* prow = smem_gen + Smem::p + x * 2 * kTileBytes + r * 128;
+#pragma unroll
+                    for (int ch = 0; ch < kBlockN / 8; ++ch) {  // 16-byte chunks of 8 keys
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const float p0 = ex2(fmaf(s[ch * 8 + 2 * u], mul, neg_m));
+                            const float p1 = ex2(fmaf(s[ch * 8 + 2 * u + 1], mul, neg_m));
+                            sum0 += p0;
+                            sum1 += p1;
+                            pk[u] = pack2<kBf16>(p0, p1);
+                        }
+                        uint8_t* dst = prow + (ch >> 3) * kTileBytes + (((ch & 7) ^ (r & 7)) << 4);
+                        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    }
+                }
+                l_run = l_run * alpha + (sum0 + sum1);
+                m_ref = m_new;
+
+                // O_X *= alpha for rows whose reference max moved (PV of the previous tile has
+                // completed: S_X(n) was committed after it on the in-order tensor pipe)
+                if (it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+#pragma unroll
+                    for (int hb = 0; hb < kHeadDim / 32; ++hb) {
+                        uint32_t o[32];
+                        tmem_ld32(t_o + hb * 32, o);
+                        tc_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * alpha);
+                        tmem_st32(t_o + hb * 32, o);
+                    }
+                }
+                if (kPTmem) {
+                    tc_wait_st();
+                } else {
+                    tc_wait_st();
+                    fence_proxy_async_smem();
+                }
+                tc_fence_before();
+                mbar_arrive(bar(kBarPFull + x));
+                ++it;
+            }
+
+            // ---------------- epilogue ----------------
+            float o[kHeadDim];
+            if (num_live > 0) {
+                mbar_wait(bar(kBarOFull + x), 0);
+                tc_fence_after();
+                uint32_t(&ou)[kHeadDim] = reinterpret_cast<uint32_t(&)[kHeadDim]>(o);
+#pragma unroll
+                for (int hb = 0; hb < kHeadDim / 32; ++hb)
+                    tmem_ld32(t_o + hb * 32, reinterpret_cast<uint32_t(&)[32]>(ou[hb * 32]));
+                tc_wait_ld();
+            } else {
+#pragma unroll
+                for (int u = 0; u < kHeadDim; ++u) o[u] = 0.f;
+            }
+            if (row < p.S) {
+                if (p.o_partial != nullptr) {
+                    const size_t ridx = (static_cast<size_t>(b) * p.H + h) * p.S + row;
+                    float4* dst = reinterpret_cast<float4*>(p.o_partial + ridx * kHeadDim);
+#pragma unroll
+                    for (int u = 0; u < kHeadDim / 4; ++u)
+                        dst[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+                    p.m_partial[ridx] = m_ref;
+                    p.l_partial[ridx] = l_run;
+                } else {
+                    const float inv = l_run > 0.f ? 1.0f / l_run : 0.f;
+                    const size_t off = static_cast<size_t>(b) * p.o_sb + static_cast<size_t>(h) * p.o_sh +
+                                       static_cast<size_t>(row) * p.o_ss;
+                    if (p.out_dtype == 2) {
+                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+#pragma unroll
+                        for (int u = 0; u < kHeadDim / 4; ++u)
+                            dst[u] = make_float4(o[4 * u] * inv, o[4 * u + 1] * inv, o[4 * u + 2] * inv,
+                                                 o[4 * u + 3] * inv);
+                    } else {
+                        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + off);
+#pragma unroll
+                        for (int u = 0; u < kHeadDim / 8; ++u) {
+                            uint32_t w[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float a0 = o[8 * u + 2 * e] * inv, a1 = o[8 * u + 2 * e + 1] * inv;
+                                w[e] = (p.out_dtype == 0) ? pack2<true>(a0, a1) : pack2<false>(a0, a1);
+                            }
+                            dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    // ---------------- teardown ----------------
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+}  // namespace
+
+size_t fa_fwd_sm100_smem_bytes(bool p_in_tmem) {
+    return (p_in_tmem ? Smem::bars_tmem : Smem::bars_ss) + Smem::bar_bytes + 1024;  // + alignment slack
+}
+
+cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
+                                const FaParams& p, bool bf16, bool p_in_tmem, cudaStream_t stream, int* grid_ctas) {
+    void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const FaParams) = nullptr;
+    if (bf16 && p_in_tmem) kern = fa_fwd_sm100_kernel<true, true>;
+    if (bf16 && !p_in_tmem) kern = fa_fwd_sm100_kernel<true, false>;
+    if (!bf16 && p_in_tmem) kern = fa_fwd_sm100_kernel<false, true>;
+    if (!bf16 && !p_in_tmem) kern = fa_fwd_sm100_kernel<false, false>;
+    const size_t smem = fa_fwd_sm100_smem_bytes(p_in_tmem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid((p.S + kRowsPerCta - 1) / kRowsPerCta, p.H, p.B);
+    if (grid_ctas) *grid_ctas = static_cast<int>(grid.x * grid.y * grid.z);
+    kern<<<grid, kThreads, smem, stream>>>(tmq, tmk, tmv, p);
+    return cudaGetLastError();
+}
+
+}  // namespace rf

@@ -1,0 +1,71 @@
+// fa_internal.h -- device-side parameter blocks and launcher prototypes shared by the
+// kernels (fa_fwd_sm100.cu, fa_fwd_simt.cu, fa_aux.cu) and the C-ABI layer (fa_api.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rf {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kMaskThreshold = -30000.0f;  // reference attention.hpp:16
+
+// Geometry of the tcgen05 kernel.
+constexpr int kBlockM = 128;                  // query rows per UMMA tile
+constexpr int kBlockN = 128;                  // keys per tile
+constexpr int kQTilesPerCta = 2;              // two query tiles ping-pong on one SM
+constexpr int kRowsPerCta = kBlockM * kQTilesPerCta;
+
+// Key-tile classes produced by bias_prepare_kernel (one byte per (batch, 128-key tile)).
+enum : uint8_t { kTileSkip = 0, kTileFull = 1, kTileMixed = 2 };
+
+struct FaParams {
+    int B, H, S;
+    int kv_begin, kv_end;  // key range [kv_begin, kv_end), 0 <= kv_begin <= kv_end <= S
+    int wl, wr;            // window, -1 = unbounded
+    float scale_log2;      // effective scale * log2(e)
+    // padding bias in the log2 domain: bias2[b*bias_stride + j] = pad_bias*log2e, -inf if masked
+    // or j >= S.  nullptr when the op has no pad_bias input.
+    const float* bias2;
+    const uint8_t* tile_flags;  // [B, n_kv_tiles], nullptr iff bias2 == nullptr
+    int bias_stride;            // n_kv_tiles * 128
+    int n_kv_tiles;             // ceil(S / 128)
+    // output
+    void* out;
+    long long o_sb, o_sh, o_ss;  // element strides
+    int out_dtype;               // rf_dtype
+    float* o_partial;            // split-KV partials, contiguous [B,H,S,d] / [B,H,S]
+    float* m_partial;
+    float* l_partial;
+    float* debug_scores;
+};
+
+struct SimtParams {
+    const void* q;
+    const void* k;
+    const void* v;
+    long long q_sb, q_sh, q_ss, k_sb, k_sh, k_ss, v_sb, v_sh, v_ss;
+    int in_dtype;
+    int d;
+    FaParams f;
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
+                                const FaParams& p, bool bf16, bool p_in_tmem, cudaStream_t stream, int* grid_ctas);
+size_t fa_fwd_sm100_smem_bytes(bool p_in_tmem);
+cudaError_t launch_fa_fwd_simt(const SimtParams& p, cudaStream_t stream, int* grid_ctas);
+
+cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias2, uint8_t* tile_flags,
+                                int n_kv_tiles, cudaStream_t stream);
+cudaError_t launch_merge(const float* const* o_parts, const float* const* m_parts, const float* const* l_parts,
+                         int G, long long rows, int d, void* out, int out_dtype, cudaStream_t stream);
+cudaError_t launch_rescale_partial(float* o_part, float* l_part, const float* m_part, const float* m_star,
+                                   long long rows, int d, cudaStream_t stream);
+cudaError_t launch_normalize(const float* o_sum, const float* l_sum, long long rows, int d, void* out,
+                             int out_dtype, cudaStream_t stream);
+cudaError_t launch_pad_bias_from_mask(const float* mask, float* bias, long long n, cudaStream_t stream);
+cudaError_t launch_cast_from_f32(const float* src, void* dst, long long n, int dst_dtype, cudaStream_t stream);
+cudaError_t launch_cast_to_f32(const void* src, float* dst, long long n, int src_dtype, cudaStream_t stream);
+
+}  // namespace rf
