@@ -414,6 +414,15 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
 
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    {
+        // keep freed staging buffers in the device's default pool so that steady-state calls do
+        // not go back to the driver for memory (idempotent; the pool belongs to the runtime)
+        cudaMemPool_t pool = nullptr;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess && pool != nullptr) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     cudaStream_t stream = nullptr;
     e = cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");

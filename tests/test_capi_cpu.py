@@ -1,0 +1,143 @@
+"""CPU tests of the drop-in boundary: the C-ABI library loads, exports every symbol
+include/rf_fa.h declares, validates like the reference, and fails loudly without a GPU."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2603_12646_b200 import capi
+    return capi.load()
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "rf_fa.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(rf_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2603_12646_b200 import capi
+    declared = header_functions()
+    assert len(declared) >= 18
+    assert sorted(capi.EXPORTS) == declared
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.rf_abi_version() == 1
+
+
+def test_params_init_layout_and_defaults(lib):
+    from paper_2603_12646_b200 import capi
+    p = capi.new_params()
+    assert (p.window_left, p.window_right, p.scale) == (-1, -1, 0.0)
+    assert (p.dtype, p.out_dtype, p.kernel, p.flags) == (capi.RF_DTYPE_BF16, capi.RF_DTYPE_BF16, capi.RF_KERNEL_AUTO, 0)
+    assert p.q is None and p.pad_bias is None and p.o_partial is None
+    assert list(p.q_stride) == [0, 0, 0]
+
+
+def test_validation_mirrors_reference_errors(lib):
+    from paper_2603_12646_b200 import capi
+    p = capi.new_params()
+    p.B, p.H, p.S, p.d = 1, 2, 16, 48
+    p.q = p.k = p.v = p.out = 0x1000
+    assert lib.rf_fa_validate(C.byref(p)) == capi.RF_ERR_HEAD_DIM
+    assert b"head_dim must be one of {32, 64, 128}, got 48" in lib.rf_last_error()  # rewrite.cpp:266-269
+    with pytest.raises(capi.UnsupportedHeadDim):
+        capi.check(capi.RF_ERR_HEAD_DIM)
+    p.d = 64
+    assert lib.rf_fa_validate(C.byref(p)) == capi.RF_OK
+    p.B = -1
+    assert lib.rf_fa_validate(C.byref(p)) == capi.RF_ERR_SHAPE
+    p.B = 1
+    p.kv_begin, p.kv_end = 8, 4
+    assert lib.rf_fa_validate(C.byref(p)) == capi.RF_ERR_ARG
+    p.kv_begin, p.kv_end = 0, 0
+    # forcing the tensor-core kernel onto a head dim it does not cover is an explicit error
+    p.d, p.kernel = 32, capi.RF_KERNEL_TCGEN05
+    assert lib.rf_fa_validate(C.byref(p)) == capi.RF_ERR_UNSUPPORTED
+    p.kernel = capi.RF_KERNEL_AUTO
+    st = capi.RfFaStats()
+    assert lib.rf_fa_stats_query(C.byref(p), C.byref(st)) == capi.RF_OK
+    assert st.kernel == capi.RF_KERNEL_SIMT and st.score_matrix_bytes == 0
+
+
+def test_workspace_is_linear_in_S(lib):
+    from paper_2603_12646_b200 import capi
+    sizes = {}
+    for S in (8192, 16384, 32768):
+        p = capi.new_params()
+        p.B, p.H, p.S, p.d = 1, 12, S, 64
+        p.q = p.k = p.v = p.out = 0x1000
+        p.pad_bias = 0x2000
+        n = C.c_size_t()
+        assert lib.rf_fa_fwd_workspace_bytes(C.byref(p), C.byref(n)) == capi.RF_OK
+        sizes[S] = n.value
+        st = capi.RfFaStats()
+        lib.rf_fa_stats_query(C.byref(p), C.byref(st))
+        assert st.kernel == capi.RF_KERNEL_TCGEN05 and st.grid_ctas == 12 * S // 256
+        assert st.row_state_bytes == 8 * S
+    assert sizes[16384] <= 2 * sizes[8192] + 512 and sizes[32768] <= 4 * sizes[8192] + 1024
+    assert sizes[32768] < 200 * 1024  # O(S): 4 B/key + 1 B/tile, nowhere near S^2
+    p.pad_bias = None
+    assert lib.rf_fa_fwd_workspace_bytes(C.byref(p), C.byref(n)) == capi.RF_OK and n.value == 0
+
+
+def test_host_entry_checks_in_reference_order(lib):
+    """tile, then pad_bias shape (attention.cpp:110-116) -- both before any CUDA call."""
+    import paper_2603_12646_b200 as P
+    z = np.zeros((1, 1, 4, 64), np.float32)
+    with pytest.raises(P.ShapeMismatch, match="tile must be >= 1"):
+        P.flash_attention(z, z, z, P.AttentionSpec(), tile=0)
+    with pytest.raises(P.ShapeMismatch, match=r"pad_bias must be \[B,1,1,S\]"):
+        P.flash_attention(z, z, z, P.AttentionSpec(pad_bias=np.zeros((1, 1, 1, 5), np.float32)))
+    with pytest.raises(P.ShapeMismatch, match="identical shapes"):
+        P.flash_attention(z, z, np.zeros((1, 1, 5, 64), np.float32))
+    with pytest.raises(P.ShapeMismatch, match=r"\[B,H,S,d\]"):
+        P.flash_attention(z[0], z[0], z[0])
+
+
+def test_no_cpu_fallback_without_gpu(lib):
+    import torch
+
+    import paper_2603_12646_b200 as P
+    from paper_2603_12646_b200 import capi
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    z = np.zeros((1, 1, 4, 64), np.float32)
+    with pytest.raises(capi.RfError) as ei:
+        P.flash_attention(z, z, z)
+    assert ei.value.code == capi.RF_ERR_CUDA
+    assert lib.rf_device_check(0, None, None, None) == capi.RF_ERR_CUDA
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2603_12646_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", src, flags=re.M), f
+                assert "librf_oracle" not in src and "libref_attn" not in src, f
+
+
+def test_memory_model_and_window_attrs():
+    import paper_2603_12646_b200 as P
+    assert P.mask_memory_bytes(1, 12, 8192, 2) == 1610612736
+    assert P.mask_memory_bytes(1, 12, 16384, 2) == 4 * 1610612736
+    assert P.fa_memory_bytes(1, 12, 8192, 64, 64, 2) == 12779520
+    assert P.local_window_attrs() == (63, 64)                           # rewrite.cpp:355-357
+    assert P.local_window_attrs(is_global=True) == (-1, -1)
+    assert P.local_window_attrs(P.RewriteOptions(local_window=2)) == (0, 1)
+    with pytest.raises(P.UnsupportedHeadDim):
+        P.local_window_attrs(P.RewriteOptions(head_dim=48))
+    with pytest.raises(ValueError):
+        P.local_window_attrs(P.RewriteOptions(local_window=3))
+    assert P.AttentionSpec().effective_scale(64) == 0.125               # attention.cpp:34-36
+    assert P.AttentionSpec(scale=0.5).effective_scale(64) == 0.5
+    assert (P.kMaskValue, P.kMaskThreshold) == (-65504.0, -30000.0)

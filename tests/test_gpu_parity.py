@@ -1,0 +1,361 @@
+"""GPU parity tests (run with -m gpu on a B200): the CUDA path, called through the C ABI
+(capi.py -> librf_fa.so), against the oracle on identical seeded inputs.
+
+Tolerance (BASELINE.json north_star): attention output max-abs error <= 2e-2 for the bf16
+kernel vs the f32-I/O / f64-math oracle, inputs rounded to bf16 on BOTH sides first.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2  # stated tolerance (see module docstring)
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2603_12646_b200 as pkg
+    return pkg
+
+
+def dev_tensors(torch, arrs, dtype=None):
+    dtype = dtype or torch.bfloat16
+    return [torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype) for a in arrs]
+
+
+def tail_pad(B, S, lens):
+    pb = np.zeros((B, 1, 1, S), np.float32)
+    for b, n in enumerate(lens):
+        pb[b, 0, 0, n:] = -65504.0
+    return pb
+
+
+def run_case(torch, P, O, q, k, v, scale, wl, wr, pb, kernel="auto", dtype=None, flags=0, expect_kernel=None):
+    tq, tk, tv = dev_tensors(torch, (q, k, v), dtype)
+    tpb = torch.from_numpy(pb).cuda() if pb is not None else None
+    st = P.FlashStats()
+    out = P.flash_attention(tq, tk, tv, P.AttentionSpec(scale, wl, wr, tpb), stats=st, kernel=kernel, flags=flags)
+    torch.cuda.synchronize()
+    if expect_kernel:
+        assert st.kernel == expect_kernel
+    want = O.flash_attention(q, k, v, scale, wl, wr, pb, threads=8)
+    got = out.float().cpu().numpy()
+    assert not np.isnan(got).any()
+    return float(np.abs(got - want).max()), got, want
+
+
+# ------------------------------------------------------------------ BASELINE config 1
+@pytest.mark.parametrize("variant", ["global", "pad475", "pad300", "local", "local_pad", "scale_eighth"])
+def test_config1_op_parity(torch_mod, P, oracle, variant):
+    """configs[0]: ModernBERT-base attention op, 12 heads, d 64, B 1, S 512; seed 11 in q,k,v order
+    like bench_attention.cpp:16-23."""
+    B, H, S, d = 1, 12, 512, 64
+    q, k, v = [oracle.round_bf16(t) for t in oracle.random_tensors(11, (B, H, S, d), 3)]
+    wl, wr, pb, scale = -1, -1, None, 0.0
+    if variant == "pad475":
+        pb = tail_pad(B, S, [475])
+    elif variant == "pad300":
+        pb = tail_pad(B, S, [300])
+    elif variant == "local":
+        wl, wr = 63, 64
+    elif variant == "local_pad":
+        wl, wr, pb = 63, 64, tail_pad(B, S, [475])
+    elif variant == "scale_eighth":
+        scale = 0.125
+    err, _, _ = run_case(torch_mod, P, oracle, q, k, v, scale, wl, wr, pb, expect_kernel="tcgen05")
+    assert err <= TOL
+
+
+def test_golden_fixtures_on_device(torch_mod, P, oracle, golden):
+    """Committed reference outputs (tests/golden/make_golden.py) reproduced by the kernel."""
+    torch = torch_mod
+    q, k, v = [oracle.round_bf16(t) for t in oracle.random_tensors(11, (1, 2, 512, 64), 3)]
+    tq, tk, tv = dev_tensors(torch, (q, k, v))
+    pb = tail_pad(1, 512, [475])
+    tpb = torch.from_numpy(pb).cuda()
+    for name, spec in (("cfg1_global_bf16in", P.AttentionSpec()),
+                       ("cfg1_global_pad475_bf16in", P.AttentionSpec(pad_bias=tpb)),
+                       ("cfg1_local_pad475_bf16in", P.AttentionSpec(0.0, 63, 64, tpb))):
+        got = P.flash_attention(tq, tk, tv, spec).float().cpu().numpy()
+        assert np.abs(got - golden[name]).max() <= TOL, name
+    # d = 32 fixture of Rewrite.SemanticPreservationSingleLayer (rewrite_test.cpp:239-263): generic kernel
+    hidden = oracle.random_tensors(7, (1, 2, 96, 32), 1)[0]
+    th = dev_tensors(torch, (hidden,))[0]
+    tpb = torch.from_numpy(golden["rewrite_pad_bias"]).cuda()
+    st = P.FlashStats()
+    got = P.flash_attention(th, th, th, P.AttentionSpec(1 / np.sqrt(32.0), 63, 64, tpb), stats=st).float().cpu().numpy()
+    assert st.kernel == "simt"
+    assert np.abs(got - golden["rewrite_local_S96_d32"]).max() <= TOL
+    # bench_attention.cpp configs (unrounded f32 inputs on the reference side)
+    for S in (128, 512):
+        q, k, v = oracle.random_tensors(11, (1, 2, S, 64), 3)
+        tq, tk, tv = dev_tensors(torch, (q, k, v))
+        got = P.flash_attention(tq, tk, tv, P.AttentionSpec(0.125)).float().cpu().numpy()
+        assert np.abs(got - golden[f"bench_global_S{S}"]).max() <= TOL
+    got = P.flash_attention(tq, tk, tv, P.AttentionSpec(0.125, 63, 64)).float().cpu().numpy()
+    assert np.abs(got - golden["bench_local_S512"]).max() <= TOL
+
+
+# ------------------------------------------------------------------ the reference's grid
+@pytest.mark.parametrize("d,kernel", [(64, "tcgen05"), (64, "simt"), (32, "simt"), (128, "simt")])
+def test_small_grid(torch_mod, P, oracle, d, kernel):
+    """SPEC.md:540 grid: S in {1..8,37,100,512,1000} x windows x random padding."""
+    rng = np.random.default_rng(d)
+    worst = 0.0
+    for S in list(range(1, 9)) + [37, 100, 512, 1000]:
+        H = 1 if S >= 512 else 2
+        q, k, v = [oracle.round_bf16(rng.uniform(-1, 1, (2, H, S, d)).astype(np.float32)) for _ in range(3)]
+        pb = np.where(rng.uniform(size=(2, 1, 1, S)) < 0.25, -65504.0, 0.0).astype(np.float32)
+        for (wl, wr) in ((-1, -1), (0, 0), (1, 2), (63, 64)):
+            err, _, _ = run_case(torch_mod, P, oracle, q, k, v, 0.0, wl, wr, pb, kernel=kernel, expect_kernel=kernel)
+            worst = max(worst, err)
+            assert err <= TOL, (S, wl, wr, err)
+    print("worst max-abs", worst)
+
+
+def test_edge_cases(torch_mod, P, oracle):
+    torch = torch_mod
+    rng = np.random.default_rng(5)
+    # additive (non-masking) bias values + a fully masked batch row -> zeros (attention.cpp:169,175,204-207)
+    q, k, v = [oracle.round_bf16(rng.uniform(-1, 1, (2, 3, 200, 64)).astype(np.float32)) for _ in range(3)]
+    pb = np.zeros((2, 1, 1, 200), np.float32)
+    pb[0, 0, 0, :] = np.linspace(-3, 2, 200, dtype=np.float32)
+    pb[0, 0, 0, 50:60] = -65504.0
+    pb[1] = -65504.0
+    for kernel in ("tcgen05", "simt"):
+        err, got, _ = run_case(torch, P, oracle, q, k, v, 0.3, -1, 5, pb, kernel=kernel)
+        assert err <= TOL
+        assert np.all(got[1] == 0.0)
+    # one-sided windows, window larger than S, padding in the middle of the window
+    for (wl, wr) in ((-1, 0), (0, -1), (5, -1), (1000, 1000), (130, 1)):
+        err, _, _ = run_case(torch, P, oracle, q, k, v, 0.0, wl, wr, None, kernel="tcgen05")
+        assert err <= TOL, (wl, wr)
+    # f16 inputs
+    q16 = q.astype(np.float16).astype(np.float32)
+    k16 = k.astype(np.float16).astype(np.float32)
+    v16 = v.astype(np.float16).astype(np.float32)
+    err, _, _ = run_case(torch, P, oracle, q16, k16, v16, 0.0, 63, 64, None, kernel="tcgen05", dtype=torch.float16)
+    assert err <= TOL
+    # P staged through shared memory (SS variant) gives the same answer
+    err, _, _ = run_case(torch, P, oracle, q, k, v, 0.0, -1, -1, pb, kernel="tcgen05", flags=1)
+    assert err <= TOL
+    # empty tensors are a no-op
+    e = torch.empty((0, 2, 16, 64), device="cuda", dtype=torch.bfloat16)
+    assert P.flash_attention(e, e, e).shape == (0, 2, 16, 64)
+    e = torch.empty((1, 2, 0, 64), device="cuda", dtype=torch.bfloat16)
+    assert P.flash_attention(e, e, e).shape == (1, 2, 0, 64)
+    # negative scale: valid in the reference, served by the generic kernel
+    err, _, _ = run_case(torch, P, oracle, q, k, v, -0.2, -1, -1, None, expect_kernel="simt")
+    assert err <= TOL
+
+
+def test_layout_glue_strided_views(torch_mod, P, oracle):
+    """[B,S,H,d] and packed [B,S,3,H,d] QKV views are consumed in place; O can be [B,S,H*d]."""
+    torch = torch_mod
+    rng = np.random.default_rng(2)
+    B, S, H, d = 2, 333, 4, 64
+    qkv = oracle.round_bf16(rng.uniform(-1, 1, (B, S, 3, H, d)).astype(np.float32))
+    t = torch.from_numpy(qkv).to("cuda", torch.bfloat16)
+    tq, tk, tv = [t[:, :, i].permute(0, 2, 1, 3) for i in range(3)]  # [B,H,S,d] views, no copy
+    assert not tq.is_contiguous()
+    out_bshd = torch.empty((B, S, H * d), device="cuda", dtype=torch.bfloat16)
+    out_view = out_bshd.view(B, S, H, d).permute(0, 2, 1, 3)
+    st = P.FlashStats()
+    P.flash_attention(tq, tk, tv, P.AttentionSpec(0.0, 63, 64), out=out_view, stats=st)
+    torch.cuda.synchronize()
+    assert st.kernel == "tcgen05"
+    q, k, v = [np.ascontiguousarray(qkv[:, :, i].transpose(0, 2, 1, 3)) for i in range(3)]
+    want = oracle.flash_attention(q, k, v, 0.0, 63, 64, threads=8)
+    got = out_bshd.view(B, S, H, d).permute(0, 2, 1, 3).float().cpu().numpy()
+    assert np.abs(got - want).max() <= TOL
+    # f32 output
+    out32 = P.flash_attention(tq, tk, tv, P.AttentionSpec(0.0, 63, 64), out_dtype=torch.float32)
+    assert out32.dtype == torch.float32 and np.abs(out32.cpu().numpy() - want).max() <= TOL
+
+
+def test_error_behaviour_on_device(torch_mod, P):
+    torch = torch_mod
+    z = torch.zeros((1, 2, 16, 64), device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(P.ShapeMismatch, match="identical shapes"):
+        P.flash_attention(z, z, z[:, :1])
+    with pytest.raises(P.ShapeMismatch, match=r"pad_bias must be \[B,1,1,S\]"):
+        P.flash_attention(z, z, z, P.AttentionSpec(pad_bias=torch.zeros((1, 1, 1, 15), device="cuda")))
+    with pytest.raises(P.ShapeMismatch, match="tile"):
+        P.flash_attention(z, z, z, tile=0)
+    z48 = torch.zeros((1, 2, 16, 48), device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(P.UnsupportedHeadDim):
+        P.flash_attention(z48, z48, z48)
+
+
+def test_host_entry_point_and_fused_op(torch_mod, P, oracle):
+    """rf_fa_fwd_host / rf_fused_flash_attention_op: the reference's own calling convention
+    (host f32 tensors in, host f32 tensor out; interpreter.cpp:308-318 attr defaults)."""
+    from paper_2603_12646_b200 import capi
+    rng = np.random.default_rng(8)
+    B, H, S, d = 1, 2, 96, 64
+    q, k, v = [rng.uniform(-1, 1, (B, H, S, d)).astype(np.float32) for _ in range(3)]
+    mask = np.ones((B, 1, 1, S), np.float32)
+    mask[..., -7:] = 0
+    pb = oracle.pad_bias_from_mask(mask)
+    st = P.FlashStats()
+    got = P.flash_attention(q, k, v, P.AttentionSpec(0.0, 63, 64, pb), stats=st)
+    want = oracle.flash_attention(q, k, v, 0.0, 63, 64, pb)
+    assert got.dtype == np.float32 and np.abs(got - want).max() <= TOL
+    assert (st.tile_scratch_floats, st.row_state_floats, st.output_floats) == (64, 2 * S, B * H * S * d)
+    # the graph op with attrs absent -> scale 0.0 (1/sqrt(d)), windows -1
+    lib = capi.load()
+    f32p = C.POINTER(C.c_float)
+    ins = (f32p * 4)(*[a.ctypes.data_as(f32p) for a in (q, k, v, pb)])
+    dims = [(C.c_int64 * 4)(*a.shape) for a in (q, k, v, pb)]
+    dimp = (C.POINTER(C.c_int64) * 4)(*[C.cast(x, C.POINTER(C.c_int64)) for x in dims])
+    ranks = (C.c_int32 * 4)(4, 4, 4, 4)
+    out = np.empty_like(q)
+    rc = lib.rf_fused_flash_attention_op(ins, dimp, ranks, 4, 0, 0.0, 0, 0, 0, 0, out.ctypes.data_as(f32p), 0)
+    assert rc == 0, lib.rf_last_error()
+    assert np.abs(out - oracle.flash_attention(q, k, v, 0.0, -1, -1, pb)).max() <= TOL
+    rc = lib.rf_fused_flash_attention_op(ins, dimp, ranks, 3, 1, 0.125, 1, 63, 1, 64, out.ctypes.data_as(f32p), 0)
+    assert rc == 0
+    assert np.abs(out - oracle.flash_attention(q, k, v, 0.125, 63, 64)).max() <= TOL
+    bad = (C.c_int32 * 4)(4, 3, 4, 4)
+    assert lib.rf_fused_flash_attention_op(ins, dimp, bad, 3, 0, 0.0, 0, 0, 0, 0, out.ctypes.data_as(f32p), 0) == capi.RF_ERR_SHAPE
+    assert b"attention inputs must be [B,H,S,d]" in lib.rf_last_error()
+
+
+def test_pad_bias_chain_bit_exact(torch_mod, P, oracle):
+    """Cast_f16(-65504*(1-mask)) on device == the reference chain, bit for bit (integer-exact work)."""
+    torch = torch_mod
+    rng = np.random.default_rng(1)
+    mask = (rng.uniform(size=(3, 1, 1, 1000)) < 0.8).astype(np.float32)
+    mask[0, 0, 0, :5] = [0.5, 0.25, 0.999, 1e-3, 2.0]  # non-binary masks go through the same arithmetic
+    got = P.pad_bias_from_mask(torch.from_numpy(mask).cuda()).cpu().numpy()
+    want = oracle.pad_bias_from_mask(mask)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+# ------------------------------------------------------------------ split-KV (config 4 algebra)
+@pytest.mark.parametrize("kernel", ["tcgen05", "simt"])
+def test_split_kv_merge_equals_single_pass(torch_mod, P, oracle, kernel):
+    torch = torch_mod
+    from paper_2603_12646_b200 import capi
+    lib = capi.load()
+    rng = np.random.default_rng(4)
+    B, H, S, d = 1, 3, 1000, 64
+    q, k, v = [oracle.round_bf16(rng.uniform(-1, 1, (B, H, S, d)).astype(np.float32)) for _ in range(3)]
+    pb = tail_pad(B, S, [900])
+    pb[0, 0, 0, 100:228] = -65504.0  # one whole 128-key tile masked
+    tq, tk, tv = dev_tensors(torch, (q, k, v))
+    tpb = torch.from_numpy(pb).cuda()
+    for (wl, wr) in ((-1, -1), (63, 64)):
+        spec = P.AttentionSpec(0.0, wl, wr, tpb)
+        whole = P.flash_attention(tq, tk, tv, spec, kernel=kernel, out_dtype=torch.float32)
+        for G in (2, 4, 7):
+            bounds = [S * g // G for g in range(G + 1)]
+            parts = []
+            for g in range(G):
+                o = torch.full((B, H, S, d), float("nan"), device="cuda")
+                m = torch.full((B, H, S), float("nan"), device="cuda")
+                l = torch.full((B, H, S), float("nan"), device="cuda")
+                P.flash_attention(tq, tk, tv, spec, kernel=kernel, kv_range=(bounds[g], bounds[g + 1]), partials=(o, m, l))
+                parts.append((o, m, l))
+            vp = C.c_void_p
+            op = (vp * G)(*[p[0].data_ptr() for p in parts])
+            mp = (vp * G)(*[p[1].data_ptr() for p in parts])
+            lp = (vp * G)(*[p[2].data_ptr() for p in parts])
+            merged = torch.empty((B, H, S, d), device="cuda")
+            capi.check(lib.rf_fa_merge(op, mp, lp, G, B * H * S, d, merged.data_ptr(), capi.RF_DTYPE_F32, None))
+            torch.cuda.synchronize()
+            assert not torch.isnan(merged).any()
+            assert (merged - whole).abs().max().item() <= 5e-3, (wl, G)
+            # NCCL-shaped variant: all-reduce(max) m -> rescale -> sum -> normalize
+            mstar = torch.stack([p[1] for p in parts]).amax(0).contiguous()
+            osum = torch.zeros((B, H, S, d), device="cuda")
+            lsum = torch.zeros((B, H, S), device="cuda")
+            for (o, m, l) in parts:
+                o2, l2 = o.clone(), l.clone()
+                capi.check(lib.rf_fa_rescale_partial(o2.data_ptr(), l2.data_ptr(), m.data_ptr(), mstar.data_ptr(),
+                                                     B * H * S, d, None))
+                osum += o2
+                lsum += l2
+            out2 = torch.empty((B, H, S, d), device="cuda")
+            capi.check(lib.rf_fa_normalize(osum.data_ptr(), lsum.data_ptr(), B * H * S, d, out2.data_ptr(),
+                                           capi.RF_DTYPE_F32, None))
+            torch.cuda.synchronize()
+            assert (out2 - whole).abs().max().item() <= 5e-3
+        want = oracle.flash_attention(q, k, v, 0.0, wl, wr, pb, threads=8)
+        assert np.abs(whole.cpu().numpy() - want).max() <= TOL
+
+
+# ------------------------------------------------------------------ full-size properties (S = 8192+)
+def test_full_size_properties_8k(torch_mod, P, oracle):
+    """BASELINE configs[1] attention shape (B=1,H=12,S=8192,d=64): size-independent properties."""
+    torch = torch_mod
+    B, H, S, d = 1, 12, 8192, 64
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = [(torch.rand((B, H, S, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+    lens = [7000]
+    pb = torch.from_numpy(tail_pad(B, S, lens)).cuda()
+    for (wl, wr) in ((-1, -1), (63, 64)):
+        spec = P.AttentionSpec(0.0, wl, wr, pb)
+        st = P.FlashStats()
+        o1 = P.flash_attention(q, k, v, spec, stats=st, out_dtype=torch.float32)
+        assert st.kernel == "tcgen05" and st.score_matrix_bytes == 0 and st.workspace_bytes < 64 * 1024
+        # determinism: bit-identical across runs (attention.hpp:43)
+        o2 = P.flash_attention(q, k, v, spec, out_dtype=torch.float32)
+        assert torch.equal(o1, o2)
+        # softmax rows sum to one: V = 1 -> O = 1 on every row (all rows have a live key here)
+        ones = torch.ones_like(v)
+        o_ones = P.flash_attention(q, k, ones, spec, out_dtype=torch.float32)
+        assert (o_ones - 1.0).abs().max().item() <= 1e-2
+        # linearity in V
+        v2 = (torch.rand((B, H, S, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+        o_v2 = P.flash_attention(q, k, v2, spec, out_dtype=torch.float32)
+        o_sum = P.flash_attention(q, k, (v.float() + v2.float()).to(torch.bfloat16), spec, out_dtype=torch.float32)
+        assert (o_sum - (o1 + o_v2)).abs().max().item() <= 3e-2
+        # independent kernel family on the same inputs
+        o_simt = P.flash_attention(q, k, v, spec, kernel="simt", out_dtype=torch.float32)
+        assert (o1 - o_simt).abs().max().item() <= TOL
+        # padded keys carry no weight: changing V there changes nothing
+        v3 = v.clone()
+        v3[:, :, lens[0]:] = 7.0
+        assert torch.equal(P.flash_attention(q, k, v3, spec, out_dtype=torch.float32), o1)
+    # global attention is invariant to a permutation of the live keys
+    perm = torch.randperm(lens[0], device="cuda", generator=g)
+    idx = torch.cat([perm, torch.arange(lens[0], S, device="cuda")])
+    spec = P.AttentionSpec(pad_bias=pb)
+    a = P.flash_attention(q, k, v, spec, out_dtype=torch.float32)
+    b = P.flash_attention(q, k[:, :, idx].contiguous(), v[:, :, idx].contiguous(), spec, out_dtype=torch.float32)
+    assert (a - b).abs().max().item() <= 1e-2
+    # one head against the oracle at full length (about 8 s of CPU)
+    qn, kn, vn = [t[:, :1].float().cpu().numpy() for t in (q, k, v)]
+    want = oracle.flash_attention(qn, kn, vn, 0.0, -1, -1, tail_pad(1, S, lens))
+    assert np.abs(a[:, :1].cpu().numpy() - want).max() <= TOL
+
+
+def test_long_sequences_o_n_memory(torch_mod, P):
+    """S = 32768 runs in O(S) extra memory: workspace + outputs only (no S x S buffer)."""
+    torch = torch_mod
+    B, H, S, d = 1, 12, 32768, 64
+    q = (torch.rand((B, H, S, d), device="cuda") * 2 - 1).to(torch.bfloat16)
+    pb = torch.zeros((B, 1, 1, S), device="cuda")
+    pb[..., 30000:] = -65504.0
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    st = P.FlashStats()
+    out = P.flash_attention(q, q, q, P.AttentionSpec(pad_bias=pb), stats=st)
+    torch.cuda.synchronize()
+    extra = torch.cuda.max_memory_allocated() - base
+    assert extra <= out.numel() * 2 + (1 << 20)  # output + < 1 MiB workspace
+    assert st.workspace_bytes <= 4 * S + 4096
+    assert P.mask_memory_bytes(B, H, S, 2) == 25769803776  # what SDPA would have needed (24 GiB)
+    o_ones = P.flash_attention(q, q, torch.ones_like(q), P.AttentionSpec(pad_bias=pb), out_dtype=torch.float32)
+    assert (o_ones - 1.0).abs().max().item() <= 1e-2
