@@ -56,10 +56,6 @@ typedef enum rf_dtype { RF_DTYPE_BF16 = 0, RF_DTYPE_F16 = 1, RF_DTYPE_F32 = 2 } 
 /* Which kernel family runs.  AUTO picks tcgen05 whenever the shape allows (head_dim 64);
  * SIMT is the generic sm_100a kernel (any head_dim in {32,64,128}), also used as an
  * on-device cross-check in tests.  Neither is a CPU path. */
-/* flags: stage P through shared memory (tcgen05.mma SS) instead of TMEM (TS).  Both variants
- * are tensor-core paths with identical results; TMEM is the default. */
-#define RF_FA_FLAG_P_SMEM 1
-
 typedef enum rf_kernel { RF_KERNEL_AUTO = 0, RF_KERNEL_TCGEN05 = 1, RF_KERNEL_SIMT = 2 } rf_kernel;
 
 /*
@@ -101,7 +97,7 @@ typedef struct rf_fa_params {
     int32_t dtype;     /* rf_dtype of Q/K/V: BF16 or F16 */
     int32_t out_dtype; /* rf_dtype of O */
     int32_t kernel;    /* rf_kernel */
-    int32_t flags;     /* RF_FA_FLAG_* */
+    int32_t flags;     /* reserved, must be 0 */
     int64_t kv_begin; /* split-KV key range; both 0 => [0,S) */
     int64_t kv_end;
     float* o_partial;

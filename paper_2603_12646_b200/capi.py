@@ -13,7 +13,6 @@ from . import _build
 RF_OK, RF_ERR_SHAPE, RF_ERR_HEAD_DIM, RF_ERR_ARG, RF_ERR_CUDA, RF_ERR_WORKSPACE, RF_ERR_UNSUPPORTED = range(7)
 RF_DTYPE_BF16, RF_DTYPE_F16, RF_DTYPE_F32 = 0, 1, 2
 RF_KERNEL_AUTO, RF_KERNEL_TCGEN05, RF_KERNEL_SIMT = 0, 1, 2
-RF_FA_FLAG_P_SMEM = 1
 
 # every symbol include/rf_fa.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [

@@ -234,9 +234,8 @@ int rf_fa_stats_query(const rf_fa_params* p, rf_fa_stats* st) {
     std::memset(st, 0, sizeof(*st));
     st->kernel = kernel;
     st->workspace_bytes = workspace_bytes_for(p, kernel);
-    const bool p_tmem = !(p->flags & RF_FA_FLAG_P_SMEM);
     st->tile_scratch_bytes = kernel == RF_KERNEL_TCGEN05
-                                 ? rf::fa_fwd_sm100_smem_bytes(p_tmem) + 512ull * 128 * 4  // smem + TMEM
+                                 ? rf::fa_fwd_sm100_smem_bytes() + 512ull * 128 * 4  // smem + TMEM
                                  : (2ull * 32 * p->d + 32) * sizeof(float);
     st->row_state_bytes = 2ull * sizeof(float) * static_cast<uint64_t>(p->S);
     const uint64_t esz = p->out_dtype == RF_DTYPE_F32 ? 4 : 2;
@@ -298,8 +297,7 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
-    const bool p_tmem = !(p->flags & RF_FA_FLAG_P_SMEM);
-    cudaError_t e = rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, p_tmem, stream, &grid);
+    cudaError_t e = rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, stream, &grid);
     if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100 launch");
     return RF_OK;
 }

@@ -9,8 +9,10 @@
 //               (cp.async.bulk.tensor, 128B swizzle, mbarrier complete_tx)
 //   warp 9      UMMA issuer (one elected lane): S_X = Q_X K^T  (tcgen05.mma SS, M128 N128 K16 x4)
 //                                               O_X += P_X V   (tcgen05.mma TS, M128 N64  K16 x8)
-//               accumulators in TMEM: S_A cols [0,128) S_B [128,256) O_A [256,320) O_B [320,384);
-//               P_X (bf16) aliases the first 64 columns of S_X.
+//               accumulators in TMEM: three rotating S buffers, cols [0,384) (tile g = 2*it + X of
+//               the A,B,A,B,... sequence uses buffer g % 3, so the next S of a warpgroup is computed
+//               while it is still busy with the current one), O_A [384,448), O_B [448,512);
+//               P (bf16) aliases the first 64 columns of its S buffer.
 //   warps 0-3   softmax for tile A, warps 4-7 for tile B: one thread owns one query row
 //               (tcgen05.ld 32x32b), so row max / row sum need no shuffles; exp2 with the scale
 //               folded in; lazy rescale of O (only when the running max grows by > 2^8).
@@ -33,37 +35,37 @@ namespace {
 using namespace rfptx;
 
 constexpr int kHeadDim = 64;
-constexpr int kStages = 3;                          // ring depth for K and for V
+constexpr int kStagesK = 4;                         // K ring depth (K runs two tiles ahead of V)
+constexpr int kStagesV = 3;                         // V ring depth
+constexpr int kSBufs = 3;                           // rotating S/P accumulators in TMEM
 constexpr int kTileBytes = kBlockN * kHeadDim * 2;  // 16 KiB: one 128 x 64 16-bit tile
 constexpr int kNumSoftmaxWarps = 8;
 constexpr int kProducerWarp = 8;
 constexpr int kMmaWarp = 9;
 constexpr int kThreads = 320;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColS = 0;    // + 128 * X
-constexpr uint32_t kColO = 256;  // + 64 * X
+constexpr uint32_t kColS = 0;    // + 128 * buffer
+constexpr uint32_t kColO = 384;  // + 64 * X
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P <= 2^8 before a rescale is forced
 
 // dynamic shared memory map (offsets from a 1024B-aligned base)
 struct Smem {
     static constexpr uint32_t q = 0;                                   // 2 tiles
-    static constexpr uint32_t k = q + 2 * kTileBytes;                  // kStages tiles
-    static constexpr uint32_t v = k + kStages * kTileBytes;            // kStages tiles
-    static constexpr uint32_t p = v + kStages * kTileBytes;            // SS mode only: 2 x 32 KiB
-    static constexpr uint32_t bars_tmem = p;                           // barrier block (TS mode)
-    static constexpr uint32_t bars_ss = p + 2 * 2 * kTileBytes;        // barrier block (SS mode)
+    static constexpr uint32_t k = q + 2 * kTileBytes;                  // kStagesK tiles
+    static constexpr uint32_t v = k + kStagesK * kTileBytes;           // kStagesV tiles
+    static constexpr uint32_t bars = v + kStagesV * kTileBytes;        // barrier block
     static constexpr uint32_t bar_bytes = 256;
 };
 // barrier indices inside the barrier block (8 bytes each)
 enum : uint32_t {
     kBarQFull = 0,
-    kBarKFull = 1,                      // [kStages]
-    kBarKEmpty = kBarKFull + kStages,   // [kStages]
-    kBarVFull = kBarKEmpty + kStages,   // [kStages]
-    kBarVEmpty = kBarVFull + kStages,   // [kStages]
-    kBarSFull = kBarVEmpty + kStages,   // [2]
-    kBarPFull = kBarSFull + 2,          // [2]
-    kBarOFull = kBarPFull + 2,          // [2]
+    kBarKFull = 1,                       // [kStagesK]
+    kBarKEmpty = kBarKFull + kStagesK,   // [kStagesK]
+    kBarVFull = kBarKEmpty + kStagesK,   // [kStagesV]
+    kBarVEmpty = kBarVFull + kStagesV,   // [kStagesV]
+    kBarSFull = kBarVEmpty + kStagesV,   // [kSBufs] one per S buffer: no phase can be skipped
+    kBarPFull = kBarSFull + kSBufs,      // [kSBufs]
+    kBarOFull = kBarPFull + kSBufs,      // [2]
     kNumBars = kBarOFull + 2,
 };
 static_assert(kNumBars * 8 + 8 <= Smem::bar_bytes, "barrier block too small");
@@ -72,17 +74,17 @@ __device__ __forceinline__ bool tile_live(const FaParams& p, int b, int n) {
     return p.tile_flags == nullptr || p.tile_flags[b * p.n_kv_tiles + n] != kTileSkip;
 }
 
-template <bool kBf16, bool kPTmem>
+template <bool kBf16>
 __global__ void __launch_bounds__(kThreads, 1)
 fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const FaParams p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
-    const uint32_t bars = smem_base + (kPTmem ? Smem::bars_tmem : Smem::bars_ss);
+    const uint32_t bars = smem_base + Smem::bars;
     auto bar = [&](uint32_t i) { return bars + 8u * i; };
     volatile uint32_t* tmem_slot =
-        reinterpret_cast<volatile uint32_t*>(smem_gen + (kPTmem ? Smem::bars_tmem : Smem::bars_ss) + 8 * kNumBars);
+        reinterpret_cast<volatile uint32_t*>(smem_gen + Smem::bars + 8 * kNumBars);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -107,17 +109,19 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         prefetch_tensormap(&tm_k);
         prefetch_tensormap(&tm_v);
         mbar_init(bar(kBarQFull), 1);
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kStagesK; ++s) {
             mbar_init(bar(kBarKFull + s), 1);
             mbar_init(bar(kBarKEmpty + s), 1);
+        }
+        for (int s = 0; s < kStagesV; ++s) {
             mbar_init(bar(kBarVFull + s), 1);
             mbar_init(bar(kBarVEmpty + s), 1);
         }
-        for (int x = 0; x < 2; ++x) {
-            mbar_init(bar(kBarSFull + x), 1);
-            mbar_init(bar(kBarPFull + x), kBlockM);
-            mbar_init(bar(kBarOFull + x), 1);
+        for (int s = 0; s < kSBufs; ++s) {
+            mbar_init(bar(kBarSFull + s), 1);
+            mbar_init(bar(kBarPFull + s), kBlockM);
         }
+        for (int x = 0; x < 2; ++x) mbar_init(bar(kBarOFull + x), 1);
         fence_barrier_init();
     }
     if (warp == kMmaWarp) {
@@ -135,18 +139,37 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             mbar_arrive_expect_tx(bar(kBarQFull), has_b ? 2 * kTileBytes : kTileBytes);
             tma_load_4d(smem_base + Smem::q, &tm_q, bar(kBarQFull), 0, q0, h, b);
             if (has_b) tma_load_4d(smem_base + Smem::q + kTileBytes, &tm_q, bar(kBarQFull), 0, q0 + kBlockM, h, b);
-            int it = 0;
-            for (int n = n0; n < n1; ++n) {
-                if (!tile_live(p, b, n)) continue;
-                const int st = it % kStages;
-                const uint32_t ph = (it / kStages) & 1;
+            // K runs two tiles ahead of V: QK^T of tile it+2 is issued while tile it is in softmax
+            auto load_k = [&](int it, int n) {
+                const int st = it % kStagesK;
+                const uint32_t ph = (it / kStagesK) & 1;
                 mbar_wait(bar(kBarKEmpty + st), ph ^ 1);
                 mbar_arrive_expect_tx(bar(kBarKFull + st), kTileBytes);
                 tma_load_4d(smem_base + Smem::k + st * kTileBytes, &tm_k, bar(kBarKFull + st), 0, n * kBlockN, h, b);
+            };
+            auto load_v = [&](int it, int n) {
+                const int st = it % kStagesV;
+                const uint32_t ph = (it / kStagesV) & 1;
                 mbar_wait(bar(kBarVEmpty + st), ph ^ 1);
                 mbar_arrive_expect_tx(bar(kBarVFull + st), kTileBytes);
                 tma_load_4d(smem_base + Smem::v + st * kTileBytes, &tm_v, bar(kBarVFull + st), 0, n * kBlockN, h, b);
-                ++it;
+            };
+            auto next_live = [&](int n) {
+                while (n < n1 && !tile_live(p, b, n)) ++n;
+                return n;
+            };
+            int nk = next_live(n0), itk = 0;  // K cursor
+            for (int pre = 0; pre < 2 && nk < n1; ++pre) {
+                load_k(itk++, nk);
+                nk = next_live(nk + 1);
+            }
+            int itv = 0;
+            for (int n = next_live(n0); n < n1; n = next_live(n + 1)) {
+                if (nk < n1) {
+                    load_k(itk++, nk);
+                    nk = next_live(nk + 1);
+                }
+                load_v(itv++, n);
             }
         }
     } else if (warp == kMmaWarp) {
@@ -158,85 +181,81 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 
             // S_X = Q_X * K^T : both operands K-major (head dim contiguous), 128B swizzle,
             // 8-row core-matrix groups 1024 B apart; a K=16 step advances 32 B inside the atom.
-            auto issue_qk = [&](int x, int st) {
+            // tile g = 2*it + x of the A,B,A,B,... sequence lives in S buffer g % 3
+            auto sbuf = [](int it, int x) { return (2 * it + x) % kSBufs; };
+            auto suse_parity = [](int it, int x) { return static_cast<uint32_t>(((2 * it + x) / kSBufs) & 1); };
+
+            // S = Q_X * K^T : both operands K-major (head dim contiguous), 128B swizzle,
+            // 8-row core-matrix groups 1024 B apart; a K=16 step advances 32 B inside the atom.
+            auto issue_qk = [&](int x, int it) {
                 const uint32_t qa = smem_base + Smem::q + x * kTileBytes;
-                const uint32_t ka = smem_base + Smem::k + st * kTileBytes;
+                const uint32_t ka = smem_base + Smem::k + (it % kStagesK) * kTileBytes;
+                const uint32_t td = tmem_base + kColS + sbuf(it, x) * kBlockN;
 #pragma unroll
                 for (int kk = 0; kk < kHeadDim / 16; ++kk) {
                     const uint64_t ad = make_smem_desc(qa + kk * 32, 16, 1024, kSwizzle128B);
                     const uint64_t bd = make_smem_desc(ka + kk * 32, 16, 1024, kSwizzle128B);
-                    mma_ss(tmem_base + kColS + x * kBlockN, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+                    mma_ss(td, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
                 }
+                tc_commit(bar(kBarSFull + sbuf(it, x)));
             };
-            // O_X += P_X * V : B operand V is [key][d] with d contiguous = MN-major, 128B swizzle;
+            // O_X += P * V : B operand V is [key][d] with d contiguous = MN-major, 128B swizzle;
             // 8-key groups 1024 B apart (SBO); a K=16 step advances 16 keys = 2048 B.
-            auto issue_pv = [&](int x, int st, bool accumulate) {
-                const uint32_t va = smem_base + Smem::v + st * kTileBytes;
+            auto issue_pv = [&](int x, int it) {
+                const uint32_t va = smem_base + Smem::v + (it % kStagesV) * kTileBytes;
+                const int sb = sbuf(it, x);
 #pragma unroll
                 for (int kk = 0; kk < kBlockN / 16; ++kk) {
                     const uint64_t bd = make_smem_desc(va + kk * 2048, kTileBytes, 1024, kSwizzle128B);
-                    const uint32_t acc = (accumulate || kk > 0) ? 1u : 0u;
-                    if (kPTmem) {
-                        // A = P from TMEM: 16 bf16 per row per step = 8 packed 32-bit columns
-                        mma_ts(tmem_base + kColO + x * kHeadDim, tmem_base + kColS + x * kBlockN + kk * 8, bd,
-                               idesc_pv, acc);
-                    } else {
-                        // A = P from smem, K-major 128B swizzle, two 64-key sub-tiles of 16 KiB
-                        const uint32_t pa = smem_base + Smem::p + x * 2 * kTileBytes + (kk >> 2) * kTileBytes +
-                                            (kk & 3) * 32;
-                        const uint64_t ad = make_smem_desc(pa, 16, 1024, kSwizzle128B);
-                        mma_ss(tmem_base + kColO + x * kHeadDim, ad, bd, idesc_pv, acc);
-                    }
+                    const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+                    // A = P from TMEM: 16 bf16 per row per step = 8 packed 32-bit columns
+                    mma_ts(tmem_base + kColO + x * kHeadDim, tmem_base + kColS + sb * kBlockN + kk * 8, bd, idesc_pv,
+                           acc);
                 }
             };
+            auto wait_k = [&](int it) {
+                mbar_wait(bar(kBarKFull + it % kStagesK), (it / kStagesK) & 1);
+                tc_fence_after();
+            };
+            auto release_k = [&](int it) { tc_commit(bar(kBarKEmpty + it % kStagesK)); };
 
+            // prologue: S_A(0), S_B(0), and already S_A(1) into the third buffer
             mbar_wait(bar(kBarQFull), 0);
-            mbar_wait(bar(kBarKFull + 0), 0);
-            tc_fence_after();
+            wait_k(0);
             issue_qk(0, 0);
-            tc_commit(bar(kBarSFull + 0));
-            if (has_b) {
-                issue_qk(1, 0);
-                tc_commit(bar(kBarSFull + 1));
+            if (has_b) issue_qk(1, 0);
+            release_k(0);
+            if (num_live > 1) {
+                wait_k(1);
+                issue_qk(0, 1);
+                if (!has_b) release_k(1);
             }
-            tc_commit(bar(kBarKEmpty + 0));
 
             for (int it = 0; it < num_live; ++it) {
-                const int st = it % kStages;
-                const uint32_t ph = (it / kStages) & 1;
-                const bool has_next = it + 1 < num_live;
-                const int st_n = (it + 1) % kStages;
-                const uint32_t ph_n = ((it + 1) / kStages) & 1;
-
-                mbar_wait(bar(kBarVFull + st), ph);
-                // ---- tile A ----
-                mbar_wait(bar(kBarPFull + 0), it & 1);
+                const bool last = it + 1 == num_live;
+                mbar_wait(bar(kBarVFull + it % kStagesV), (it / kStagesV) & 1);
+                // ---- P_A(it) ready: O_A += P_A V; its S buffer is then free for S_B(it+1) ----
+                mbar_wait(bar(kBarPFull + sbuf(it, 0)), suse_parity(it, 0));
                 tc_fence_after();
-                issue_pv(0, st, it > 0);
-                if (has_next) {
-                    mbar_wait(bar(kBarKFull + st_n), ph_n);
-                    tc_fence_after();
-                    issue_qk(0, st_n);
-                    tc_commit(bar(kBarSFull + 0));
-                } else {
-                    tc_commit(bar(kBarOFull + 0));
-                }
-                // ---- tile B ----
+                issue_pv(0, it);
+                if (last) tc_commit(bar(kBarOFull + 0));
                 if (has_b) {
-                    mbar_wait(bar(kBarPFull + 1), it & 1);
-                    tc_fence_after();
-                    issue_pv(1, st, it > 0);
-                }
-                tc_commit(bar(kBarVEmpty + st));
-                if (has_b) {
-                    if (has_next) {
-                        issue_qk(1, st_n);
-                        tc_commit(bar(kBarSFull + 1));
-                    } else {
-                        tc_commit(bar(kBarOFull + 1));
+                    if (!last) {
+                        issue_qk(1, it + 1);  // K(it+1) was waited for when S_A(it+1) was issued
+                        release_k(it + 1);
                     }
+                    // ---- P_B(it) ready: O_B += P_B V; its S buffer is then free for S_A(it+2) ----
+                    mbar_wait(bar(kBarPFull + sbuf(it, 1)), suse_parity(it, 1));
+                    tc_fence_after();
+                    issue_pv(1, it);
+                    if (last) tc_commit(bar(kBarOFull + 1));
                 }
-                if (has_next) tc_commit(bar(kBarKEmpty + st_n));
+                tc_commit(bar(kBarVEmpty + it % kStagesV));
+                if (it + 2 < num_live) {
+                    wait_k(it + 2);
+                    issue_qk(0, it + 2);
+                    if (!has_b) release_k(it + 2);
+                }
             }
         }
     } else {
@@ -246,7 +265,6 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const int row = q0 + x * kBlockM + r;
         const bool active = (x == 0) || has_b;
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-        const uint32_t t_s = tmem_base + lane_base + kColS + x * kBlockN;
         const uint32_t t_o = tmem_base + lane_base + kColO + x * kHeadDim;
         const int kv_end_eff = min(p.kv_end, p.S);
         const int tile_r_lo = q0 + x * kBlockM;
@@ -261,7 +279,9 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             for (int n = n0; n < n1; ++n) {
                 if (!tile_live(p, b, n)) continue;
                 const int kv0 = n * kBlockN;
-                mbar_wait(bar(kBarSFull + x), it & 1);
+                const int sb = (2 * it + x) % kSBufs;  // S/P buffer of this tile
+                const uint32_t t_s = tmem_base + lane_base + kColS + sb * kBlockN;
+                mbar_wait(bar(kBarSFull + sb), ((2 * it + x) / kSBufs) & 1);
                 tc_fence_after();
 
                 float s[kBlockN];
@@ -331,36 +351,18 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const float neg_m = (m_new == -CUDART_INF_F) ? 0.f : -m_new;
 
                 float sum0 = 0.f, sum1 = 0.f;
-                if (kPTmem) {
 #pragma unroll
-                    for (int cb = 0; cb < kBlockN / 32; ++cb) {
-                        uint32_t pk[16];
+                for (int cb = 0; cb < kBlockN / 32; ++cb) {
+                    uint32_t pk[16];
 #pragma unroll
-                        for (int u = 0; u < 16; ++u) {
-                            const float p0 = ex2(fmaf(s[cb * 32 + 2 * u], mul, neg_m));
-                            const float p1 = ex2(fmaf(s[cb * 32 + 2 * u + 1], mul, neg_m));
-                            sum0 += p0;
-                            sum1 += p1;
-                            pk[u] = pack2<kBf16>(p0, p1);
-                        }
-                        tmem_st16(t_s + cb * 16, pk);
+                    for (int u = 0; u < 16; ++u) {
+                        const float p0 = ex2(fmaf(s[cb * 32 + 2 * u], mul, neg_m));
+                        const float p1 = ex2(fmaf(s[cb * 32 + 2 * u + 1], mul, neg_m));
+                        sum0 += p0;
+                        sum1 += p1;
+                        pk[u] = pack2<kBf16>(p0, p1);
                     }
-                } else {
-                    uint8_t* prow = smem_gen + Smem::p + x * 2 * kTileBytes + r * 128;
-#pragma unroll
-                    for (int ch = 0; ch < kBlockN / 8; ++ch) {  // 16-byte chunks of 8 keys
-                        uint32_t pk[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const float p0 = ex2(fmaf(s[ch * 8 + 2 * u], mul, neg_m));
-                            const float p1 = ex2(fmaf(s[ch * 8 + 2 * u + 1], mul, neg_m));
-                            sum0 += p0;
-                            sum1 += p1;
-                            pk[u] = pack2<kBf16>(p0, p1);
-                        }
-                        uint8_t* dst = prow + (ch >> 3) * kTileBytes + (((ch & 7) ^ (r & 7)) << 4);
-                        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                    }
+                    tmem_st16(t_s + cb * 16, pk);
                 }
                 l_run = l_run * alpha + (sum0 + sum1);
                 m_ref = m_new;
@@ -378,14 +380,9 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         tmem_st32(t_o + hb * 32, o);
                     }
                 }
-                if (kPTmem) {
-                    tc_wait_st();
-                } else {
-                    tc_wait_st();
-                    fence_proxy_async_smem();
-                }
+                tc_wait_st();
                 tc_fence_before();
-                mbar_arrive(bar(kBarPFull + x));
+                mbar_arrive(bar(kBarPFull + sb));
                 ++it;
             }
 
@@ -451,18 +448,15 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 
 }  // namespace
 
-size_t fa_fwd_sm100_smem_bytes(bool p_in_tmem) {
-    return (p_in_tmem ? Smem::bars_tmem : Smem::bars_ss) + Smem::bar_bytes + 1024;  // + alignment slack
+size_t fa_fwd_sm100_smem_bytes() {
+    return Smem::bars + Smem::bar_bytes + 1024;  // + alignment slack
 }
 
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
-                                const FaParams& p, bool bf16, bool p_in_tmem, cudaStream_t stream, int* grid_ctas) {
-    void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const FaParams) = nullptr;
-    if (bf16 && p_in_tmem) kern = fa_fwd_sm100_kernel<true, true>;
-    if (bf16 && !p_in_tmem) kern = fa_fwd_sm100_kernel<true, false>;
-    if (!bf16 && p_in_tmem) kern = fa_fwd_sm100_kernel<false, true>;
-    if (!bf16 && !p_in_tmem) kern = fa_fwd_sm100_kernel<false, false>;
-    const size_t smem = fa_fwd_sm100_smem_bytes(p_in_tmem);
+                                const FaParams& p, bool bf16, cudaStream_t stream, int* grid_ctas) {
+    void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const FaParams) =
+        bf16 ? fa_fwd_sm100_kernel<true> : fa_fwd_sm100_kernel<false>;
+    const size_t smem = fa_fwd_sm100_smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     dim3 grid((p.S + kRowsPerCta - 1) / kRowsPerCta, p.H, p.B);

@@ -52,8 +52,8 @@ struct SimtParams {
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
-                                const FaParams& p, bool bf16, bool p_in_tmem, cudaStream_t stream, int* grid_ctas);
-size_t fa_fwd_sm100_smem_bytes(bool p_in_tmem);
+                                const FaParams& p, bool bf16, cudaStream_t stream, int* grid_ctas);
+size_t fa_fwd_sm100_smem_bytes();
 cudaError_t launch_fa_fwd_simt(const SimtParams& p, cudaStream_t stream, int* grid_ctas);
 
 cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias2, uint8_t* tile_flags,

@@ -145,9 +145,6 @@ def test_edge_cases(torch_mod, P, oracle):
     v16 = v.astype(np.float16).astype(np.float32)
     err, _, _ = run_case(torch, P, oracle, q16, k16, v16, 0.0, 63, 64, None, kernel="tcgen05", dtype=torch.float16)
     assert err <= TOL
-    # P staged through shared memory (SS variant) gives the same answer
-    err, _, _ = run_case(torch, P, oracle, q, k, v, 0.0, -1, -1, pb, kernel="tcgen05", flags=1)
-    assert err <= TOL
     # empty tensors are a no-op
     e = torch.empty((0, 2, 16, 64), device="cuda", dtype=torch.bfloat16)
     assert P.flash_attention(e, e, e).shape == (0, 2, 16, 64)
@@ -311,10 +308,12 @@ def test_full_size_properties_8k(torch_mod, P, oracle):
         # determinism: bit-identical across runs (attention.hpp:43)
         o2 = P.flash_attention(q, k, v, spec, out_dtype=torch.float32)
         assert torch.equal(o1, o2)
-        # softmax rows sum to one: V = 1 -> O = 1 on every row (all rows have a live key here)
+        # softmax rows sum to one: V = 1 -> O = 1 on every row that has a live key, 0 elsewhere
         ones = torch.ones_like(v)
         o_ones = P.flash_attention(q, k, ones, spec, out_dtype=torch.float32)
-        assert (o_ones - 1.0).abs().max().item() <= 1e-2
+        n_live_rows = S if wl < 0 else min(S, lens[0] + wl)  # row i is live iff i - wl <= lens-1
+        assert (o_ones[:, :, :n_live_rows] - 1.0).abs().max().item() <= 1e-2
+        assert (o_ones[:, :, n_live_rows:] == 0).all()
         # linearity in V
         v2 = (torch.rand((B, H, S, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
         o_v2 = P.flash_attention(q, k, v2, spec, out_dtype=torch.float32)

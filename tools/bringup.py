@@ -182,11 +182,8 @@ CASES = {
     "simt_small": lambda: case_fa("simt_small", 1, 2, 200, -1, -1, None, 0, kernel="simt"),
     "simt_local_pad": lambda: case_fa("simt_local_pad", 2, 2, 300, 63, 64, [300, 211], 0, kernel="simt"),
     "ts_128": lambda: case_fa("ts_128", 1, 1, 128, -1, -1, None, 0, dump=True),
-    "ss_128": lambda: case_fa("ss_128", 1, 1, 128, -1, -1, None, 1, dump=True),
     "ts_256": lambda: case_fa("ts_256", 1, 1, 256, -1, -1, None, 0, dump=True),
-    "ss_256": lambda: case_fa("ss_256", 1, 1, 256, -1, -1, None, 1, dump=True),
     "ts_512": lambda: case_fa("ts_512", 1, 12, 512, -1, -1, None, 0),
-    "ss_512": lambda: case_fa("ss_512", 1, 12, 512, -1, -1, None, 1),
     "ts_1000_ragged": lambda: case_fa("ts_1000_ragged", 2, 3, 1000, -1, -1, None, 0),
     "ts_2048": lambda: case_fa("ts_2048", 1, 4, 2048, -1, -1, None, 0),
     "ts_pad": lambda: case_fa("ts_pad", 2, 4, 512, -1, -1, [475, 300], 0),
@@ -196,11 +193,9 @@ CASES = {
     "ts_self": lambda: case_fa("ts_self", 1, 2, 300, 0, 0, None, 0),
     "ts_tiny": lambda: case_fa("ts_tiny", 1, 1, 5, -1, -1, None, 0),
     "ts_allpad": lambda: case_fa("ts_allpad", 2, 2, 256, -1, -1, [256, 0], 0),
-    "ss_local_pad": lambda: case_fa("ss_local_pad", 2, 4, 1000, 63, 64, [1000, 777], 1),
     "cross_8k": lambda: case_cross("cross_8k", 1, 12, 8192, -1, -1, None),
     "cross_8k_local_pad": lambda: case_cross("cross_8k_local_pad", 1, 12, 8192, 63, 64, [7000]),
     "time_8k_ts": lambda: case_time("time_8k_ts", 1, 12, 8192, -1, -1, 0),
-    "time_8k_ss": lambda: case_time("time_8k_ss", 1, 12, 8192, -1, -1, 1),
     "time_16k_ts": lambda: case_time("time_16k_ts", 1, 12, 16384, -1, -1, 0, iters=10),
     "time_32k_ts": lambda: case_time("time_32k_ts", 1, 12, 32768, -1, -1, 0, iters=5),
     "time_8k_local_ts": lambda: case_time("time_8k_local_ts", 1, 12, 8192, 63, 64, 0),
