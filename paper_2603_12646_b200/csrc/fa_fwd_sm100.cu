@@ -185,13 +185,23 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
     } else if (warp == kMmaWarp) {
         // =============================== UMMA issuer ===============================
-        if (lane == 0 && num_live > 0) {
+        // The whole warp runs this loop with warp-uniform values (so descriptors and addresses
+        // live in uniform registers); only the tcgen05 instructions themselves are predicated on
+        // one elected lane.  A divergent `if (lane == 0)` around the loop would make ptxas wrap
+        // every UTCHMMA in an ELECT / R2UR waterfall loop, which puts ~16 instructions per MMA on
+        // the critical path.
+        if (num_live > 0) {
+            const bool leader = elect_one() != 0;
             constexpr uint32_t fmt = kBf16 ? 1u : 0u;
             constexpr uint32_t idesc_qk = make_idesc_f16(fmt, 0, 0, kBlockM, kBlockN);
             constexpr uint32_t idesc_pv = make_idesc_f16(fmt, 0, 1, kBlockM, kHeadDim);
+            // descriptor high words are constants; the low word is (address >> 4) | LBO field
+            constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (kSwizzle128B << 29);  // SBO, version, swizzle
+            constexpr uint32_t kLboK = (16u >> 4) << 16;                                    // K-major operands
+            constexpr uint32_t kLboV = (static_cast<uint32_t>(kTileBytes) >> 4) << 16;      // MN-major V
+            const uint32_t sb16 = smem_base >> 4;
+            auto desc = [&](uint32_t lo) { return (static_cast<uint64_t>(kDescHi) << 32) | lo; };
 
-            // S_X = Q_X * K^T : both operands K-major (head dim contiguous), 128B swizzle,
-            // 8-row core-matrix groups 1024 B apart; a K=16 step advances 32 B inside the atom.
             // tile g = 2*it + x of the A,B,A,B,... sequence lives in S buffer g % 3
             auto sbuf = [](int it, int x) { return (2 * it + x) % kSBufs; };
             auto suse_parity = [](int it, int x) { return static_cast<uint32_t>(((2 * it + x) / kSBufs) & 1); };
@@ -199,36 +209,42 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // S = Q_X * K^T : both operands K-major (head dim contiguous), 128B swizzle,
             // 8-row core-matrix groups 1024 B apart; a K=16 step advances 32 B inside the atom.
             auto issue_qk = [&](int x, int it) {
-                const uint32_t qa = smem_base + Smem::q + x * kTileBytes;
-                const uint32_t ka = smem_base + Smem::k + (it % kStagesK) * kTileBytes;
+                const uint32_t qlo = kLboK | (sb16 + (Smem::q + x * kTileBytes) / 16);
+                const uint32_t klo = kLboK | (sb16 + (Smem::k + (it % kStagesK) * kTileBytes) / 16);
                 const uint32_t td = tmem_base + kColS + sbuf(it, x) * kBlockN;
+                const uint32_t sbar = bar(kBarSFull + sbuf(it, x));
+                if (leader) {
 #pragma unroll
-                for (int kk = 0; kk < kHeadDim / 16; ++kk) {
-                    const uint64_t ad = make_smem_desc(qa + kk * 32, 16, 1024, kSwizzle128B);
-                    const uint64_t bd = make_smem_desc(ka + kk * 32, 16, 1024, kSwizzle128B);
-                    mma_ss(td, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+                    for (int kk = 0; kk < kHeadDim / 16; ++kk)
+                        mma_ss(td, desc(qlo + kk * 2), desc(klo + kk * 2), idesc_qk, kk > 0 ? 1u : 0u);
+                    tc_commit(sbar);
                 }
-                tc_commit(bar(kBarSFull + sbuf(it, x)));
+                __syncwarp();
             };
             // O_X += P * V : B operand V is [key][d] with d contiguous = MN-major, 128B swizzle;
             // 8-key groups 1024 B apart (SBO); a K=16 step advances 16 keys = 2048 B.
+            // A = P from TMEM: 16 bf16 per row per step = 8 packed 32-bit columns.
             auto issue_pv = [&](int x, int it) {
-                const uint32_t va = smem_base + Smem::v + (it % kStagesV) * kTileBytes;
-                const int sb = sbuf(it, x);
+                const uint32_t vlo = kLboV | (sb16 + (Smem::v + (it % kStagesV) * kTileBytes) / 16);
+                const uint32_t td = tmem_base + kColO + x * kHeadDim;
+                const uint32_t ta = tmem_base + kColS + sbuf(it, x) * kBlockN;
+                const uint32_t acc0 = it > 0 ? 1u : 0u;
+                if (leader) {
 #pragma unroll
-                for (int kk = 0; kk < kBlockN / 16; ++kk) {
-                    const uint64_t bd = make_smem_desc(va + kk * 2048, kTileBytes, 1024, kSwizzle128B);
-                    const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-                    // A = P from TMEM: 16 bf16 per row per step = 8 packed 32-bit columns
-                    mma_ts(tmem_base + kColO + x * kHeadDim, tmem_base + kColS + sb * kBlockN + kk * 8, bd, idesc_pv,
-                           acc);
+                    for (int kk = 0; kk < kBlockN / 16; ++kk)
+                        mma_ts(td, ta + kk * 8, desc(vlo + kk * 128), idesc_pv, kk > 0 ? 1u : acc0);
                 }
+                __syncwarp();
+            };
+            auto commit = [&](uint32_t b_) {
+                if (leader) tc_commit(b_);
+                __syncwarp();
             };
             auto wait_k = [&](int it) {
                 mbar_wait(bar(kBarKFull + it % kStagesK), (it / kStagesK) & 1);
                 tc_fence_after();
             };
-            auto release_k = [&](int it) { tc_commit(bar(kBarKEmpty + it % kStagesK)); };
+            auto release_k = [&](int it) { commit(bar(kBarKEmpty + it % kStagesK)); };
 
             // prologue: S_A(0), S_B(0), and already S_A(1) into the third buffer
             mbar_wait(bar(kBarQFull), 0);
@@ -249,7 +265,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 mbar_wait(bar(kBarPFull + sbuf(it, 0)), suse_parity(it, 0));
                 tc_fence_after();
                 issue_pv(0, it);
-                if (last) tc_commit(bar(kBarOFull + 0));
+                if (last) commit(bar(kBarOFull + 0));
                 if (has_b) {
                     if (!last) {
                         issue_qk(1, it + 1);  // K(it+1) was waited for when S_A(it+1) was issued
@@ -259,9 +275,9 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     mbar_wait(bar(kBarPFull + sbuf(it, 1)), suse_parity(it, 1));
                     tc_fence_after();
                     issue_pv(1, it);
-                    if (last) tc_commit(bar(kBarOFull + 1));
+                    if (last) commit(bar(kBarOFull + 1));
                 }
-                tc_commit(bar(kBarVEmpty + it % kStagesV));
+                commit(bar(kBarVEmpty + it % kStagesV));
                 if (it + 2 < num_live) {
                     wait_k(it + 2);
                     issue_qk(0, it + 2);
