@@ -4,18 +4,22 @@
 // non-causal, additive padding bias (masked at <= -30000), optional two-sided sliding window,
 // online softmax, rows without a live key -> 0.  No S x S tensor is ever materialised.
 //
-// Hardware mapping (one CTA per SM, 320 threads, two 128-row query tiles "A"/"B" ping-pong):
-//   warp 8      TMA producer: Q once, then K/V 128-key tiles through two 3-deep smem rings
+// Hardware mapping (one CTA per SM, 640 threads, two 128-row query tiles "A"/"B" ping-pong):
+//   warp 16     TMA producer: Q once, then K/V 128-key tiles through smem rings
 //               (cp.async.bulk.tensor, 128B swizzle, mbarrier complete_tx)
-//   warp 9      UMMA issuer (one elected lane): S_X = Q_X K^T  (tcgen05.mma SS, M128 N128 K16 x4)
+//   warp 17     UMMA issuer (one elected lane): S_X = Q_X K^T  (tcgen05.mma SS, M128 N128 K16 x4)
 //                                               O_X += P_X V   (tcgen05.mma TS, M128 N64  K16 x8)
 //               accumulators in TMEM: three rotating S buffers, cols [0,384) (tile g = 2*it + X of
 //               the A,B,A,B,... sequence uses buffer g % 3, so the next S of a warpgroup is computed
 //               while it is still busy with the current one), O_A [384,448), O_B [448,512);
 //               P (bf16) aliases the first 64 columns of its S buffer.
-//   warps 0-3   softmax for tile A, warps 4-7 for tile B: one thread owns one query row
-//               (tcgen05.ld 32x32b), so row max / row sum need no shuffles; exp2 with the scale
-//               folded in; lazy rescale of O (only when the running max grows by > 2^8).
+//   warps 0-7   softmax for tile A, warps 8-15 for tile B.  Two threads share one query row
+//               (key columns [0,64) and [64,128) of the tile; tcgen05.ld 32x32b), so four softmax
+//               warps per SM sub-partition hide each other's MUFU/ALU latencies.  The two halves
+//               exchange their row max through shared memory (one named barrier per tile); row
+//               sums stay per-thread until the epilogue.  exp2 with the scale folded in, packed
+//               f32x2 math, lazy rescale of O (only when the running max grows by > 2^8).
+//               setmaxnreg moves registers from the producer/MMA warpgroup to the softmax ones.
 // K/V are loaded once per 256 query rows; the tensor pipe and the MUFU pipe overlap because
 // tile A's softmax runs while tile B's MMAs execute and vice versa.
 #include <cuda.h>
@@ -39,10 +43,13 @@ constexpr int kStagesK = 4;                         // K ring depth (K runs two 
 constexpr int kStagesV = 3;                         // V ring depth
 constexpr int kSBufs = 3;                           // rotating S/P accumulators in TMEM
 constexpr int kTileBytes = kBlockN * kHeadDim * 2;  // 16 KiB: one 128 x 64 16-bit tile
-constexpr int kNumSoftmaxWarps = 8;
-constexpr int kProducerWarp = 8;
-constexpr int kMmaWarp = 9;
-constexpr int kThreads = 320;
+constexpr int kNumSoftmaxWarps = 16;
+constexpr int kProducerWarp = 16;
+constexpr int kMmaWarp = 17;
+constexpr int kThreads = 640;  // 5 warpgroups: 4 softmax + 1 (producer, MMA, 2 idle warps)
+constexpr int kHalfN = kBlockN / 2;  // key columns per softmax thread
+constexpr int kRegsSoftmax = 112;
+constexpr int kRegsOther = 32;  // 128*32 + 512*112 == 640*96: the CTA register pool balances exactly
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;    // + 128 * buffer
 constexpr uint32_t kColO = 384;  // + 64 * X
@@ -55,6 +62,8 @@ struct Smem {
     static constexpr uint32_t v = k + kStagesK * kTileBytes;           // kStagesV tiles
     static constexpr uint32_t bars = v + kStagesV * kTileBytes;        // barrier block
     static constexpr uint32_t bar_bytes = 256;
+    static constexpr uint32_t xchg = bars + bar_bytes;                 // row-max exchange: [2 parity][2 tile][2 half][128] f32
+    static constexpr uint32_t xchg_bytes = 2 * 2 * 2 * kBlockM * 4;
 };
 // barrier indices inside the barrier block (8 bytes each)
 enum : uint32_t {
@@ -119,7 +128,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
         for (int s = 0; s < kSBufs; ++s) {
             mbar_init(bar(kBarSFull + s), 1);
-            mbar_init(bar(kBarPFull + s), kBlockM);
+            mbar_init(bar(kBarPFull + s), 2 * kBlockM);
         }
         for (int x = 0; x < 2; ++x) mbar_init(bar(kBarOFull + x), 1);
         fence_barrier_init();
@@ -133,6 +142,8 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    static_assert(128 * kRegsOther + 512 * kRegsSoftmax <= kThreads * 96, "setmaxnreg pool must balance");
+    if (warp >= kNumSoftmaxWarps) setmaxnreg_dec<kRegsOther>();
     if (warp == kProducerWarp) {
         // =============================== TMA producer ===============================
         if (lane == 0 && num_live > 0) {
@@ -274,21 +285,25 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 }
             }
         }
-    } else {
+    } else if (warp < kNumSoftmaxWarps) {
         // =============================== softmax / epilogue ===============================
-        const int x = warp >> 2;            // 0 = tile A, 1 = tile B
-        const int r = threadIdx.x & 127;    // row inside the tile == TMEM lane
+        setmaxnreg_inc<kRegsSoftmax>();
+        const int x = warp >> 3;            // 0 = tile A, 1 = tile B
+        const int hf = (warp >> 2) & 1;     // which half of the tile's key columns this thread owns
+        const int r = (warp & 3) * 32 + lane;  // row inside the tile == TMEM lane
         const int row = q0 + x * kBlockM + r;
         const bool active = (x == 0) || has_b;
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-        const uint32_t t_o = tmem_base + lane_base + kColO + x * kHeadDim;
+        const uint32_t t_o = tmem_base + lane_base + kColO + x * kHeadDim + hf * (kHeadDim / 2);
         const int kv_end_eff = min(p.kv_end, p.S);
         const int tile_r_lo = q0 + x * kBlockM;
         const int tile_r_hi = tile_r_lo + kBlockM - 1;
         const float c = p.scale_log2;
+        float* xchg = reinterpret_cast<float*>(smem_gen + Smem::xchg);
+        const uint32_t bar_id = 1 + x;  // named barrier of this tile's 256 threads
 
         float m_ref = -CUDART_INF_F;
-        float l_run = 0.f;
+        float l_run = 0.f;  // this thread's share of the row sum (its 64 columns of every tile)
 
         if (active) {
             int it = 0;
@@ -300,19 +315,19 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 mbar_wait(bar(kBarSFull + sb), ((2 * it + x) / kSBufs) & 1);
                 tc_fence_after();
 
-                float s[kBlockN];
+                float s[kHalfN];
                 {
-                    uint32_t(&su)[kBlockN] = reinterpret_cast<uint32_t(&)[kBlockN]>(s);
+                    uint32_t(&su)[kHalfN] = reinterpret_cast<uint32_t(&)[kHalfN]>(s);
 #pragma unroll
-                    for (int cb = 0; cb < kBlockN / 32; ++cb)
-                        tmem_ld32(t_s + cb * 32, reinterpret_cast<uint32_t(&)[32]>(su[cb * 32]));
+                    for (int cb = 0; cb < kHalfN / 32; ++cb)
+                        tmem_ld32(t_s + hf * kHalfN + cb * 32, reinterpret_cast<uint32_t(&)[32]>(su[cb * 32]));
                     tc_wait_ld();
                 }
                 if (p.debug_scores != nullptr && it == 0) {
                     const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-                    float* dst = p.debug_scores + ((cta * 2 + x) * kBlockM + r) * kBlockN;
+                    float* dst = p.debug_scores + ((cta * 2 + x) * kBlockM + r) * kBlockN + hf * kHalfN;
 #pragma unroll
-                    for (int j = 0; j < kBlockN; ++j) dst[j] = s[j];
+                    for (int j = 0; j < kHalfN; ++j) dst[j] = s[j];
                 }
 
                 // tile class (warp-uniform): "full" tiles need no per-element predicate
@@ -322,30 +337,30 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                                   (p.wl < 0 || tile_r_hi - kv0 <= p.wl) &&
                                   (p.wr < 0 || kv0 + kBlockN - 1 - tile_r_lo <= p.wr);
 
-                float tile_max;
+                float my_max;
                 float mul;
                 if (full) {
                     float mx0 = s[0], mx1 = s[1];
 #pragma unroll
-                    for (int j = 2; j < kBlockN; j += 4) {
+                    for (int j = 2; j < kHalfN; j += 4) {
                         mx0 = max3(mx0, s[j], s[j + 1]);
-                        if (j + 3 < kBlockN) mx1 = max3(mx1, s[j + 2], s[j + 3]);
+                        if (j + 3 < kHalfN) mx1 = max3(mx1, s[j + 2], s[j + 3]);
                     }
-                    tile_max = fmaxf(mx0, mx1) * c;  // scale > 0 (validated on the host)
+                    my_max = fmaxf(mx0, mx1) * c;  // scale > 0 (validated on the host)
                     mul = c;
                 } else {
                     // live columns of this row inside the tile: [lo, hi]
                     int lo = p.kv_begin, hi = kv_end_eff - 1;
                     if (p.wl >= 0) lo = max(lo, row - p.wl);
                     if (p.wr >= 0) hi = min(hi, row + p.wr);
-                    lo -= kv0;
-                    hi -= kv0;
+                    lo -= kv0 + hf * kHalfN;
+                    hi -= kv0 + hf * kHalfN;
                     const float* brow = (flag == kTileMixed && p.bias2 != nullptr)
-                                            ? p.bias2 + static_cast<size_t>(b) * p.bias_stride + kv0
+                                            ? p.bias2 + static_cast<size_t>(b) * p.bias_stride + kv0 + hf * kHalfN
                                             : nullptr;
                     float mx = -CUDART_INF_F;
 #pragma unroll
-                    for (int j4 = 0; j4 < kBlockN; j4 += 4) {
+                    for (int j4 = 0; j4 < kHalfN; j4 += 4) {
                         float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
                         if (brow != nullptr) bb = __ldg(reinterpret_cast<const float4*>(brow + j4));
                         const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
@@ -357,9 +372,17 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             mx = fmaxf(mx, s[j]);
                         }
                     }
-                    tile_max = mx;
+                    my_max = mx;
                     mul = 1.0f;
                 }
+
+                // row max over both halves: exchange through smem (double-buffered by tile parity).
+                // The barrier also orders every S read of this tile before any P write below
+                // (P aliases the first 64 columns of the S buffer, which belong to half 0).
+                float* xrow = xchg + (((it & 1) * 2 + x) * 2) * kBlockM + r;
+                xrow[hf * kBlockM] = my_max;
+                named_bar_sync(bar_id, 2 * kBlockM);
+                const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
 
                 // lazy running max: move the reference only when it would grow by > 2^8
                 const float m_new = (tile_max > m_ref + kRescaleThreshold) ? tile_max : m_ref;
@@ -368,33 +391,37 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 
                 float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
-                for (int cb = 0; cb < kBlockN / 32; ++cb) {
+                for (int cb = 0; cb < kHalfN / 32; ++cb) {
                     uint32_t pk[16];
 #pragma unroll
                     for (int u = 0; u < 16; ++u) {
-                        const float p0 = ex2(fmaf(s[cb * 32 + 2 * u], mul, neg_m));
-                        const float p1 = ex2(fmaf(s[cb * 32 + 2 * u + 1], mul, neg_m));
-                        sum0 += p0;
-                        sum1 += p1;
+                        float x0, x1;
+                        ffma2(x0, x1, s[cb * 32 + 2 * u], s[cb * 32 + 2 * u + 1], mul, neg_m);
+                        const float p0 = ex2(x0);
+                        const float p1 = ex2(x1);
+                        fadd2(sum0, sum1, p0, p1);
                         pk[u] = pack2<kBf16>(p0, p1);
                     }
-                    tmem_st16(t_s + cb * 16, pk);
+                    tmem_st16(t_s + hf * (kHalfN / 2) + cb * 16, pk);
                 }
                 l_run = l_run * alpha + (sum0 + sum1);
                 m_ref = m_new;
 
                 // O_X *= alpha for rows whose reference max moved (PV of the previous tile has
-                // completed: S_X(n) was committed after it on the in-order tensor pipe)
+                // completed: this S buffer was committed after it on the in-order tensor pipe).
+                // Each half rescales its own 32 of the 64 output columns.
                 if (it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+                    uint32_t o[32];
+                    tmem_ld32(t_o, o);
+                    tc_wait_ld();
 #pragma unroll
-                    for (int hb = 0; hb < kHeadDim / 32; ++hb) {
-                        uint32_t o[32];
-                        tmem_ld32(t_o + hb * 32, o);
-                        tc_wait_ld();
-#pragma unroll
-                        for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * alpha);
-                        tmem_st32(t_o + hb * 32, o);
+                    for (int u = 0; u < 32; u += 2) {
+                        float a0 = __uint_as_float(o[u]), a1 = __uint_as_float(o[u + 1]);
+                        fmul2(a0, a1, alpha);
+                        o[u] = __float_as_uint(a0);
+                        o[u + 1] = __float_as_uint(a1);
                     }
+                    tmem_st32(t_o, o);
                 }
                 tc_wait_st();
                 tc_fence_before();
@@ -403,42 +430,50 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             }
 
             // ---------------- epilogue ----------------
-            float o[kHeadDim];
+            // combine the two halves' row sums, then each half writes its 32 output columns
+            float* lrow = xchg + ((0 * 2 + x) * 2) * kBlockM + r;
+            named_bar_sync(bar_id, 2 * kBlockM);  // all max-exchange reads of the last tile are done
+            lrow[hf * kBlockM] = l_run;
+            named_bar_sync(bar_id, 2 * kBlockM);
+            const float l_tot = l_run + lrow[(hf ^ 1) * kBlockM];
+
+            constexpr int kOutCols = kHeadDim / 2;
+            float o[kOutCols];
             if (num_live > 0) {
                 mbar_wait(bar(kBarOFull + x), 0);
                 tc_fence_after();
-                uint32_t(&ou)[kHeadDim] = reinterpret_cast<uint32_t(&)[kHeadDim]>(o);
-#pragma unroll
-                for (int hb = 0; hb < kHeadDim / 32; ++hb)
-                    tmem_ld32(t_o + hb * 32, reinterpret_cast<uint32_t(&)[32]>(ou[hb * 32]));
+                tmem_ld32(t_o, reinterpret_cast<uint32_t(&)[32]>(o));
                 tc_wait_ld();
             } else {
 #pragma unroll
-                for (int u = 0; u < kHeadDim; ++u) o[u] = 0.f;
+                for (int u = 0; u < kOutCols; ++u) o[u] = 0.f;
             }
             if (row < p.S) {
+                const int col0 = hf * kOutCols;
                 if (p.o_partial != nullptr) {
                     const size_t ridx = (static_cast<size_t>(b) * p.H + h) * p.S + row;
-                    float4* dst = reinterpret_cast<float4*>(p.o_partial + ridx * kHeadDim);
+                    float4* dst = reinterpret_cast<float4*>(p.o_partial + ridx * kHeadDim + col0);
 #pragma unroll
-                    for (int u = 0; u < kHeadDim / 4; ++u)
+                    for (int u = 0; u < kOutCols / 4; ++u)
                         dst[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
-                    p.m_partial[ridx] = m_ref;
-                    p.l_partial[ridx] = l_run;
+                    if (hf == 0) {
+                        p.m_partial[ridx] = m_ref;
+                        p.l_partial[ridx] = l_tot;
+                    }
                 } else {
-                    const float inv = l_run > 0.f ? 1.0f / l_run : 0.f;
+                    const float inv = l_tot > 0.f ? 1.0f / l_tot : 0.f;
                     const size_t off = static_cast<size_t>(b) * p.o_sb + static_cast<size_t>(h) * p.o_sh +
-                                       static_cast<size_t>(row) * p.o_ss;
+                                       static_cast<size_t>(row) * p.o_ss + col0;
                     if (p.out_dtype == 2) {
                         float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
 #pragma unroll
-                        for (int u = 0; u < kHeadDim / 4; ++u)
+                        for (int u = 0; u < kOutCols / 4; ++u)
                             dst[u] = make_float4(o[4 * u] * inv, o[4 * u + 1] * inv, o[4 * u + 2] * inv,
                                                  o[4 * u + 3] * inv);
                     } else {
                         uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + off);
 #pragma unroll
-                        for (int u = 0; u < kHeadDim / 8; ++u) {
+                        for (int u = 0; u < kOutCols / 8; ++u) {
                             uint32_t w[4];
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
@@ -465,7 +500,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 }  // namespace
 
 size_t fa_fwd_sm100_smem_bytes() {
-    return Smem::bars + Smem::bar_bytes + 1024;  // + alignment slack
+    return Smem::xchg + Smem::xchg_bytes + 1024;  // + alignment slack
 }
 
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
