@@ -300,7 +300,9 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const int tile_r_hi = tile_r_lo + kBlockM - 1;
         const float c = p.scale_log2;
         float* xchg = reinterpret_cast<float*>(smem_gen + Smem::xchg);
-        const uint32_t bar_id = 1 + x;  // named barrier of this tile's 256 threads
+        // named barrier shared by the two warps that own the same 32 rows (ids 1..8)
+        const uint32_t bar_id = 1 + x * 4 + (warp & 3);
+        constexpr uint32_t kPairThreads = 64;
 
         float m_ref = -CUDART_INF_F;
         float l_run = 0.f;  // this thread's share of the row sum (its 64 columns of every tile)
@@ -381,7 +383,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 // (P aliases the first 64 columns of the S buffer, which belong to half 0).
                 float* xrow = xchg + (((it & 1) * 2 + x) * 2) * kBlockM + r;
                 xrow[hf * kBlockM] = my_max;
-                named_bar_sync(bar_id, 2 * kBlockM);
+                named_bar_sync(bar_id, kPairThreads);
                 const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
 
                 // lazy running max: move the reference only when it would grow by > 2^8
@@ -432,9 +434,9 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // ---------------- epilogue ----------------
             // combine the two halves' row sums, then each half writes its 32 output columns
             float* lrow = xchg + ((0 * 2 + x) * 2) * kBlockM + r;
-            named_bar_sync(bar_id, 2 * kBlockM);  // all max-exchange reads of the last tile are done
+            named_bar_sync(bar_id, kPairThreads);  // all max-exchange reads of the last tile are done
             lrow[hf * kBlockM] = l_run;
-            named_bar_sync(bar_id, 2 * kBlockM);
+            named_bar_sync(bar_id, kPairThreads);
             const float l_tot = l_run + lrow[(hf ^ 1) * kBlockM];
 
             constexpr int kOutCols = kHeadDim / 2;
