@@ -65,7 +65,8 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    # RF_FA_LIB lets a developer point at an experimental build of the same ABI (kernel tuning)
+    return os.environ.get("RF_FA_LIB") or _build.LIB
 
 
 def load(build_if_missing: bool = True):

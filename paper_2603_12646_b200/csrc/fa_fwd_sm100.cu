@@ -49,6 +49,10 @@ constexpr int kMmaWarp = 17;
 constexpr int kThreads = 640;  // 5 warpgroups: 4 softmax + 1 (producer, MMA, 2 idle warps)
 constexpr int kHalfN = kBlockN / 2;  // key columns per softmax thread
 constexpr int kRegsSoftmax = 112;
+#ifndef RF_FA_EMU_EVERY
+#define RF_FA_EMU_EVERY 4
+#endif
+constexpr int kEmuEvery = RF_FA_EMU_EVERY;  // every n-th element pair takes the FMA-pipe exp2 (0 = none)
 constexpr int kRegsOther = 32;  // 128*32 + 512*112 == 640*96: the CTA register pool balances exactly
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;    // + 128 * buffer
@@ -79,17 +83,20 @@ enum : uint32_t {
 };
 static_assert(kNumBars * 8 + 8 <= Smem::bar_bytes, "barrier block too small");
 
-__device__ __forceinline__ bool tile_live(const FaParams& p, int b, int n) {
-    return p.tile_flags == nullptr || p.tile_flags[b * p.n_kv_tiles + n] != kTileSkip;
+template <bool kHasBias>
+__device__ __forceinline__ bool tile_live_t(const FaParams& p, int b, int n) {
+    return !kHasBias || p.tile_flags[b * p.n_kv_tiles + n] != kTileSkip;
 }
+#define tile_live(p, b, n) tile_live_t<kHasBias>(p, b, n)
 
-template <bool kBf16>
+template <bool kBf16, bool kHasBias>
 __global__ void __launch_bounds__(kThreads, 1)
 fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const FaParams p) {
     extern __shared__ uint8_t smem_raw[];
-    const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
+    asm volatile("mov.u32 %0, %0;" : "+r"(smem_base));  // keep in a register: do not rematerialise
     const uint32_t bars = smem_base + Smem::bars;
     auto bar = [&](uint32_t i) { return bars + 8u * i; };
     volatile uint32_t* tmem_slot =
@@ -307,48 +314,70 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         float m_ref = -CUDART_INF_F;
         float l_run = 0.f;  // this thread's share of the row sum (its 64 columns of every tile)
 
+        // key tiles [nf0, nf1) need no window / range predicate for any row of this query tile
+        int nf0, nf1;
+        {
+            int lo_key = p.kv_begin, hi_key = kv_end_eff - kBlockN;  // bounds on the tile's first key
+            if (p.wl >= 0) lo_key = max(lo_key, tile_r_hi - p.wl);
+            if (p.wr >= 0) hi_key = min(hi_key, tile_r_lo + p.wr - (kBlockN - 1));
+            nf0 = (lo_key + kBlockN - 1) >> 7;
+            nf1 = hi_key >= 0 ? (hi_key >> 7) + 1 : 0;
+        }
+        const uint8_t* flags_row = kHasBias ? p.tile_flags + b * p.n_kv_tiles : nullptr;
+        const uint32_t t_sbase = tmem_base + lane_base + kColS;
+        uint32_t bars_r = bars;
+        asm volatile("mov.u32 %0, %0;" : "+r"(bars_r));
+        float* xrow_base = xchg + (x * 2) * kBlockM + r;
+
         if (active) {
             int it = 0;
+            int sb = x;               // S/P buffer of tile g = 2*it + x is g % 3 ...
+            uint32_t sb_par = 0;      // ... and its barrier phase parity is (g / 3) & 1
+            uint32_t xpar = 0;        // exchange double buffer
             for (int n = n0; n < n1; ++n) {
-                if (!tile_live(p, b, n)) continue;
+                uint8_t flag = kTileFull;
+                if (kHasBias) {
+                    flag = flags_row[n];
+                    if (flag == kTileSkip) continue;
+                }
                 const int kv0 = n * kBlockN;
-                const int sb = (2 * it + x) % kSBufs;  // S/P buffer of this tile
-                const uint32_t t_s = tmem_base + lane_base + kColS + sb * kBlockN;
-                mbar_wait(bar(kBarSFull + sb), ((2 * it + x) / kSBufs) & 1);
+                const uint32_t t_s = t_sbase + sb * kBlockN;
+                mbar_wait(bars_r + 8u * (kBarSFull + sb), sb_par);
                 tc_fence_after();
 
-                float s[kHalfN];
-                {
-                    uint32_t(&su)[kHalfN] = reinterpret_cast<uint32_t(&)[kHalfN]>(s);
+                uint32_t su[kHalfN];
 #pragma unroll
-                    for (int cb = 0; cb < kHalfN / 32; ++cb)
-                        tmem_ld32(t_s + hf * kHalfN + cb * 32, reinterpret_cast<uint32_t(&)[32]>(su[cb * 32]));
-                    tc_wait_ld();
-                }
+                for (int cb = 0; cb < kHalfN / 32; ++cb)
+                    tmem_ld32(t_s + hf * kHalfN + cb * 32, reinterpret_cast<uint32_t(&)[32]>(su[cb * 32]));
+                tc_wait_ld();
                 if (p.debug_scores != nullptr && it == 0) {
                     const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
                     float* dst = p.debug_scores + ((cta * 2 + x) * kBlockM + r) * kBlockN + hf * kHalfN;
 #pragma unroll
-                    for (int j = 0; j < kHalfN; ++j) dst[j] = s[j];
+                    for (int j = 0; j < kHalfN; ++j) dst[j] = __uint_as_float(su[j]);
                 }
 
                 // tile class (warp-uniform): "full" tiles need no per-element predicate
-                uint8_t flag = kTileFull;
-                if (p.tile_flags != nullptr) flag = p.tile_flags[b * p.n_kv_tiles + n];
-                const bool full = flag == kTileFull && kv0 >= p.kv_begin && kv0 + kBlockN <= kv_end_eff &&
-                                  (p.wl < 0 || tile_r_hi - kv0 <= p.wl) &&
-                                  (p.wr < 0 || kv0 + kBlockN - 1 - tile_r_lo <= p.wr);
+                const bool full = (n >= nf0) && (n < nf1) && (flag == kTileFull);
 
                 float my_max;
                 float mul;
                 if (full) {
-                    float mx0 = s[0], mx1 = s[1];
+                    float mx[4];
 #pragma unroll
-                    for (int j = 2; j < kHalfN; j += 4) {
-                        mx0 = max3(mx0, s[j], s[j + 1]);
-                        if (j + 3 < kHalfN) mx1 = max3(mx1, s[j + 2], s[j + 3]);
+                    for (int q4 = 0; q4 < 4; ++q4) mx[q4] = __uint_as_float(su[q4]);
+#pragma unroll
+                    for (int j = 4; j < kHalfN; j += 8) {
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            const int j0 = j + 2 * q4;
+                            if (j0 + 1 < kHalfN)
+                                mx[q4] = max3(mx[q4], __uint_as_float(su[j0]), __uint_as_float(su[j0 + 1]));
+                        }
                     }
-                    my_max = fmaxf(mx0, mx1) * c;  // scale > 0 (validated on the host)
+                    // elements kHalfN-4 .. kHalfN-1 when (kHalfN - 4) % 8 != 0 are covered above:
+                    // j runs 4,12,...,60 and j0 spans j..j+7 < 68 -> guarded by j0 + 1 < kHalfN
+                    my_max = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * c;  // scale > 0 (host-checked)
                     mul = c;
                 } else {
                     // live columns of this row inside the tile: [lo, hi]
@@ -357,21 +386,22 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     if (p.wr >= 0) hi = min(hi, row + p.wr);
                     lo -= kv0 + hf * kHalfN;
                     hi -= kv0 + hf * kHalfN;
-                    const float* brow = (flag == kTileMixed && p.bias2 != nullptr)
+                    const float* brow = (kHasBias && flag == kTileMixed)
                                             ? p.bias2 + static_cast<size_t>(b) * p.bias_stride + kv0 + hf * kHalfN
                                             : nullptr;
                     float mx = -CUDART_INF_F;
 #pragma unroll
                     for (int j4 = 0; j4 < kHalfN; j4 += 4) {
                         float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (brow != nullptr) bb = __ldg(reinterpret_cast<const float4*>(brow + j4));
+                        if (kHasBias && brow != nullptr) bb = __ldg(reinterpret_cast<const float4*>(brow + j4));
                         const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int j = j4 + u;
-                            const float xs = fmaf(s[j], c, bv[u]);  // bias -inf => masked key
-                            s[j] = (j >= lo && j <= hi) ? xs : -CUDART_INF_F;
-                            mx = fmaxf(mx, s[j]);
+                            const float xs = fmaf(__uint_as_float(su[j]), c, bv[u]);  // bias -inf => masked key
+                            const float xm = (j >= lo && j <= hi) ? xs : -CUDART_INF_F;
+                            su[j] = __float_as_uint(xm);
+                            mx = fmaxf(mx, xm);
                         }
                     }
                     my_max = mx;
@@ -381,7 +411,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 // row max over both halves: exchange through smem (double-buffered by tile parity).
                 // The barrier also orders every S read of this tile before any P write below
                 // (P aliases the first 64 columns of the S buffer, which belong to half 0).
-                float* xrow = xchg + (((it & 1) * 2 + x) * 2) * kBlockM + r;
+                float* xrow = xrow_base + xpar * (4 * kBlockM);
                 xrow[hf * kBlockM] = my_max;
                 named_bar_sync(bar_id, kPairThreads);
                 const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
@@ -391,21 +421,27 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const float alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
                 const float neg_m = (m_new == -CUDART_INF_F) ? 0.f : -m_new;
 
-                float sum0 = 0.f, sum1 = 0.f;
+                // P = 2^(s*mul - m)
+                uint64_t sum2 = 0;  // packed (0.f, 0.f)
+                const uint64_t mul2 = bc2(mul), negm2 = bc2(neg_m);
 #pragma unroll
                 for (int cb = 0; cb < kHalfN / 32; ++cb) {
                     uint32_t pk[16];
 #pragma unroll
                     for (int u = 0; u < 16; ++u) {
-                        float x0, x1;
-                        ffma2(x0, x1, s[cb * 32 + 2 * u], s[cb * 32 + 2 * u + 1], mul, neg_m);
-                        const float p0 = ex2(x0);
-                        const float p1 = ex2(x1);
-                        fadd2(sum0, sum1, p0, p1);
+                        float p0, p1;
+                        unpk2(ffma2v(pk2(__uint_as_float(su[cb * 32 + 2 * u]), __uint_as_float(su[cb * 32 + 2 * u + 1])),
+                                     mul2, negm2),
+                              p0, p1);
+                        p0 = ex2(p0);
+                        p1 = ex2(p1);
+                        sum2 = fadd2v(sum2, pk2(p0, p1));
                         pk[u] = pack2<kBf16>(p0, p1);
                     }
                     tmem_st16(t_s + hf * (kHalfN / 2) + cb * 16, pk);
                 }
+                float sum0, sum1;
+                unpk2(sum2, sum0, sum1);
                 l_run = l_run * alpha + (sum0 + sum1);
                 m_ref = m_new;
 
@@ -427,13 +463,19 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 }
                 tc_wait_st();
                 tc_fence_before();
-                mbar_arrive(bar(kBarPFull + sb));
+                mbar_arrive(bars_r + 8u * (kBarPFull + sb));
                 ++it;
+                xpar ^= 1u;
+                sb += 2;
+                if (sb >= kSBufs) {
+                    sb -= kSBufs;
+                    sb_par ^= 1u;
+                }
             }
 
             // ---------------- epilogue ----------------
             // combine the two halves' row sums, then each half writes its 32 output columns
-            float* lrow = xchg + ((0 * 2 + x) * 2) * kBlockM + r;
+            float* lrow = xrow_base;
             named_bar_sync(bar_id, kPairThreads);  // all max-exchange reads of the last tile are done
             lrow[hf * kBlockM] = l_run;
             named_bar_sync(bar_id, kPairThreads);
@@ -507,8 +549,10 @@ size_t fa_fwd_sm100_smem_bytes() {
 
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
                                 const FaParams& p, bool bf16, cudaStream_t stream, int* grid_ctas) {
+    const bool has_bias = p.tile_flags != nullptr;
     void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const FaParams) =
-        bf16 ? fa_fwd_sm100_kernel<true> : fa_fwd_sm100_kernel<false>;
+        bf16 ? (has_bias ? fa_fwd_sm100_kernel<true, true> : fa_fwd_sm100_kernel<true, false>)
+             : (has_bias ? fa_fwd_sm100_kernel<false, true> : fa_fwd_sm100_kernel<false, false>);
     const size_t smem = fa_fwd_sm100_smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;

@@ -247,6 +247,54 @@ __device__ __forceinline__ void fmul2(float& d0, float& d1, float b) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(a));
 }
 
+// 64-bit register-pair forms (avoid pack/unpack moves when chaining packed ops)
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ uint64_t bc2(float v) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(v));
+    return r;
+}
+__device__ __forceinline__ void unpk2(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2v(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2v(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// 2^x for two lanes on the FMA/ALU pipes only (no MUFU): Cody-Waite split x = n + f with the
+// 1.5*2^23 rounding trick, degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (max relative
+// error 7.5e-5, far below the bf16 rounding applied to P afterwards), exponent insertion by an
+// integer add.  x <= ~100; -inf (masked) is clamped to -126 and yields ~1e-38 (a denormal that
+// flushes to 0 in the bf16 pack).
+__device__ __forceinline__ void exp2_poly2(float& x0, float& x1) {
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+    x0 = fmaxf(x0, -126.0f);
+    x1 = fmaxf(x1, -126.0f);
+    const uint64_t x = pk2(x0, x1);
+    const uint64_t t = fadd2v(x, bc2(kMagic));            // low mantissa bits = round(x)
+    const uint64_t r = fadd2v(t, bc2(-kMagic));           // round(x) as float
+    const uint64_t f = ffma2v(r, bc2(-1.0f), x);          // x - round(x) in [-0.5, 0.5]
+    uint64_t pl = ffma2v(f, bc2(0.055171459913253784f), bc2(0.2426108568906784f));
+    pl = ffma2v(pl, f, bc2(0.6932609677314758f));
+    pl = ffma2v(pl, f, bc2(0.9999281167984009f));
+    float t0, t1, p0, p1;
+    unpk2(t, t0, t1);
+    unpk2(pl, p0, p1);
+    x0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+    x1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
 // named barrier among a subset of the CTA's warps (id 1..15; id 0 is __syncthreads)
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
