@@ -138,11 +138,52 @@ int select_kernel(const rf_fa_params* p, const Resolved& r, int* kernel) {
 int64_t n_kv_tiles(int64_t S) { return (S + rf::kBlockN - 1) / rf::kBlockN; }
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-size_t workspace_bytes_for(const rf_fa_params* p, int kernel) {
-    if (kernel != RF_KERNEL_TCGEN05 || p->pad_bias == nullptr || p->B == 0 || p->S == 0) return 0;
-    const size_t nt = static_cast<size_t>(n_kv_tiles(p->S));
-    return align_up(static_cast<size_t>(p->B) * nt * rf::kBlockN * sizeof(float), 256) +
-           align_up(static_cast<size_t>(p->B) * nt, 256);
+// SM count of the current device (148 on B200; also the answer when no device is visible, so
+// that workspace queries work on a CPU-only build box).
+int sm_count_or_default() {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+        return sms;
+    cudaGetLastError();  // clear the sticky "no device" status
+    return 148;
+}
+
+struct Plan {
+    int kernel;
+    int sched_mode;   // tcgen05 only
+    int grid;         // CTAs
+    int64_t total_pairs, pairs_per_head;
+    size_t bias_bytes, flag_bytes_bias, part_bytes;
+    size_t workspace_bytes() const { return bias_bytes + flag_bytes_bias + part_bytes; }
+};
+
+Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
+    Plan pl{};
+    pl.kernel = kernel;
+    if (p->B == 0 || p->H == 0 || p->S == 0) return pl;
+    if (kernel != RF_KERNEL_TCGEN05) {
+        pl.grid = static_cast<int>(((p->S + 31) / 32) * p->H * p->B);
+        return pl;
+    }
+    pl.pairs_per_head = (p->S + rf::kRowsPerCta - 1) / rf::kRowsPerCta;
+    pl.total_pairs = pl.pairs_per_head * p->H * p->B;
+    pl.grid = static_cast<int>(pl.total_pairs);
+    if (p->pad_bias != nullptr) {
+        const size_t nt = static_cast<size_t>(n_kv_tiles(p->S));
+        pl.bias_bytes = align_up(static_cast<size_t>(p->B) * nt * rf::kBlockN * sizeof(float), 256);
+        pl.flag_bytes_bias = align_up(static_cast<size_t>(p->B) * nt, 256);
+    }
+    // dense global attention over more pairs than SMs: persistent balanced schedule
+    const bool dense = p->pad_bias == nullptr && p->window_left < 0 && p->window_right < 0 && !r.partial &&
+                       r.kv_begin == 0 && r.kv_end == p->S;
+    const int sms = sm_count_or_default();
+    if (dense && pl.total_pairs > sms) {
+        pl.sched_mode = 1;
+        pl.grid = sms;
+        pl.part_bytes = align_up(rf::fa_fwd_sm100_partial_bytes(pl.grid), 256);
+    }
+    return pl;
 }
 
 int make_tmap(CUtensorMap* tm, const void* base, int dtype, int64_t d, int64_t S, int64_t H, int64_t B,
@@ -219,7 +260,7 @@ int rf_fa_fwd_workspace_bytes(const rf_fa_params* p, size_t* bytes) {
     int kernel;
     rc = select_kernel(p, r, &kernel);
     if (rc != RF_OK) return rc;
-    *bytes = workspace_bytes_for(p, kernel);
+    *bytes = make_plan(p, r, kernel).workspace_bytes();
     return RF_OK;
 }
 
@@ -232,8 +273,9 @@ int rf_fa_stats_query(const rf_fa_params* p, rf_fa_stats* st) {
     rc = select_kernel(p, r, &kernel);
     if (rc != RF_OK) return rc;
     std::memset(st, 0, sizeof(*st));
+    const Plan pl = make_plan(p, r, kernel);
     st->kernel = kernel;
-    st->workspace_bytes = workspace_bytes_for(p, kernel);
+    st->workspace_bytes = pl.workspace_bytes();
     st->tile_scratch_bytes = kernel == RF_KERNEL_TCGEN05
                                  ? rf::fa_fwd_sm100_smem_bytes() + 512ull * 128 * 4  // smem + TMEM
                                  : (2ull * 32 * p->d + 32) * sizeof(float);
@@ -241,8 +283,7 @@ int rf_fa_stats_query(const rf_fa_params* p, rf_fa_stats* st) {
     const uint64_t esz = p->out_dtype == RF_DTYPE_F32 ? 4 : 2;
     st->output_bytes = static_cast<uint64_t>(p->B) * p->H * p->S * p->d * (r.partial ? 4 : esz);
     st->score_matrix_bytes = 0;
-    const int64_t rows_per_cta = kernel == RF_KERNEL_TCGEN05 ? rf::kRowsPerCta : 32;
-    st->grid_ctas = static_cast<int32_t>(((p->S + rows_per_cta - 1) / rows_per_cta) * p->H * p->B);
+    st->grid_ctas = pl.grid;
     return RF_OK;
 }
 
@@ -259,6 +300,7 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     rf::FaParams f;
     fill_fa_params(p, r, &f);
     int grid = 0;
+    (void)grid;
 
     if (kernel == RF_KERNEL_SIMT) {
         rf::SimtParams sp;
@@ -279,25 +321,37 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     }
 
     // ---- tcgen05 path ----
-    const size_t need = workspace_bytes_for(p, kernel);
+    const Plan pl = make_plan(p, r, kernel);
+    const size_t need = pl.workspace_bytes();
     if (need > 0) {
         if (workspace == nullptr || workspace_bytes < need)
             return fail(RF_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
         if (!aligned16(workspace)) return fail(RF_ERR_WORKSPACE, "workspace must be 16-byte aligned");
-        const size_t nt = static_cast<size_t>(f.n_kv_tiles);
-        float* bias2 = static_cast<float*>(workspace);
-        uint8_t* flags = static_cast<uint8_t*>(workspace) +
-                         align_up(static_cast<size_t>(p->B) * nt * rf::kBlockN * sizeof(float), 256);
+    }
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    if (pl.bias_bytes > 0) {
+        float* bias2 = reinterpret_cast<float*>(ws);
+        uint8_t* flags = ws + pl.bias_bytes;
         cudaError_t e = rf::launch_bias_prepare(p->pad_bias, f.B, f.S, bias2, flags, f.n_kv_tiles, stream);
         if (e != cudaSuccess) return cuda_fail(e, "bias_prepare launch");
         f.bias2 = bias2;
         f.tile_flags = flags;
     }
+    f.sched_mode = pl.sched_mode;
+    f.total_pairs = static_cast<int>(pl.total_pairs);
+    f.pairs_per_head = static_cast<int>(pl.pairs_per_head);
+    if (pl.sched_mode == 1) {
+        void* flag_ptr = nullptr;
+        size_t flag_bytes = 0;
+        rf::fa_fwd_sm100_partial_carve(ws + pl.bias_bytes + pl.flag_bytes_bias, pl.grid, &f, &flag_ptr, &flag_bytes);
+        cudaError_t e = cudaMemsetAsync(flag_ptr, 0, flag_bytes, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(partial flags)");
+    }
     CUtensorMap tmq, tmk, tmv;
     if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
-    cudaError_t e = rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, stream, &grid);
+    cudaError_t e = rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100 launch");
     return RF_OK;
 }

@@ -5,30 +5,37 @@
 // online softmax, rows without a live key -> 0.  No S x S tensor is ever materialised.
 //
 // Hardware mapping (one CTA per SM, 640 threads, two 128-row query tiles "A"/"B" ping-pong):
-//   warp 16     TMA producer: Q once, then K/V 128-key tiles through smem rings
+//   warp 16     TMA producer: Q per work item, K/V 128-key tiles through smem rings
 //               (cp.async.bulk.tensor, 128B swizzle, mbarrier complete_tx)
-//   warp 17     UMMA issuer (one elected lane): S_X = Q_X K^T  (tcgen05.mma SS, M128 N128 K16 x4)
-//                                               O_X += P_X V   (tcgen05.mma TS, M128 N64  K16 x8)
-//               accumulators in TMEM: three rotating S buffers, cols [0,384) (tile g = 2*it + X of
+//   warp 17     UMMA issuer: S_X = Q_X K^T  (tcgen05.mma SS, M128 N128 K16 x4)
+//                            O_X += P_X V   (tcgen05.mma TS, M128 N64  K16 x8)
+//               accumulators in TMEM: three rotating S buffers, cols [0,384) (tile g = 2*t + X of
 //               the A,B,A,B,... sequence uses buffer g % 3, so the next S of a warpgroup is computed
 //               while it is still busy with the current one), O_A [384,448), O_B [448,512);
 //               P (bf16) aliases the first 64 columns of its S buffer.
 //   warps 0-7   softmax for tile A, warps 8-15 for tile B.  Two threads share one query row
 //               (key columns [0,64) and [64,128) of the tile; tcgen05.ld 32x32b), so four softmax
 //               warps per SM sub-partition hide each other's MUFU/ALU latencies.  The two halves
-//               exchange their row max through shared memory (one named barrier per tile); row
-//               sums stay per-thread until the epilogue.  exp2 with the scale folded in, packed
-//               f32x2 math, lazy rescale of O (only when the running max grows by > 2^8).
+//               exchange their row max through shared memory (one 64-thread named barrier per
+//               tile); row sums stay per-thread until the epilogue.  exp2 with the scale folded in,
+//               packed f32x2 math, lazy rescale of O (only when the running max grows by > 2^8).
 //               setmaxnreg moves registers from the producer/MMA warpgroup to the softmax ones.
-// K/V are loaded once per 256 query rows; the tensor pipe and the MUFU pipe overlap because
-// tile A's softmax runs while tile B's MMAs execute and vice versa.
+//
+// Work distribution.  A work item is (query-tile pair, key-tile range).
+//   mode 0: one item per CTA (grid = number of pairs); used with windows, padding bias, split-KV.
+//   mode 1: persistent, statically balanced: the flat (pair x key-tile) iteration space is cut
+//           into gridDim.x equal contiguous slices.  A pair cut between CTA c (its first key
+//           tiles, processed LAST by c) and CTA c+1 (its remaining key tiles, processed FIRST by
+//           c+1) is merged in-kernel: c+1 publishes an un-normalised partial (O, m, l) to the
+//           workspace, c combines it with its own in a fixed order.  This removes the wave
+//           quantisation of the dense global layers (e.g. 384 pairs on 148 SMs) and stays
+//           run-to-run deterministic.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
-#include <stdio.h>
 
 #include "fa_internal.h"
 #include "ptx.cuh"
@@ -46,14 +53,10 @@ constexpr int kTileBytes = kBlockN * kHeadDim * 2;  // 16 KiB: one 128 x 64 16-b
 constexpr int kNumSoftmaxWarps = 16;
 constexpr int kProducerWarp = 16;
 constexpr int kMmaWarp = 17;
-constexpr int kThreads = 640;  // 5 warpgroups: 4 softmax + 1 (producer, MMA, 2 idle warps)
+constexpr int kThreads = 640;        // 5 warpgroups: 4 softmax + 1 (producer, MMA, 2 idle warps)
 constexpr int kHalfN = kBlockN / 2;  // key columns per softmax thread
 constexpr int kRegsSoftmax = 112;
-#ifndef RF_FA_EMU_EVERY
-#define RF_FA_EMU_EVERY 4
-#endif
-constexpr int kEmuEvery = RF_FA_EMU_EVERY;  // every n-th element pair takes the FMA-pipe exp2 (0 = none)
-constexpr int kRegsOther = 32;  // 128*32 + 512*112 == 640*96: the CTA register pool balances exactly
+constexpr int kRegsOther = 32;       // 128*32 + 512*112 == 640*96: the CTA register pool balances exactly
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;    // + 128 * buffer
 constexpr uint32_t kColO = 384;  // + 64 * X
@@ -72,7 +75,8 @@ struct Smem {
 // barrier indices inside the barrier block (8 bytes each)
 enum : uint32_t {
     kBarQFull = 0,
-    kBarKFull = 1,                       // [kStagesK]
+    kBarQEmpty = 1,
+    kBarKFull = 2,                       // [kStagesK]
     kBarKEmpty = kBarKFull + kStagesK,   // [kStagesK]
     kBarVFull = kBarKEmpty + kStagesK,   // [kStagesV]
     kBarVEmpty = kBarVFull + kStagesV,   // [kStagesV]
@@ -83,11 +87,86 @@ enum : uint32_t {
 };
 static_assert(kNumBars * 8 + 8 <= Smem::bar_bytes, "barrier block too small");
 
+enum : int { kItemFull = 0, kItemHeadPart = 1, kItemTailPart = 2 };
+
+// One unit of work of a CTA: a query-tile pair and a range of key tiles.
+struct Item {
+    int b, h, q0;
+    int n0, n1;    // key tiles [n0, n1)
+    int num_live;  // tiles in the range that are not fully padded
+    int kind;
+    bool has_b;
+};
+
+struct Sched {
+    long long t, t_end;  // mode 1: flat (pair, key tile) cursor
+    bool done;           // mode 0
+};
+
 template <bool kHasBias>
-__device__ __forceinline__ bool tile_live_t(const FaParams& p, int b, int n) {
+__device__ __forceinline__ bool tile_live(const FaParams& p, int b, int n) {
     return !kHasBias || p.tile_flags[b * p.n_kv_tiles + n] != kTileSkip;
 }
-#define tile_live(p, b, n) tile_live_t<kHasBias>(p, b, n)
+
+__device__ __forceinline__ void sched_init(const FaParams& p, Sched& s) {
+    s.done = false;
+    if (p.sched_mode == 1) {
+        const long long total = static_cast<long long>(p.total_pairs) * p.n_kv_tiles;
+        s.t = total * blockIdx.x / gridDim.x;
+        s.t_end = total * (blockIdx.x + 1) / gridDim.x;
+    } else {
+        s.t = s.t_end = 0;
+    }
+}
+
+template <bool kHasBias>
+__device__ __forceinline__ bool next_item(const FaParams& p, Sched& s, Item& it) {
+    int pair_lin;
+    if (p.sched_mode == 1) {
+        if (s.t >= s.t_end) return false;
+        const int K = p.n_kv_tiles;
+        pair_lin = static_cast<int>(s.t / K);
+        const int k0 = static_cast<int>(s.t - static_cast<long long>(pair_lin) * K);
+        const int k1 = static_cast<int>(min(static_cast<long long>(K), k0 + (s.t_end - s.t)));
+        s.t += k1 - k0;
+        it.n0 = k0;
+        it.n1 = k1;
+        it.num_live = k1 - k0;
+        it.kind = k0 > 0 ? kItemHeadPart : (k1 < K ? kItemTailPart : kItemFull);
+    } else {
+        if (s.done) return false;
+        s.done = true;
+        pair_lin = blockIdx.x;
+    }
+    const int px = pair_lin % p.pairs_per_head;
+    const int bh = pair_lin / p.pairs_per_head;
+    it.h = bh % p.H;
+    it.b = bh / p.H;
+    it.q0 = px * kRowsPerCta;
+    it.has_b = it.q0 + kBlockM < p.S;
+    if (p.sched_mode != 1) {
+        // key-tile range of this pair (union over its rows of window and split range)
+        const int rows_end = min(it.q0 + kRowsPerCta, p.S);
+        int j_lo = p.kv_begin, j_hi = p.kv_end;
+        if (p.wl >= 0) j_lo = max(j_lo, it.q0 - p.wl);
+        if (p.wr >= 0) j_hi = min(j_hi, rows_end + p.wr);
+        it.n0 = j_lo >> 7;
+        it.n1 = (j_hi > j_lo) ? ((j_hi + kBlockN - 1) >> 7) : it.n0;
+        it.num_live = 0;
+        for (int n = it.n0; n < it.n1; ++n) it.num_live += tile_live<kHasBias>(p, it.b, n) ? 1 : 0;
+        it.kind = kItemFull;
+    }
+    return true;
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
 
 template <bool kBf16, bool kHasBias>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -104,20 +183,6 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int q0 = blockIdx.x * kRowsPerCta;
-    const int h = blockIdx.y;
-    const int b = blockIdx.z;
-    const bool has_b = q0 + kBlockM < p.S;
-    const int rows_end = min(q0 + kRowsPerCta, p.S);
-
-    // key-tile range of this CTA (union over its rows of window and split range)
-    int j_lo = p.kv_begin, j_hi = p.kv_end;
-    if (p.wl >= 0) j_lo = max(j_lo, q0 - p.wl);
-    if (p.wr >= 0) j_hi = min(j_hi, rows_end + p.wr);
-    const int n0 = j_lo >> 7;
-    const int n1 = (j_hi > j_lo) ? ((j_hi + kBlockN - 1) >> 7) : n0;
-    int num_live = 0;
-    for (int n = n0; n < n1; ++n) num_live += tile_live(p, b, n) ? 1 : 0;
 
     // ---------------- prologue ----------------
     if (warp == kProducerWarp && lane == 0) {
@@ -125,6 +190,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         prefetch_tensormap(&tm_k);
         prefetch_tensormap(&tm_v);
         mbar_init(bar(kBarQFull), 1);
+        mbar_init(bar(kBarQEmpty), 1);
         for (int s = 0; s < kStagesK; ++s) {
             mbar_init(bar(kBarKFull + s), 1);
             mbar_init(bar(kBarKEmpty + s), 1);
@@ -149,45 +215,68 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    Sched sched;
+    sched_init(p, sched);
+    Item item;
+
     static_assert(128 * kRegsOther + 512 * kRegsSoftmax <= kThreads * 96, "setmaxnreg pool must balance");
     if (warp >= kNumSoftmaxWarps) setmaxnreg_dec<kRegsOther>();
+
     if (warp == kProducerWarp) {
         // =============================== TMA producer ===============================
-        if (lane == 0 && num_live > 0) {
-            mbar_arrive_expect_tx(bar(kBarQFull), has_b ? 2 * kTileBytes : kTileBytes);
-            tma_load_4d(smem_base + Smem::q, &tm_q, bar(kBarQFull), 0, q0, h, b);
-            if (has_b) tma_load_4d(smem_base + Smem::q + kTileBytes, &tm_q, bar(kBarQFull), 0, q0 + kBlockM, h, b);
-            // K runs two tiles ahead of V: QK^T of tile it+2 is issued while tile it is in softmax
-            auto load_k = [&](int it, int n) {
-                const int st = it % kStagesK;
-                const uint32_t ph = (it / kStagesK) & 1;
-                mbar_wait(bar(kBarKEmpty + st), ph ^ 1);
-                mbar_arrive_expect_tx(bar(kBarKFull + st), kTileBytes);
-                tma_load_4d(smem_base + Smem::k + st * kTileBytes, &tm_k, bar(kBarKFull + st), 0, n * kBlockN, h, b);
+        // warp-uniform control flow; only the TMA / expect_tx instructions are predicated
+        const bool leader = elect_one() != 0;
+        uint32_t qi = 0;  // items with work so far (Q barrier phase)
+        uint32_t kc = 0;  // K tiles loaded so far (ring position)
+        uint32_t vc = 0;  // V tiles loaded so far
+        while (next_item<kHasBias>(p, sched, item)) {
+            if (item.num_live == 0) continue;
+            const int b = item.b, h = item.h;
+            mbar_wait(bar(kBarQEmpty), (qi & 1) ^ 1);
+            if (leader) {
+                mbar_arrive_expect_tx(bar(kBarQFull), item.has_b ? 2 * kTileBytes : kTileBytes);
+                tma_load_4d(smem_base + Smem::q, &tm_q, bar(kBarQFull), 0, item.q0, h, b);
+                if (item.has_b)
+                    tma_load_4d(smem_base + Smem::q + kTileBytes, &tm_q, bar(kBarQFull), 0, item.q0 + kBlockM, h, b);
+            }
+            __syncwarp();
+            ++qi;
+            // K runs two tiles ahead of V: QK^T of tile t+2 is issued while tile t is in softmax
+            auto load_k = [&](int n) {
+                const uint32_t st = kc % kStagesK;
+                mbar_wait(bar(kBarKEmpty + st), ((kc / kStagesK) & 1) ^ 1);
+                if (leader) {
+                    mbar_arrive_expect_tx(bar(kBarKFull + st), kTileBytes);
+                    tma_load_4d(smem_base + Smem::k + st * kTileBytes, &tm_k, bar(kBarKFull + st), 0, n * kBlockN, h, b);
+                }
+                __syncwarp();
+                ++kc;
             };
-            auto load_v = [&](int it, int n) {
-                const int st = it % kStagesV;
-                const uint32_t ph = (it / kStagesV) & 1;
-                mbar_wait(bar(kBarVEmpty + st), ph ^ 1);
-                mbar_arrive_expect_tx(bar(kBarVFull + st), kTileBytes);
-                tma_load_4d(smem_base + Smem::v + st * kTileBytes, &tm_v, bar(kBarVFull + st), 0, n * kBlockN, h, b);
+            auto load_v = [&](int n) {
+                const uint32_t st = vc % kStagesV;
+                mbar_wait(bar(kBarVEmpty + st), ((vc / kStagesV) & 1) ^ 1);
+                if (leader) {
+                    mbar_arrive_expect_tx(bar(kBarVFull + st), kTileBytes);
+                    tma_load_4d(smem_base + Smem::v + st * kTileBytes, &tm_v, bar(kBarVFull + st), 0, n * kBlockN, h, b);
+                }
+                __syncwarp();
+                ++vc;
             };
             auto next_live = [&](int n) {
-                while (n < n1 && !tile_live(p, b, n)) ++n;
+                while (n < item.n1 && !tile_live<kHasBias>(p, b, n)) ++n;
                 return n;
             };
-            int nk = next_live(n0), itk = 0;  // K cursor
-            for (int pre = 0; pre < 2 && nk < n1; ++pre) {
-                load_k(itk++, nk);
+            int nk = next_live(item.n0);
+            for (int pre = 0; pre < 2 && nk < item.n1; ++pre) {
+                load_k(nk);
                 nk = next_live(nk + 1);
             }
-            int itv = 0;
-            for (int n = next_live(n0); n < n1; n = next_live(n + 1)) {
-                if (nk < n1) {
-                    load_k(itk++, nk);
+            for (int n = next_live(item.n0); n < item.n1; n = next_live(n + 1)) {
+                if (nk < item.n1) {
+                    load_k(nk);
                     nk = next_live(nk + 1);
                 }
-                load_v(itv++, n);
+                load_v(n);
             }
         }
     } else if (warp == kMmaWarp) {
@@ -197,29 +286,38 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         // one elected lane.  A divergent `if (lane == 0)` around the loop would make ptxas wrap
         // every UTCHMMA in an ELECT / R2UR waterfall loop, which puts ~16 instructions per MMA on
         // the critical path.
-        if (num_live > 0) {
-            const bool leader = elect_one() != 0;
-            constexpr uint32_t fmt = kBf16 ? 1u : 0u;
-            constexpr uint32_t idesc_qk = make_idesc_f16(fmt, 0, 0, kBlockM, kBlockN);
-            constexpr uint32_t idesc_pv = make_idesc_f16(fmt, 0, 1, kBlockM, kHeadDim);
-            // descriptor high words are constants; the low word is (address >> 4) | LBO field
-            constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (kSwizzle128B << 29);  // SBO, version, swizzle
-            constexpr uint32_t kLboK = (16u >> 4) << 16;                                    // K-major operands
-            constexpr uint32_t kLboV = (static_cast<uint32_t>(kTileBytes) >> 4) << 16;      // MN-major V
-            const uint32_t sb16 = smem_base >> 4;
-            auto desc = [&](uint32_t lo) { return (static_cast<uint64_t>(kDescHi) << 32) | lo; };
+        const bool leader = elect_one() != 0;
+        constexpr uint32_t fmt = kBf16 ? 1u : 0u;
+        constexpr uint32_t idesc_qk = make_idesc_f16(fmt, 0, 0, kBlockM, kBlockN);
+        constexpr uint32_t idesc_pv = make_idesc_f16(fmt, 0, 1, kBlockM, kHeadDim);
+        // descriptor high words are constants; the low word is (address >> 4) | LBO field
+        constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (kSwizzle128B << 29);  // SBO, version, swizzle
+        constexpr uint32_t kLboK = (16u >> 4) << 16;                                    // K-major operands
+        constexpr uint32_t kLboV = (static_cast<uint32_t>(kTileBytes) >> 4) << 16;      // MN-major V
+        const uint32_t sb16 = smem_base >> 4;
+        auto desc = [&](uint32_t lo) { return (static_cast<uint64_t>(kDescHi) << 32) | lo; };
+        auto commit = [&](uint32_t b_) {
+            if (leader) tc_commit(b_);
+            __syncwarp();
+        };
 
-            // tile g = 2*it + x of the A,B,A,B,... sequence lives in S buffer g % 3
-            auto sbuf = [](int it, int x) { return (2 * it + x) % kSBufs; };
-            auto suse_parity = [](int it, int x) { return static_cast<uint32_t>(((2 * it + x) / kSBufs) & 1); };
+        uint32_t qi = 0, kc = 0, vc = 0, tc = 0;  // items / K tiles / V tiles / tiles consumed so far
+        while (next_item<kHasBias>(p, sched, item)) {
+            const int num_live = item.num_live;
+            if (num_live == 0) continue;
+            const bool has_b = item.has_b;
+
+            // tile g = 2*t + x of the A,B,A,B,... sequence lives in S buffer g % 3
+            auto sbuf = [&](int i, int x) { return (2 * (tc + i) + x) % kSBufs; };
+            auto suse_parity = [&](int i, int x) { return ((2 * (tc + i) + x) / kSBufs) & 1u; };
 
             // S = Q_X * K^T : both operands K-major (head dim contiguous), 128B swizzle,
             // 8-row core-matrix groups 1024 B apart; a K=16 step advances 32 B inside the atom.
-            auto issue_qk = [&](int x, int it) {
+            auto issue_qk = [&](int x, int i) {
                 const uint32_t qlo = kLboK | (sb16 + (Smem::q + x * kTileBytes) / 16);
-                const uint32_t klo = kLboK | (sb16 + (Smem::k + (it % kStagesK) * kTileBytes) / 16);
-                const uint32_t td = tmem_base + kColS + sbuf(it, x) * kBlockN;
-                const uint32_t sbar = bar(kBarSFull + sbuf(it, x));
+                const uint32_t klo = kLboK | (sb16 + (Smem::k + ((kc + i) % kStagesK) * kTileBytes) / 16);
+                const uint32_t td = tmem_base + kColS + sbuf(i, x) * kBlockN;
+                const uint32_t sbar = bar(kBarSFull + sbuf(i, x));
                 if (leader) {
 #pragma unroll
                     for (int kk = 0; kk < kHeadDim / 16; ++kk)
@@ -231,11 +329,11 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // O_X += P * V : B operand V is [key][d] with d contiguous = MN-major, 128B swizzle;
             // 8-key groups 1024 B apart (SBO); a K=16 step advances 16 keys = 2048 B.
             // A = P from TMEM: 16 bf16 per row per step = 8 packed 32-bit columns.
-            auto issue_pv = [&](int x, int it) {
-                const uint32_t vlo = kLboV | (sb16 + (Smem::v + (it % kStagesV) * kTileBytes) / 16);
+            auto issue_pv = [&](int x, int i) {
+                const uint32_t vlo = kLboV | (sb16 + (Smem::v + ((vc + i) % kStagesV) * kTileBytes) / 16);
                 const uint32_t td = tmem_base + kColO + x * kHeadDim;
-                const uint32_t ta = tmem_base + kColS + sbuf(it, x) * kBlockN;
-                const uint32_t acc0 = it > 0 ? 1u : 0u;
+                const uint32_t ta = tmem_base + kColS + sbuf(i, x) * kBlockN;
+                const uint32_t acc0 = i > 0 ? 1u : 0u;
                 if (leader) {
 #pragma unroll
                     for (int kk = 0; kk < kBlockN / 16; ++kk)
@@ -243,18 +341,18 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 }
                 __syncwarp();
             };
-            auto commit = [&](uint32_t b_) {
-                if (leader) tc_commit(b_);
-                __syncwarp();
-            };
-            auto wait_k = [&](int it) {
-                mbar_wait(bar(kBarKFull + it % kStagesK), (it / kStagesK) & 1);
+            auto wait_k = [&](int i) {
+                mbar_wait(bar(kBarKFull + (kc + i) % kStagesK), ((kc + i) / kStagesK) & 1);
                 tc_fence_after();
             };
-            auto release_k = [&](int it) { commit(bar(kBarKEmpty + it % kStagesK)); };
+            // every QK^T that reads K tile i has been issued; the last one of the item also frees Q
+            auto release_k = [&](int i) {
+                commit(bar(kBarKEmpty + (kc + i) % kStagesK));
+                if (i == num_live - 1) commit(bar(kBarQEmpty));
+            };
 
             // prologue: S_A(0), S_B(0), and already S_A(1) into the third buffer
-            mbar_wait(bar(kBarQFull), 0);
+            mbar_wait(bar(kBarQFull), qi & 1);
             wait_k(0);
             issue_qk(0, 0);
             if (has_b) issue_qk(1, 0);
@@ -265,270 +363,331 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 if (!has_b) release_k(1);
             }
 
-            for (int it = 0; it < num_live; ++it) {
-                const bool last = it + 1 == num_live;
-                mbar_wait(bar(kBarVFull + it % kStagesV), (it / kStagesV) & 1);
-                // ---- P_A(it) ready: O_A += P_A V; its S buffer is then free for S_B(it+1) ----
-                mbar_wait(bar(kBarPFull + sbuf(it, 0)), suse_parity(it, 0));
+            for (int i = 0; i < num_live; ++i) {
+                const bool last = i + 1 == num_live;
+                mbar_wait(bar(kBarVFull + (vc + i) % kStagesV), ((vc + i) / kStagesV) & 1);
+                // ---- P_A(i) ready: O_A += P_A V; its S buffer is then free for S_B(i+1) ----
+                mbar_wait(bar(kBarPFull + sbuf(i, 0)), suse_parity(i, 0));
                 tc_fence_after();
-                issue_pv(0, it);
+                issue_pv(0, i);
                 if (last) commit(bar(kBarOFull + 0));
                 if (has_b) {
                     if (!last) {
-                        issue_qk(1, it + 1);  // K(it+1) was waited for when S_A(it+1) was issued
-                        release_k(it + 1);
+                        issue_qk(1, i + 1);  // K(i+1) was waited for when S_A(i+1) was issued
+                        release_k(i + 1);
                     }
-                    // ---- P_B(it) ready: O_B += P_B V; its S buffer is then free for S_A(it+2) ----
-                    mbar_wait(bar(kBarPFull + sbuf(it, 1)), suse_parity(it, 1));
+                    // ---- P_B(i) ready: O_B += P_B V; its S buffer is then free for S_A(i+2) ----
+                    mbar_wait(bar(kBarPFull + sbuf(i, 1)), suse_parity(i, 1));
                     tc_fence_after();
-                    issue_pv(1, it);
+                    issue_pv(1, i);
                     if (last) commit(bar(kBarOFull + 1));
                 }
-                commit(bar(kBarVEmpty + it % kStagesV));
-                if (it + 2 < num_live) {
-                    wait_k(it + 2);
-                    issue_qk(0, it + 2);
-                    if (!has_b) release_k(it + 2);
+                commit(bar(kBarVEmpty + (vc + i) % kStagesV));
+                if (i + 2 < num_live) {
+                    wait_k(i + 2);
+                    issue_qk(0, i + 2);
+                    if (!has_b) release_k(i + 2);
                 }
             }
+            kc += num_live;
+            vc += num_live;
+            tc += num_live;
+            ++qi;
         }
     } else if (warp < kNumSoftmaxWarps) {
         // =============================== softmax / epilogue ===============================
         setmaxnreg_inc<kRegsSoftmax>();
-        const int x = warp >> 3;            // 0 = tile A, 1 = tile B
-        const int hf = (warp >> 2) & 1;     // which half of the tile's key columns this thread owns
+        const int x = warp >> 3;               // 0 = tile A, 1 = tile B
+        const int hf = (warp >> 2) & 1;        // which half of the tile's key columns this thread owns
         const int r = (warp & 3) * 32 + lane;  // row inside the tile == TMEM lane
-        const int row = q0 + x * kBlockM + r;
-        const bool active = (x == 0) || has_b;
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const uint32_t t_o = tmem_base + lane_base + kColO + x * kHeadDim + hf * (kHeadDim / 2);
+        const uint32_t t_sbase = tmem_base + lane_base + kColS;
         const int kv_end_eff = min(p.kv_end, p.S);
-        const int tile_r_lo = q0 + x * kBlockM;
-        const int tile_r_hi = tile_r_lo + kBlockM - 1;
         const float c = p.scale_log2;
         float* xchg = reinterpret_cast<float*>(smem_gen + Smem::xchg);
+        float* xrow_base = xchg + (x * 2) * kBlockM + r;
         // named barrier shared by the two warps that own the same 32 rows (ids 1..8)
         const uint32_t bar_id = 1 + x * 4 + (warp & 3);
         constexpr uint32_t kPairThreads = 64;
-
-        float m_ref = -CUDART_INF_F;
-        float l_run = 0.f;  // this thread's share of the row sum (its 64 columns of every tile)
-
-        // key tiles [nf0, nf1) need no window / range predicate for any row of this query tile
-        int nf0, nf1;
-        {
-            int lo_key = p.kv_begin, hi_key = kv_end_eff - kBlockN;  // bounds on the tile's first key
-            if (p.wl >= 0) lo_key = max(lo_key, tile_r_hi - p.wl);
-            if (p.wr >= 0) hi_key = min(hi_key, tile_r_lo + p.wr - (kBlockN - 1));
-            nf0 = (lo_key + kBlockN - 1) >> 7;
-            nf1 = hi_key >= 0 ? (hi_key >> 7) + 1 : 0;
-        }
-        const uint8_t* flags_row = kHasBias ? p.tile_flags + b * p.n_kv_tiles : nullptr;
-        const uint32_t t_sbase = tmem_base + lane_base + kColS;
         uint32_t bars_r = bars;
         asm volatile("mov.u32 %0, %0;" : "+r"(bars_r));
-        float* xrow_base = xchg + (x * 2) * kBlockM + r;
 
-        if (active) {
-            int it = 0;
-            int sb = x;               // S/P buffer of tile g = 2*it + x is g % 3 ...
-            uint32_t sb_par = 0;      // ... and its barrier phase parity is (g / 3) & 1
-            uint32_t xpar = 0;        // exchange double buffer
-            for (int n = n0; n < n1; ++n) {
-                uint8_t flag = kTileFull;
-                if (kHasBias) {
-                    flag = flags_row[n];
-                    if (flag == kTileSkip) continue;
+        uint32_t oi = 0;    // items this warpgroup worked on so far (O barrier phase)
+        uint32_t g = x;     // sequence index 2*t + x of this warpgroup's next tile
+        uint32_t xpar = 0;  // exchange double buffer
+
+        while (next_item<kHasBias>(p, sched, item)) {
+            const int b = item.b, h = item.h;
+            const int num_live = item.num_live;
+            const bool active = (x == 0) || item.has_b;
+            const int tile_r_lo = item.q0 + x * kBlockM;
+            const int tile_r_hi = tile_r_lo + kBlockM - 1;
+            const int row = tile_r_lo + r;
+
+            float m_ref = -CUDART_INF_F;
+            float l_run = 0.f;  // this thread's share of the row sum (its 64 columns of every tile)
+
+            if (active && num_live > 0) {
+                // key tiles [nf0, nf1) need no window / range predicate for any row of this query tile
+                int nf0, nf1;
+                {
+                    int lo_key = p.kv_begin, hi_key = kv_end_eff - kBlockN;  // bounds on the tile's first key
+                    if (p.wl >= 0) lo_key = max(lo_key, tile_r_hi - p.wl);
+                    if (p.wr >= 0) hi_key = min(hi_key, tile_r_lo + p.wr - (kBlockN - 1));
+                    nf0 = (lo_key + kBlockN - 1) >> 7;
+                    nf1 = hi_key >= 0 ? (hi_key >> 7) + 1 : 0;
                 }
-                const int kv0 = n * kBlockN;
-                const uint32_t t_s = t_sbase + sb * kBlockN;
-                mbar_wait(bars_r + 8u * (kBarSFull + sb), sb_par);
-                tc_fence_after();
-
-                uint32_t su[kHalfN];
-#pragma unroll
-                for (int cb = 0; cb < kHalfN / 32; ++cb)
-                    tmem_ld32(t_s + hf * kHalfN + cb * 32, reinterpret_cast<uint32_t(&)[32]>(su[cb * 32]));
-                tc_wait_ld();
-                if (p.debug_scores != nullptr && it == 0) {
-                    const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-                    float* dst = p.debug_scores + ((cta * 2 + x) * kBlockM + r) * kBlockN + hf * kHalfN;
-#pragma unroll
-                    for (int j = 0; j < kHalfN; ++j) dst[j] = __uint_as_float(su[j]);
-                }
-
-                // tile class (warp-uniform): "full" tiles need no per-element predicate
-                const bool full = (n >= nf0) && (n < nf1) && (flag == kTileFull);
-
-                float my_max;
-                float mul;
-                if (full) {
-                    float mx[4];
-#pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) mx[q4] = __uint_as_float(su[q4]);
-#pragma unroll
-                    for (int j = 4; j < kHalfN; j += 8) {
-#pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4) {
-                            const int j0 = j + 2 * q4;
-                            if (j0 + 1 < kHalfN)
-                                mx[q4] = max3(mx[q4], __uint_as_float(su[j0]), __uint_as_float(su[j0 + 1]));
-                        }
+                const uint8_t* flags_row = kHasBias ? p.tile_flags + b * p.n_kv_tiles : nullptr;
+                int sb = g % kSBufs;                 // S/P buffer of the current tile ...
+                uint32_t sb_par = (g / kSBufs) & 1;  // ... and its barrier phase parity
+                int it = 0;
+                for (int n = item.n0; n < item.n1; ++n) {
+                    uint8_t flag = kTileFull;
+                    if (kHasBias) {
+                        flag = flags_row[n];
+                        if (flag == kTileSkip) continue;
                     }
-                    // elements kHalfN-4 .. kHalfN-1 when (kHalfN - 4) % 8 != 0 are covered above:
-                    // j runs 4,12,...,60 and j0 spans j..j+7 < 68 -> guarded by j0 + 1 < kHalfN
-                    my_max = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * c;  // scale > 0 (host-checked)
-                    mul = c;
-                } else {
-                    // live columns of this row inside the tile: [lo, hi]
-                    int lo = p.kv_begin, hi = kv_end_eff - 1;
-                    if (p.wl >= 0) lo = max(lo, row - p.wl);
-                    if (p.wr >= 0) hi = min(hi, row + p.wr);
-                    lo -= kv0 + hf * kHalfN;
-                    hi -= kv0 + hf * kHalfN;
-                    const float* brow = (kHasBias && flag == kTileMixed)
-                                            ? p.bias2 + static_cast<size_t>(b) * p.bias_stride + kv0 + hf * kHalfN
-                                            : nullptr;
-                    float mx = -CUDART_INF_F;
-#pragma unroll
-                    for (int j4 = 0; j4 < kHalfN; j4 += 4) {
-                        float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (kHasBias && brow != nullptr) bb = __ldg(reinterpret_cast<const float4*>(brow + j4));
-                        const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int j = j4 + u;
-                            const float xs = fmaf(__uint_as_float(su[j]), c, bv[u]);  // bias -inf => masked key
-                            const float xm = (j >= lo && j <= hi) ? xs : -CUDART_INF_F;
-                            su[j] = __float_as_uint(xm);
-                            mx = fmaxf(mx, xm);
-                        }
-                    }
-                    my_max = mx;
-                    mul = 1.0f;
-                }
+                    const int kv0 = n * kBlockN;
+                    const uint32_t t_s = t_sbase + sb * kBlockN;
+                    mbar_wait(bars_r + 8u * (kBarSFull + sb), sb_par);
+                    tc_fence_after();
 
-                // row max over both halves: exchange through smem (double-buffered by tile parity).
-                // The barrier also orders every S read of this tile before any P write below
-                // (P aliases the first 64 columns of the S buffer, which belong to half 0).
-                float* xrow = xrow_base + xpar * (4 * kBlockM);
-                xrow[hf * kBlockM] = my_max;
-                named_bar_sync(bar_id, kPairThreads);
-                const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
-
-                // lazy running max: move the reference only when it would grow by > 2^8
-                const float m_new = (tile_max > m_ref + kRescaleThreshold) ? tile_max : m_ref;
-                const float alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
-                const float neg_m = (m_new == -CUDART_INF_F) ? 0.f : -m_new;
-
-                // P = 2^(s*mul - m)
-                uint64_t sum2 = 0;  // packed (0.f, 0.f)
-                const uint64_t mul2 = bc2(mul), negm2 = bc2(neg_m);
+                    uint32_t su[kHalfN];
 #pragma unroll
-                for (int cb = 0; cb < kHalfN / 32; ++cb) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        float p0, p1;
-                        unpk2(ffma2v(pk2(__uint_as_float(su[cb * 32 + 2 * u]), __uint_as_float(su[cb * 32 + 2 * u + 1])),
-                                     mul2, negm2),
-                              p0, p1);
-                        p0 = ex2(p0);
-                        p1 = ex2(p1);
-                        sum2 = fadd2v(sum2, pk2(p0, p1));
-                        pk[u] = pack2<kBf16>(p0, p1);
-                    }
-                    tmem_st16(t_s + hf * (kHalfN / 2) + cb * 16, pk);
-                }
-                float sum0, sum1;
-                unpk2(sum2, sum0, sum1);
-                l_run = l_run * alpha + (sum0 + sum1);
-                m_ref = m_new;
-
-                // O_X *= alpha for rows whose reference max moved (PV of the previous tile has
-                // completed: this S buffer was committed after it on the in-order tensor pipe).
-                // Each half rescales its own 32 of the 64 output columns.
-                if (it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
-                    uint32_t o[32];
-                    tmem_ld32(t_o, o);
+                    for (int cb = 0; cb < kHalfN / 32; ++cb)
+                        tmem_ld32(t_s + hf * kHalfN + cb * 32, reinterpret_cast<uint32_t(&)[32]>(su[cb * 32]));
                     tc_wait_ld();
+                    if (p.debug_scores != nullptr && it == 0) {
+                        float* dst = p.debug_scores +
+                                     ((static_cast<size_t>(blockIdx.x) * 2 + x) * kBlockM + r) * kBlockN + hf * kHalfN;
 #pragma unroll
-                    for (int u = 0; u < 32; u += 2) {
-                        float a0 = __uint_as_float(o[u]), a1 = __uint_as_float(o[u + 1]);
-                        fmul2(a0, a1, alpha);
-                        o[u] = __float_as_uint(a0);
-                        o[u + 1] = __float_as_uint(a1);
+                        for (int j = 0; j < kHalfN; ++j) dst[j] = __uint_as_float(su[j]);
                     }
-                    tmem_st32(t_o, o);
-                }
-                tc_wait_st();
-                tc_fence_before();
-                mbar_arrive(bars_r + 8u * (kBarPFull + sb));
-                ++it;
-                xpar ^= 1u;
-                sb += 2;
-                if (sb >= kSBufs) {
-                    sb -= kSBufs;
-                    sb_par ^= 1u;
-                }
-            }
 
-            // ---------------- epilogue ----------------
-            // combine the two halves' row sums, then each half writes its 32 output columns
-            float* lrow = xrow_base;
-            named_bar_sync(bar_id, kPairThreads);  // all max-exchange reads of the last tile are done
-            lrow[hf * kBlockM] = l_run;
-            named_bar_sync(bar_id, kPairThreads);
-            const float l_tot = l_run + lrow[(hf ^ 1) * kBlockM];
+                    // tile class (warp-uniform): "full" tiles need no per-element predicate
+                    const bool full = (n >= nf0) && (n < nf1) && (flag == kTileFull);
 
-            constexpr int kOutCols = kHeadDim / 2;
-            float o[kOutCols];
-            if (num_live > 0) {
-                mbar_wait(bar(kBarOFull + x), 0);
-                tc_fence_after();
-                tmem_ld32(t_o, reinterpret_cast<uint32_t(&)[32]>(o));
-                tc_wait_ld();
-            } else {
+                    float my_max;
+                    float mul;
+                    if (full) {
+                        float mx[4];
 #pragma unroll
-                for (int u = 0; u < kOutCols; ++u) o[u] = 0.f;
+                        for (int q4 = 0; q4 < 4; ++q4) mx[q4] = __uint_as_float(su[q4]);
+#pragma unroll
+                        for (int j = 4; j < kHalfN; j += 8) {
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4) {
+                                const int j0 = j + 2 * q4;
+                                if (j0 + 1 < kHalfN)
+                                    mx[q4] = max3(mx[q4], __uint_as_float(su[j0]), __uint_as_float(su[j0 + 1]));
+                            }
+                        }
+                        my_max = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * c;  // scale > 0 (host-checked)
+                        mul = c;
+                    } else {
+                        // live columns of this row inside the tile: [lo, hi]
+                        int lo = p.kv_begin, hi = kv_end_eff - 1;
+                        if (p.wl >= 0) lo = max(lo, row - p.wl);
+                        if (p.wr >= 0) hi = min(hi, row + p.wr);
+                        lo -= kv0 + hf * kHalfN;
+                        hi -= kv0 + hf * kHalfN;
+                        const float* brow = (kHasBias && flag == kTileMixed)
+                                                ? p.bias2 + static_cast<size_t>(b) * p.bias_stride + kv0 + hf * kHalfN
+                                                : nullptr;
+                        float mx = -CUDART_INF_F;
+#pragma unroll
+                        for (int j4 = 0; j4 < kHalfN; j4 += 4) {
+                            float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (kHasBias && brow != nullptr) bb = __ldg(reinterpret_cast<const float4*>(brow + j4));
+                            const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int j = j4 + u;
+                                const float xs = fmaf(__uint_as_float(su[j]), c, bv[u]);  // bias -inf => masked key
+                                const float xm = (j >= lo && j <= hi) ? xs : -CUDART_INF_F;
+                                su[j] = __float_as_uint(xm);
+                                mx = fmaxf(mx, xm);
+                            }
+                        }
+                        my_max = mx;
+                        mul = 1.0f;
+                    }
+
+                    // row max over both halves: exchange through smem (double-buffered by tile parity).
+                    // The barrier also orders every S read of this tile before any P write below
+                    // (P aliases the first 64 columns of the S buffer, which belong to half 0).
+                    float* xrow = xrow_base + xpar * (4 * kBlockM);
+                    xrow[hf * kBlockM] = my_max;
+                    named_bar_sync(bar_id, kPairThreads);
+                    const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
+
+                    // lazy running max: move the reference only when it would grow by > 2^8
+                    const float m_new = (tile_max > m_ref + kRescaleThreshold) ? tile_max : m_ref;
+                    const float alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
+                    const float neg_m = (m_new == -CUDART_INF_F) ? 0.f : -m_new;
+
+                    // P = 2^(s*mul - m)
+                    uint64_t sum2 = 0;  // packed (0.f, 0.f)
+                    const uint64_t mul2 = bc2(mul), negm2 = bc2(neg_m);
+#pragma unroll
+                    for (int cb = 0; cb < kHalfN / 32; ++cb) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            float p0, p1;
+                            unpk2(ffma2v(pk2(__uint_as_float(su[cb * 32 + 2 * u]), __uint_as_float(su[cb * 32 + 2 * u + 1])),
+                                         mul2, negm2),
+                                  p0, p1);
+                            p0 = ex2(p0);
+                            p1 = ex2(p1);
+                            sum2 = fadd2v(sum2, pk2(p0, p1));
+                            pk[u] = pack2<kBf16>(p0, p1);
+                        }
+                        tmem_st16(t_s + hf * (kHalfN / 2) + cb * 16, pk);
+                    }
+                    float sum0, sum1;
+                    unpk2(sum2, sum0, sum1);
+                    l_run = l_run * alpha + (sum0 + sum1);
+                    m_ref = m_new;
+
+                    // O_X *= alpha for rows whose reference max moved (PV of the previous tile has
+                    // completed: this S buffer was committed after it on the in-order tensor pipe).
+                    // Each half rescales its own 32 of the 64 output columns.
+                    if (it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+                        uint32_t o[32];
+                        tmem_ld32(t_o, o);
+                        tc_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            float a0 = __uint_as_float(o[u]), a1 = __uint_as_float(o[u + 1]);
+                            fmul2(a0, a1, alpha);
+                            o[u] = __float_as_uint(a0);
+                            o[u + 1] = __float_as_uint(a1);
+                        }
+                        tmem_st32(t_o, o);
+                    }
+                    tc_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(bars_r + 8u * (kBarPFull + sb));
+                    ++it;
+                    xpar ^= 1u;
+                    sb += 2;
+                    if (sb >= kSBufs) {
+                        sb -= kSBufs;
+                        sb_par ^= 1u;
+                    }
+                }
             }
-            if (row < p.S) {
+            // keep the sequence counter of both warpgroups in step even when tile B sat this item out
+            g += 2u * static_cast<uint32_t>(num_live);
+
+            if (active) {
+                // ---------------- epilogue ----------------
+                // combine the two halves' row sums, then each half handles its 32 output columns
+                float* lrow = xrow_base;
+                named_bar_sync(bar_id, kPairThreads);  // all max-exchange reads of the last tile are done
+                lrow[hf * kBlockM] = l_run;
+                named_bar_sync(bar_id, kPairThreads);
+                float l_tot = l_run + lrow[(hf ^ 1) * kBlockM];
+                named_bar_sync(bar_id, kPairThreads);  // reads done before the next item reuses the slot
+
+                constexpr int kOutCols = kHeadDim / 2;
                 const int col0 = hf * kOutCols;
-                if (p.o_partial != nullptr) {
-                    const size_t ridx = (static_cast<size_t>(b) * p.H + h) * p.S + row;
-                    float4* dst = reinterpret_cast<float4*>(p.o_partial + ridx * kHeadDim + col0);
+                float o[kOutCols];
+                if (num_live > 0) {
+                    mbar_wait(bars_r + 8u * (kBarOFull + x), oi & 1);
+                    tc_fence_after();
+                    tmem_ld32(t_o, reinterpret_cast<uint32_t(&)[32]>(o));
+                    tc_wait_ld();
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kOutCols; ++u) o[u] = 0.f;
+                }
+
+                if (item.kind == kItemHeadPart) {
+                    // this CTA owns only the trailing key tiles of the pair: publish an un-normalised
+                    // partial for CTA blockIdx.x - 1, which holds the leading key tiles
+                    const size_t slot = (static_cast<size_t>(blockIdx.x) * 2 + x) * kBlockM + r;
+                    float4* dst = reinterpret_cast<float4*>(p.part_o + slot * kHeadDim + col0);
 #pragma unroll
                     for (int u = 0; u < kOutCols / 4; ++u)
                         dst[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
                     if (hf == 0) {
-                        p.m_partial[ridx] = m_ref;
-                        p.l_partial[ridx] = l_tot;
+                        p.part_ml[slot * 2] = m_ref;
+                        p.part_ml[slot * 2 + 1] = l_tot;
                     }
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) st_release_gpu(p.part_flag + blockIdx.x * kNumSoftmaxWarps + warp, 1);
                 } else {
-                    const float inv = l_tot > 0.f ? 1.0f / l_tot : 0.f;
-                    const size_t off = static_cast<size_t>(b) * p.o_sb + static_cast<size_t>(h) * p.o_sh +
-                                       static_cast<size_t>(row) * p.o_ss + col0;
-                    if (p.out_dtype == 2) {
-                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+                    if (item.kind == kItemTailPart) {
+                        // merge with the partial CTA blockIdx.x + 1 published for the same rows (its
+                        // half-0 warp of the same quadrant wrote m and l, this warp's twin wrote the
+                        // columns); own part first: fixed order, deterministic
+                        const int* flag_o = p.part_flag + (blockIdx.x + 1) * kNumSoftmaxWarps + warp;
+                        const int* flag_ml = p.part_flag + (blockIdx.x + 1) * kNumSoftmaxWarps + (warp & ~4);
+                        uint32_t spins = 0;
+                        while (ld_acquire_gpu(flag_o) == 0 || ld_acquire_gpu(flag_ml) == 0) {
+                            if (++spins > RF_MBAR_SPIN_LIMIT) __trap();
+                        }
+                        const size_t slot = (static_cast<size_t>(blockIdx.x + 1) * 2 + x) * kBlockM + r;
+                        const float m2 = __ldcg(p.part_ml + slot * 2);
+                        const float l2 = __ldcg(p.part_ml + slot * 2 + 1);
+                        const float ms = fmaxf(m_ref, m2);
+                        const float w1 = (m_ref == -CUDART_INF_F) ? 0.f : ex2(m_ref - ms);
+                        const float w2 = (m2 == -CUDART_INF_F) ? 0.f : ex2(m2 - ms);
+                        const float4* src = reinterpret_cast<const float4*>(p.part_o + slot * kHeadDim + col0);
 #pragma unroll
-                        for (int u = 0; u < kOutCols / 4; ++u)
-                            dst[u] = make_float4(o[4 * u] * inv, o[4 * u + 1] * inv, o[4 * u + 2] * inv,
-                                                 o[4 * u + 3] * inv);
-                    } else {
-                        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + off);
+                        for (int u = 0; u < kOutCols / 4; ++u) {
+                            const float4 t = __ldcg(src + u);
+                            o[4 * u] = o[4 * u] * w1 + t.x * w2;
+                            o[4 * u + 1] = o[4 * u + 1] * w1 + t.y * w2;
+                            o[4 * u + 2] = o[4 * u + 2] * w1 + t.z * w2;
+                            o[4 * u + 3] = o[4 * u + 3] * w1 + t.w * w2;
+                        }
+                        l_tot = l_tot * w1 + l2 * w2;
+                        m_ref = ms;
+                    }
+                    if (row < p.S) {
+                        if (p.o_partial != nullptr) {
+                            const size_t ridx = (static_cast<size_t>(b) * p.H + h) * p.S + row;
+                            float4* dst = reinterpret_cast<float4*>(p.o_partial + ridx * kHeadDim + col0);
 #pragma unroll
-                        for (int u = 0; u < kOutCols / 8; ++u) {
-                            uint32_t w[4];
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const float a0 = o[8 * u + 2 * e] * inv, a1 = o[8 * u + 2 * e + 1] * inv;
-                                w[e] = (p.out_dtype == 0) ? pack2<true>(a0, a1) : pack2<false>(a0, a1);
+                            for (int u = 0; u < kOutCols / 4; ++u)
+                                dst[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+                            if (hf == 0) {
+                                p.m_partial[ridx] = m_ref;
+                                p.l_partial[ridx] = l_tot;
                             }
-                            dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+                        } else {
+                            const float inv = l_tot > 0.f ? 1.0f / l_tot : 0.f;
+                            const size_t off = static_cast<size_t>(b) * p.o_sb + static_cast<size_t>(h) * p.o_sh +
+                                               static_cast<size_t>(row) * p.o_ss + col0;
+                            if (p.out_dtype == 2) {
+                                float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+#pragma unroll
+                                for (int u = 0; u < kOutCols / 4; ++u)
+                                    dst[u] = make_float4(o[4 * u] * inv, o[4 * u + 1] * inv, o[4 * u + 2] * inv,
+                                                         o[4 * u + 3] * inv);
+                            } else {
+                                uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + off);
+#pragma unroll
+                                for (int u = 0; u < kOutCols / 8; ++u) {
+                                    uint32_t w[4];
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        const float a0 = o[8 * u + 2 * e] * inv, a1 = o[8 * u + 2 * e + 1] * inv;
+                                        w[e] = (p.out_dtype == 0) ? pack2<true>(a0, a1) : pack2<false>(a0, a1);
+                                    }
+                                    dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+                                }
+                            }
                         }
                     }
                 }
             }
+            if (active && num_live > 0) ++oi;
         }
     }
 
@@ -547,8 +706,25 @@ size_t fa_fwd_sm100_smem_bytes() {
     return Smem::xchg + Smem::xchg_bytes + 1024;  // + alignment slack
 }
 
+size_t fa_fwd_sm100_partial_bytes(int grid) {
+    // per CTA: O partial [2][128][64] f32, (m, l) [2][128][2] f32, 16 warp flags
+    return static_cast<size_t>(grid) * (2 * kBlockM * kHeadDim * 4 + 2 * kBlockM * 2 * 4 + kNumSoftmaxWarps * 4);
+}
+
+// Carves the split-pair workspace; the flag block must be zero when the kernel starts.
+void fa_fwd_sm100_partial_carve(void* base, int grid, FaParams* p, void** flags, size_t* flag_bytes) {
+    uint8_t* b = static_cast<uint8_t*>(base);
+    p->part_o = reinterpret_cast<float*>(b);
+    b += static_cast<size_t>(grid) * 2 * kBlockM * kHeadDim * 4;
+    p->part_ml = reinterpret_cast<float*>(b);
+    b += static_cast<size_t>(grid) * 2 * kBlockM * 2 * 4;
+    p->part_flag = reinterpret_cast<int*>(b);
+    *flags = b;
+    *flag_bytes = static_cast<size_t>(grid) * kNumSoftmaxWarps * 4;
+}
+
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
-                                const FaParams& p, bool bf16, cudaStream_t stream, int* grid_ctas) {
+                                const FaParams& p, bool bf16, int grid, cudaStream_t stream) {
     const bool has_bias = p.tile_flags != nullptr;
     void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const FaParams) =
         bf16 ? (has_bias ? fa_fwd_sm100_kernel<true, true> : fa_fwd_sm100_kernel<true, false>)
@@ -556,8 +732,6 @@ cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, 
     const size_t smem = fa_fwd_sm100_smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    dim3 grid((p.S + kRowsPerCta - 1) / kRowsPerCta, p.H, p.B);
-    if (grid_ctas) *grid_ctas = static_cast<int>(grid.x * grid.y * grid.z);
     kern<<<grid, kThreads, smem, stream>>>(tmq, tmk, tmv, p);
     return cudaGetLastError();
 }

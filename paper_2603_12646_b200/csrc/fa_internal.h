@@ -38,6 +38,14 @@ struct FaParams {
     float* m_partial;
     float* l_partial;
     float* debug_scores;
+    // work distribution (see fa_fwd_sm100.cu): 0 = one query-tile pair per CTA, 1 = persistent,
+    // statically balanced slices of the flat (pair x key tile) space with in-kernel merge
+    int sched_mode;
+    int total_pairs;     // B * H * pairs_per_head
+    int pairs_per_head;  // ceil(S / 256)
+    float* part_o;       // mode 1 workspace: partials of pairs cut between two CTAs
+    float* part_ml;
+    int* part_flag;
 };
 
 struct SimtParams {
@@ -52,8 +60,10 @@ struct SimtParams {
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
-                                const FaParams& p, bool bf16, cudaStream_t stream, int* grid_ctas);
+                                const FaParams& p, bool bf16, int grid, cudaStream_t stream);
 size_t fa_fwd_sm100_smem_bytes();
+size_t fa_fwd_sm100_partial_bytes(int grid);
+void fa_fwd_sm100_partial_carve(void* base, int grid, FaParams* p, void** flags, size_t* flag_bytes);
 cudaError_t launch_fa_fwd_simt(const SimtParams& p, cudaStream_t stream, int* grid_ctas);
 
 cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias2, uint8_t* tile_flags,
