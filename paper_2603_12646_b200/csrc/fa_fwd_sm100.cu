@@ -37,6 +37,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "fa_internal.h"
 #include "ptx.cuh"
 
@@ -56,6 +58,10 @@ constexpr int kMmaWarp = 17;
 constexpr int kThreads = 640;        // 5 warpgroups: 4 softmax + 1 (producer, MMA, 2 idle warps)
 constexpr int kHalfN = kBlockN / 2;  // key columns per softmax thread
 constexpr int kRegsSoftmax = 112;
+#ifndef RF_FA_EMU_EVERY
+#define RF_FA_EMU_EVERY 8
+#endif
+constexpr int kEmuEvery = RF_FA_EMU_EVERY;  // every n-th element pair uses the FMA-pipe exp2 (0 = MUFU only)
 constexpr int kRegsOther = 32;       // 128*32 + 512*112 == 640*96: the CTA register pool balances exactly
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;    // + 128 * buffer
@@ -527,25 +533,39 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     const float alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
                     const float neg_m = (m_new == -CUDART_INF_F) ? 0.f : -m_new;
 
-                    // P = 2^(s*mul - m)
+                    // P = 2^(s*mul - m).  On full tiles every kEmuEvery-th element pair takes the FMA-pipe
+                    // polynomial (exp2_poly2) instead of MUFU.EX2 so both pipes share the exponentials;
+                    // edge tiles keep MUFU only, because a masked score (-inf) must give exactly 0.
                     uint64_t sum2 = 0;  // packed (0.f, 0.f)
                     const uint64_t mul2 = bc2(mul), negm2 = bc2(neg_m);
+                    auto exp_store = [&](auto emu_tag) {
+                        constexpr bool kEmu = decltype(emu_tag)::value;
 #pragma unroll
-                    for (int cb = 0; cb < kHalfN / 32; ++cb) {
-                        uint32_t pk[16];
+                        for (int cb = 0; cb < kHalfN / 32; ++cb) {
+                            uint32_t pk[16];
 #pragma unroll
-                        for (int u = 0; u < 16; ++u) {
-                            float p0, p1;
-                            unpk2(ffma2v(pk2(__uint_as_float(su[cb * 32 + 2 * u]), __uint_as_float(su[cb * 32 + 2 * u + 1])),
-                                         mul2, negm2),
-                                  p0, p1);
-                            p0 = ex2(p0);
-                            p1 = ex2(p1);
-                            sum2 = fadd2v(sum2, pk2(p0, p1));
-                            pk[u] = pack2<kBf16>(p0, p1);
+                            for (int u = 0; u < 16; ++u) {
+                                float p0, p1;
+                                unpk2(ffma2v(pk2(__uint_as_float(su[cb * 32 + 2 * u]),
+                                                 __uint_as_float(su[cb * 32 + 2 * u + 1])),
+                                             mul2, negm2),
+                                      p0, p1);
+                                if (kEmu && (u % (kEmuEvery > 0 ? kEmuEvery : 1)) == (kEmuEvery > 0 ? kEmuEvery - 1 : 0)) {
+                                    exp2_poly2(p0, p1);
+                                } else {
+                                    p0 = ex2(p0);
+                                    p1 = ex2(p1);
+                                }
+                                sum2 = fadd2v(sum2, pk2(p0, p1));
+                                pk[u] = pack2<kBf16>(p0, p1);
+                            }
+                            tmem_st16(t_s + hf * (kHalfN / 2) + cb * 16, pk);
                         }
-                        tmem_st16(t_s + hf * (kHalfN / 2) + cb * 16, pk);
-                    }
+                    };
+                    if (kEmuEvery > 0 && full)
+                        exp_store(std::true_type{});
+                    else
+                        exp_store(std::false_type{});
                     float sum0, sum1;
                     unpk2(sum2, sum0, sum1);
                     l_run = l_run * alpha + (sum0 + sum1);
