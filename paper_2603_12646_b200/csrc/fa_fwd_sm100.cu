@@ -308,6 +308,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         };
 
         uint32_t qi = 0, kc = 0, vc = 0, tc = 0;  // items / K tiles / V tiles / tiles consumed so far
+        uint32_t par_bits = 0;  // bit s = phase parity of the next use of S buffer s (S-full / P-full barriers)
         while (next_item<kHasBias>(p, sched, item)) {
             const int num_live = item.num_live;
             if (num_live == 0) continue;
@@ -315,7 +316,6 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 
             // tile g = 2*t + x of the A,B,A,B,... sequence lives in S buffer g % 3
             auto sbuf = [&](int i, int x) { return (2 * (tc + i) + x) % kSBufs; };
-            auto suse_parity = [&](int i, int x) { return ((2 * (tc + i) + x) / kSBufs) & 1u; };
 
             // S = Q_X * K^T : both operands K-major (head dim contiguous), 128B swizzle,
             // 8-row core-matrix groups 1024 B apart; a K=16 step advances 32 B inside the atom.
@@ -373,7 +373,8 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const bool last = i + 1 == num_live;
                 mbar_wait(bar(kBarVFull + (vc + i) % kStagesV), ((vc + i) / kStagesV) & 1);
                 // ---- P_A(i) ready: O_A += P_A V; its S buffer is then free for S_B(i+1) ----
-                mbar_wait(bar(kBarPFull + sbuf(i, 0)), suse_parity(i, 0));
+                const uint32_t buf_a = sbuf(i, 0), buf_b = sbuf(i, 1);
+                mbar_wait(bar(kBarPFull + buf_a), (par_bits >> buf_a) & 1u);
                 tc_fence_after();
                 issue_pv(0, i);
                 if (last) commit(bar(kBarOFull + 0));
@@ -383,11 +384,12 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         release_k(i + 1);
                     }
                     // ---- P_B(i) ready: O_B += P_B V; its S buffer is then free for S_A(i+2) ----
-                    mbar_wait(bar(kBarPFull + sbuf(i, 1)), suse_parity(i, 1));
+                    mbar_wait(bar(kBarPFull + buf_b), (par_bits >> buf_b) & 1u);
                     tc_fence_after();
                     issue_pv(1, i);
                     if (last) commit(bar(kBarOFull + 1));
                 }
+                par_bits ^= (1u << buf_a) ^ (has_b ? (1u << buf_b) : 0u);
                 commit(bar(kBarVEmpty + (vc + i) % kStagesV));
                 if (i + 2 < num_live) {
                     wait_k(i + 2);
@@ -421,6 +423,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 
         uint32_t oi = 0;    // items this warpgroup worked on so far (O barrier phase)
         uint32_t g = x;     // sequence index 2*t + x of this warpgroup's next tile
+        uint32_t par_bits = 0;  // bit s = phase parity of the next use of S buffer s (both tiles' uses counted)
         uint32_t xpar = 0;  // exchange double buffer
 
         while (next_item<kHasBias>(p, sched, item)) {
@@ -445,8 +448,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     nf1 = hi_key >= 0 ? (hi_key >> 7) + 1 : 0;
                 }
                 const uint8_t* flags_row = kHasBias ? p.tile_flags + b * p.n_kv_tiles : nullptr;
-                int sb = g % kSBufs;                 // S/P buffer of the current tile ...
-                uint32_t sb_par = (g / kSBufs) & 1;  // ... and its barrier phase parity
+                int sb = g % kSBufs;  // S/P buffer of the current tile
                 int it = 0;
                 for (int n = item.n0; n < item.n1; ++n) {
                     uint8_t flag = kTileFull;
@@ -456,7 +458,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     }
                     const int kv0 = n * kBlockN;
                     const uint32_t t_s = t_sbase + sb * kBlockN;
-                    mbar_wait(bars_r + 8u * (kBarSFull + sb), sb_par);
+                    mbar_wait(bars_r + 8u * (kBarSFull + sb), (par_bits >> sb) & 1u);
                     tc_fence_after();
 
                     uint32_t su[kHalfN];
@@ -592,12 +594,18 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     mbar_arrive(bars_r + 8u * (kBarPFull + sb));
                     ++it;
                     xpar ^= 1u;
-                    sb += 2;
-                    if (sb >= kSBufs) {
-                        sb -= kSBufs;
-                        sb_par ^= 1u;
+                    // this tile index used buffer sb for this warpgroup and, if the other tile is
+                    // active, its neighbour (A = B - 1, B = A + 1 mod 3) for the other warpgroup
+                    {
+                        const int other = x == 0 ? (sb + 1 == kSBufs ? 0 : sb + 1) : (sb == 0 ? kSBufs - 1 : sb - 1);
+                        par_bits ^= (1u << sb) ^ (item.has_b ? (1u << other) : 0u);
                     }
+                    sb += 2;
+                    if (sb >= kSBufs) sb -= kSBufs;
                 }
+            } else if (num_live > 0) {
+                // tile B sits this item out: account for tile A's uses of the shared S buffers
+                for (int i = 0; i < num_live; ++i) par_bits ^= 1u << ((g - 1u + 2u * i) % kSBufs);
             }
             // keep the sequence counter of both warpgroups in step even when tile B sat this item out
             g += 2u * static_cast<uint32_t>(num_live);

@@ -80,11 +80,20 @@ def test_workspace_is_linear_in_S(lib):
         sizes[S] = n.value
         st = capi.RfFaStats()
         lib.rf_fa_stats_query(C.byref(p), C.byref(st))
-        assert st.kernel == capi.RF_KERNEL_TCGEN05 and st.grid_ctas == 12 * S // 256
+        assert st.kernel == capi.RF_KERNEL_TCGEN05 and st.grid_ctas == 12 * S // 256  # padded: one pair per CTA
         assert st.row_state_bytes == 8 * S
     assert sizes[16384] <= 2 * sizes[8192] + 512 and sizes[32768] <= 4 * sizes[8192] + 1024
     assert sizes[32768] < 200 * 1024  # O(S): 4 B/key + 1 B/tile, nowhere near S^2
+    # dense global attention over more query-tile pairs than SMs runs the persistent balanced
+    # schedule: its split-pair workspace is a constant (per-SM), independent of S
     p.pad_bias = None
+    dense = []
+    for S in (8192, 32768):
+        p.S = S
+        assert lib.rf_fa_fwd_workspace_bytes(C.byref(p), C.byref(n)) == capi.RF_OK
+        dense.append(n.value)
+    assert dense[0] == dense[1] and 0 < dense[0] < 12 * 1024 * 1024
+    p.S = 512  # 24 pairs fit one wave: one pair per CTA, no workspace at all
     assert lib.rf_fa_fwd_workspace_bytes(C.byref(p), C.byref(n)) == capi.RF_OK and n.value == 0
 
 

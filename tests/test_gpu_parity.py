@@ -122,6 +122,41 @@ def test_small_grid(torch_mod, P, oracle, d, kernel):
     print("worst max-abs", worst)
 
 
+@pytest.mark.parametrize("S,lens", [(300, [263, 300]), (900, None), (385, [129, 385]), (129, None)])
+def test_ragged_last_pair_single_tile_row(torch_mod, P, oracle, S, lens):
+    """S % 256 in (0, 128]: the last query-tile pair has only its A tile, over several key tiles
+    (regression: per-buffer barrier phases must follow the tiles actually processed)."""
+    rng = np.random.default_rng(S)
+    B, H, d = 2, 2, 64
+    q, k, v = [oracle.round_bf16(rng.uniform(-1, 1, (B, H, S, d)).astype(np.float32)) for _ in range(3)]
+    pb = tail_pad(B, S, lens) if lens else None
+    for (wl, wr) in ((-1, -1), (63, 64)):
+        err, _, _ = run_case(torch_mod, P, oracle, q, k, v, 0.0, wl, wr, pb, expect_kernel="tcgen05")
+        assert err <= TOL, (S, wl, err)
+
+
+def test_persistent_schedule_matches_one_pair_per_cta(torch_mod, P, oracle):
+    """More query-tile pairs than SMs and no mask -> persistent balanced schedule with in-kernel
+    merge of split pairs.  Same inputs with an all-zero pad bias take the one-pair-per-CTA path;
+    the oracle checks one head; both runs are bitwise reproducible."""
+    torch = torch_mod
+    B, H, S, d = 2, 12, 2304, 64   # 2*12*9 = 216 pairs > 148 SMs, 18 key tiles each
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v = [(torch.rand((B, H, S, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+    st = P.FlashStats()
+    a = P.flash_attention(q, k, v, P.AttentionSpec(), stats=st, out_dtype=torch.float32)
+    assert st.grid_ctas < B * H * 9 and st.workspace_bytes > 0      # persistent
+    st2 = P.FlashStats()
+    zero_bias = torch.zeros((B, 1, 1, S), device="cuda")
+    b_ = P.flash_attention(q, k, v, P.AttentionSpec(pad_bias=zero_bias), stats=st2, out_dtype=torch.float32)
+    assert st2.grid_ctas == B * H * 9
+    assert (a - b_).abs().max().item() <= 5e-3
+    assert torch.equal(a, P.flash_attention(q, k, v, P.AttentionSpec(), out_dtype=torch.float32))
+    qn, kn, vn = [t[1:, 7:8].float().cpu().numpy() for t in (q, k, v)]
+    want = oracle.flash_attention(qn, kn, vn)
+    assert np.abs(a[1:, 7:8].cpu().numpy() - want).max() <= TOL
+
+
 def test_edge_cases(torch_mod, P, oracle):
     torch = torch_mod
     rng = np.random.default_rng(5)

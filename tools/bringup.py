@@ -191,6 +191,8 @@ CASES = {
     "ts_local_pad": lambda: case_fa("ts_local_pad", 2, 4, 1000, 63, 64, [1000, 777], 0),
     "ts_onesided": lambda: case_fa("ts_onesided", 1, 2, 700, 1, 2, None, 0),
     "ts_self": lambda: case_fa("ts_self", 1, 2, 300, 0, 0, None, 0),
+    "ts_aonly_pad": lambda: case_fa("ts_aonly_pad", 1, 2, 300, -1, -1, [263], 0),
+    "ts_aonly_900": lambda: case_fa("ts_aonly_900", 2, 3, 900, -1, -1, None, 0),
     "ts_tiny": lambda: case_fa("ts_tiny", 1, 1, 5, -1, -1, None, 0),
     "ts_allpad": lambda: case_fa("ts_allpad", 2, 2, 256, -1, -1, [256, 0], 0),
     "cross_8k": lambda: case_cross("cross_8k", 1, 12, 8192, -1, -1, None),
