@@ -181,6 +181,19 @@ int rf_fused_flash_attention_op(const float* const* inputs, const int64_t* const
                                 int32_t has_window_right, int64_t window_right, float* output,
                                 int32_t device);
 
+/* Encoder-layer glue either side of the op, bf16, in place where possible:
+ *   rf_rope_qkv      rotary embedding ("rotate_half" pairing i, i+d/2) on the Q and K thirds of a
+ *                    packed QKV GEMM output [tokens,3,H,d]; cos/sin f32 [S,d/2]; position = t % S.
+ *                    The attention kernel then reads the three thirds as strided views.
+ *   rf_add_layernorm x (f32 residual stream [rows,n]) += delta (bf16, or NULL); y = LN(x)*w (bf16,
+ *                    no bias; y may be NULL to only accumulate).  n % 4 == 0, n <= 4096.
+ *   rf_geglu         act[rows,I] = gelu(wi_out[:, :I]) * wi_out[:, I:]   (erf GELU)            */
+int rf_rope_qkv(void* qkv, const float* cos_table, const float* sin_table, int64_t tokens, int64_t S, int64_t H,
+                int64_t d, void* stream);
+int rf_add_layernorm(float* x, const void* delta, const float* w, void* y, int64_t rows, int64_t n, float eps,
+                     void* stream);
+int rf_geglu(const void* wi_out, void* act, int64_t rows, int64_t I, void* stream);
+
 /* Memory model (attention.cpp:244-252). */
 uint64_t rf_mask_memory_bytes(uint64_t batch, uint64_t heads, uint64_t seq_len, uint64_t bytes_per_element);
 uint64_t rf_fa_memory_bytes(uint64_t batch, uint64_t heads, uint64_t seq_len, uint64_t head_dim,

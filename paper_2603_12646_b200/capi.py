@@ -20,6 +20,7 @@ EXPORTS = [
     "rf_fa_stats_query", "rf_fa_fwd", "rf_fa_merge", "rf_fa_rescale_partial", "rf_fa_normalize",
     "rf_pad_bias_from_mask", "rf_cast_f32_to", "rf_cast_to_f32", "rf_fa_fwd_host",
     "rf_fused_flash_attention_op", "rf_mask_memory_bytes", "rf_fa_memory_bytes", "rf_device_check",
+    "rf_rope_qkv", "rf_add_layernorm", "rf_geglu",
 ]
 
 
@@ -100,6 +101,9 @@ def load(build_if_missing: bool = True):
                                    C.POINTER(i64), i64, i32, i32, C.POINTER(RfFaStats)]
     lib.rf_fused_flash_attention_op.argtypes = [C.POINTER(f32p), C.POINTER(C.POINTER(i64)), C.POINTER(i32), i32,
                                                 i32, C.c_double, i32, i64, i32, i64, f32p, i32]
+    lib.rf_rope_qkv.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp]
+    lib.rf_add_layernorm.argtypes = [vp, vp, vp, vp, i64, i64, C.c_float, vp]
+    lib.rf_geglu.argtypes = [vp, vp, i64, i64, vp]
     lib.rf_mask_memory_bytes.restype = u64
     lib.rf_mask_memory_bytes.argtypes = [u64] * 4
     lib.rf_fa_memory_bytes.restype = u64
@@ -107,7 +111,8 @@ def load(build_if_missing: bool = True):
     lib.rf_device_check.argtypes = [i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
     for name in ("rf_fa_validate", "rf_fa_fwd_workspace_bytes", "rf_fa_stats_query", "rf_fa_fwd", "rf_fa_merge",
                  "rf_fa_rescale_partial", "rf_fa_normalize", "rf_pad_bias_from_mask", "rf_cast_f32_to",
-                 "rf_cast_to_f32", "rf_fa_fwd_host", "rf_fused_flash_attention_op", "rf_device_check"):
+                 "rf_cast_to_f32", "rf_fa_fwd_host", "rf_fused_flash_attention_op", "rf_device_check",
+                 "rf_rope_qkv", "rf_add_layernorm", "rf_geglu"):
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib

@@ -1,0 +1,178 @@
+"""ModernBERT-base-shaped long-context classifier built on the FusedFlashAttention operator
+(BASELINE configs 2/3/5).
+
+The reference has NO neural classifier (its classifiers are keyword stubs,
+proj/core/src/classifiers.cpp:63-225); what it defines for this model is the attention operator,
+the shared pad-bias chain and the per-layer window rule (global every 3rd layer, else local 128
+-> (63, 64); rewrite.cpp:303-318,355-361).  Everything else here -- embeddings, pre-norm encoder
+layers with a GeGLU MLP, RoPE, CLS pooling, classification head, random-init weights from a seed
+-- is this build's own construction, sized like ModernBERT-base (22 layers, hidden 768, 12 x 64
+heads, MLP 1152, vocab 50368).
+
+Data path per layer (bf16 GEMM operands, f32 residual stream):
+  h   = LN(x)                       rf_add_layernorm (fused with the previous residual add)
+  qkv = h @ Wqkv^T                  library GEMM -> [B,S,3,H,d]
+  rope(q, k) in place               rf_rope_qkv
+  o   = FusedFlashAttention(q,k,v)  strided views of qkv in, [B,S,H*d] out: no transposes
+  x  += o @ Wo^T ; h2 = LN(x)       library GEMM + rf_add_layernorm
+  x  += (gelu(h2 Wi_a) * h2 Wi_g) Wo2    in row chunks (bounds activation memory), rf_geglu
+GEMMs are plain library GEMMs (cuBLAS via torch.matmul); all glue and the attention are the
+hand-written kernels of librf_fa.so.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Dict, Optional
+
+import torch
+
+from . import capi
+from .attention import AttentionSpec, RewriteOptions, flash_attention, local_window_attrs, pad_bias_from_mask
+
+
+@dataclass
+class ClassifierConfig:
+    vocab_size: int = 50368
+    hidden: int = 768
+    n_layers: int = 22
+    heads: int = 12
+    head_dim: int = 64
+    mlp: int = 1152
+    global_every: int = 3
+    local_window: int = 128
+    n_labels: int = 3
+    rope_theta_global: float = 160000.0
+    rope_theta_local: float = 10000.0
+    eps: float = 1e-5
+    mlp_chunk_rows: int = 8192
+
+    def is_global(self, layer: int) -> bool:
+        return layer % self.global_every == 0
+
+
+def init_weights(cfg: ClassifierConfig, seed: int) -> Dict[str, torch.Tensor]:
+    """Random-init f32 master weights on CPU, deterministic in `seed` (std 0.02, norms = 1)."""
+    g = torch.Generator().manual_seed(seed)
+
+    def rnd(*shape, std=0.02):
+        return torch.randn(*shape, generator=g) * std
+
+    w = {"tok_emb": rnd(cfg.vocab_size, cfg.hidden), "emb_norm": torch.ones(cfg.hidden),
+         "final_norm": torch.ones(cfg.hidden), "head_dense": rnd(cfg.hidden, cfg.hidden),
+         "head_norm": torch.ones(cfg.hidden), "cls_w": rnd(cfg.n_labels, cfg.hidden, std=0.05),
+         "cls_b": torch.zeros(cfg.n_labels)}
+    for i in range(cfg.n_layers):
+        w[f"l{i}.attn_norm"] = torch.ones(cfg.hidden)
+        w[f"l{i}.wqkv"] = rnd(3 * cfg.hidden, cfg.hidden)
+        w[f"l{i}.wo"] = rnd(cfg.hidden, cfg.hidden)
+        w[f"l{i}.mlp_norm"] = torch.ones(cfg.hidden)
+        w[f"l{i}.wi"] = rnd(2 * cfg.mlp, cfg.hidden)
+        w[f"l{i}.wo2"] = rnd(cfg.hidden, cfg.mlp)
+    return w
+
+
+def rope_tables(seq_len: int, head_dim: int, theta: float, device=None):
+    """cos/sin [S, d/2] f32 for the rotate-half convention."""
+    inv = 1.0 / (theta ** (torch.arange(0, head_dim, 2, dtype=torch.float64) / head_dim))
+    ang = torch.arange(seq_len, dtype=torch.float64)[:, None] * inv[None, :]
+    return ang.cos().float().to(device), ang.sin().float().to(device)
+
+
+class Classifier:
+    """Inference-only classifier session on one GPU."""
+
+    def __init__(self, cfg: ClassifierConfig, weights: Dict[str, torch.Tensor], device: torch.device):
+        self.cfg, self.device = cfg, device
+        self.lib = capi.load()
+        norm_keys = {k for k in weights if k.endswith("norm") or k == "cls_b"}
+        self.w = {k: (v.to(device, torch.float32) if k in norm_keys else v.to(device, torch.bfloat16)).contiguous()
+                  for k, v in weights.items()}
+        self._rope = {}
+        self.last_layer_ms = None
+
+    # ---- thin wrappers over the C ABI glue kernels ----
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _add_layernorm(self, x, delta, w, want_out=True):
+        rows, n = x.shape
+        y = torch.empty((rows, n), device=self.device, dtype=torch.bfloat16) if want_out else None
+        capi.check(self.lib.rf_add_layernorm(x.data_ptr(), delta.data_ptr() if delta is not None else None,
+                                             w.data_ptr() if w is not None else None,
+                                             y.data_ptr() if y is not None else None, rows, n, self.cfg.eps, self._stream()))
+        return y
+
+    def _rope_tables(self, S, is_global):
+        key = (S, is_global)
+        if key not in self._rope:
+            theta = self.cfg.rope_theta_global if is_global else self.cfg.rope_theta_local
+            self._rope[key] = rope_tables(S, self.cfg.head_dim, theta, self.device)
+        return self._rope[key]
+
+    @torch.no_grad()
+    def forward(self, input_ids: torch.Tensor, attention_mask: Optional[torch.Tensor] = None,
+                time_layers: bool = False) -> torch.Tensor:
+        """input_ids [B,S] int64 (device), attention_mask [B,S] (1 = token, 0 = padding) or None.
+        Returns logits [B, n_labels] f32."""
+        cfg, lib = self.cfg, self.lib
+        B, S = input_ids.shape
+        H, d, hid = cfg.heads, cfg.head_dim, cfg.hidden
+        rows = B * S
+        with torch.cuda.device(self.device):
+            pad_bias = None
+            if attention_mask is not None:
+                # one shared pad-bias chain per forward, as the rewriter installs it (rewrite.cpp:303-318)
+                pad_bias = pad_bias_from_mask(attention_mask.to(self.device, torch.float32).reshape(B, 1, 1, S))
+            x = self.w["tok_emb"][input_ids.reshape(-1)].float()                 # f32 stream [rows, hid]
+            h = self._add_layernorm(x, None, self.w["emb_norm"])
+            x = h.float()                                                         # stream = LN(embeddings)
+            delta = None
+            ev = []
+            for i in range(cfg.n_layers):
+                if time_layers:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                if i > 0:
+                    h = self._add_layernorm(x, delta, self.w[f"l{i}.attn_norm"])  # x += mlp(i-1); h = LN(x)
+                qkv = h @ self.w[f"l{i}.wqkv"].t()                                # [rows, 3*hid] == [B,S,3,H,d]
+                glob = cfg.is_global(i)
+                cos, sin = self._rope_tables(S, glob)
+                capi.check(lib.rf_rope_qkv(qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), rows, S, H, d, self._stream()))
+                q5 = qkv.view(B, S, 3, H, d)
+                qv, kv, vv = (q5[:, :, j].permute(0, 2, 1, 3) for j in range(3))  # [B,H,S,d] views, no copy
+                attn = torch.empty((B, S, H * d), device=self.device, dtype=torch.bfloat16)
+                wl, wr = local_window_attrs(RewriteOptions(d, cfg.local_window), is_global=glob)
+                if time_layers:
+                    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a0.record()
+                flash_attention(qv, kv, vv, AttentionSpec(0.0, wl, wr, pad_bias),
+                                out=attn.view(B, S, H, d).permute(0, 2, 1, 3))
+                if time_layers:
+                    a1.record()
+                o = attn.view(rows, hid) @ self.w[f"l{i}.wo"].t()
+                h2 = self._add_layernorm(x, o, self.w[f"l{i}.mlp_norm"])          # x += attn; h2 = LN(x)
+                delta = torch.empty((rows, hid), device=self.device, dtype=torch.bfloat16)
+                for r0 in range(0, rows, cfg.mlp_chunk_rows):                     # bounded MLP intermediate
+                    r1 = min(rows, r0 + cfg.mlp_chunk_rows)
+                    wi_out = h2[r0:r1] @ self.w[f"l{i}.wi"].t()                   # [chunk, 2*mlp]
+                    act = torch.empty((r1 - r0, cfg.mlp), device=self.device, dtype=torch.bfloat16)
+                    capi.check(lib.rf_geglu(wi_out.data_ptr(), act.data_ptr(), r1 - r0, cfg.mlp, self._stream()))
+                    torch.matmul(act, self.w[f"l{i}.wo2"].t(), out=delta[r0:r1])
+                if time_layers:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record()
+                    ev.append((glob, e0, e1, a0, a1))
+            hf = self._add_layernorm(x, delta, self.w["final_norm"])              # x += mlp(last); LN
+            pooled = hf.view(B, S, hid)[:, 0]                                     # CLS pooling
+            t = torch.nn.functional.gelu((pooled @ self.w["head_dense"].t()).float())
+            t = torch.nn.functional.layer_norm(t, (hid,), self.w["head_norm"], None, cfg.eps)
+            logits = t @ self.w["cls_w"].float().t() + self.w["cls_b"]
+            if time_layers:
+                torch.cuda.synchronize(self.device)
+                self.last_layer_ms = [{"layer": i, "global": g_, "layer_ms": e0.elapsed_time(e1), "attention_ms": a0.elapsed_time(a1)}
+                                      for i, (g_, e0, e1, a0, a1) in enumerate(ev)]
+        return logits
+
+    def weight_bytes(self) -> int:
+        return sum(v.numel() * v.element_size() for v in self.w.values())

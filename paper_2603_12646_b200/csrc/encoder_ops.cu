@@ -1,0 +1,164 @@
+// encoder_ops.cu -- the glue either side of the attention op in a ModernBERT-style encoder layer
+// (SURVEY.md 8(f) rank 1): all HBM-bound elementwise / row kernels, written so that the QKV GEMM
+// output [B,S,3,H,d] feeds the attention kernel in place (no head-split transpose) and the
+// attention output [B,S,H*d] feeds the out-projection GEMM in place.
+//   rope_qkv      rotary embedding on the Q and K thirds of a packed QKV tensor, in place
+//   add_layernorm residual add into the f32 stream + LayerNorm (no bias) -> bf16 GEMM operand
+//   geglu         act = gelu(x[:, :I]) * x[:, I:]  on the Wi GEMM output
+// The GEMMs themselves are plain library GEMMs (cuBLAS through torch.matmul).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rf_fa.h"
+
+namespace {
+
+// qkv: [tokens, 3, H, d] bf16; cos/sin: [S, d/2] f32; token t has position t % S.
+// One thread per (token, q|k, head, pair i): rotates elements (i, i + d/2) -- the "rotate_half"
+// convention of ModernBERT / HF rotary embeddings.
+__global__ void __launch_bounds__(256) rope_qkv_kernel(__nv_bfloat16* __restrict__ qkv, const float* __restrict__ cosb,
+                                                       const float* __restrict__ sinb, long long tokens, int S, int H,
+                                                       int d) {
+    const int half = d >> 1;
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long total = tokens * 2 * H * half;
+    if (idx >= total) return;
+    const int i = static_cast<int>(idx % half);
+    long long r = idx / half;
+    const int h = static_cast<int>(r % H);
+    r /= H;
+    const int which = static_cast<int>(r % 2);  // 0 = q, 1 = k
+    const long long t = r / 2;
+    const int pos = static_cast<int>(t % S);
+    __nv_bfloat16* base = qkv + ((t * 3 + which) * H + h) * d;
+    const float x1 = __bfloat162float(base[i]);
+    const float x2 = __bfloat162float(base[i + half]);
+    const float c = cosb[static_cast<long long>(pos) * half + i];
+    const float s = sinb[static_cast<long long>(pos) * half + i];
+    base[i] = __float2bfloat16_rn(x1 * c - x2 * s);
+    base[i + half] = __float2bfloat16_rn(x2 * c + x1 * s);
+}
+
+// x (f32 residual stream, [rows, n]) += delta (bf16, may be null); y = LayerNorm(x) * w -> bf16.
+// One warp per row, n <= 1024 * 8.  Statistics in f32 (two-pass over registers).
+template <int kVecPerLane>
+__global__ void __launch_bounds__(128) add_layernorm_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
+                                                            const float* __restrict__ w, __nv_bfloat16* __restrict__ y,
+                                                            long long rows, int n, float eps) {
+    const long long row = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const int lane = threadIdx.x & 31;
+    float* xr = x + row * n;
+    float v[kVecPerLane * 4];
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < kVecPerLane; ++k) {
+        const int c = (k * 32 + lane) * 4;
+        if (c < n) {
+            float4 a = *reinterpret_cast<const float4*>(xr + c);
+            if (delta != nullptr) {
+                const uint2 dq = *reinterpret_cast<const uint2*>(delta + row * n + c);
+                const __nv_bfloat162 d0 = *reinterpret_cast<const __nv_bfloat162*>(&dq.x);
+                const __nv_bfloat162 d1 = *reinterpret_cast<const __nv_bfloat162*>(&dq.y);
+                a.x += __bfloat162float(d0.x);
+                a.y += __bfloat162float(d0.y);
+                a.z += __bfloat162float(d1.x);
+                a.w += __bfloat162float(d1.y);
+                *reinterpret_cast<float4*>(xr + c) = a;
+            }
+            v[4 * k] = a.x; v[4 * k + 1] = a.y; v[4 * k + 2] = a.z; v[4 * k + 3] = a.w;
+            sum += a.x + a.y + a.z + a.w;
+        } else {
+            v[4 * k] = v[4 * k + 1] = v[4 * k + 2] = v[4 * k + 3] = 0.f;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum / n;
+    float var = 0.f;
+#pragma unroll
+    for (int k = 0; k < kVecPerLane; ++k) {
+        const int c = (k * 32 + lane) * 4;
+        if (c < n) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float dlt = v[4 * k + e] - mean;
+                var += dlt * dlt;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+    const float rstd = rsqrtf(var / n + eps);
+    if (y == nullptr) return;
+#pragma unroll
+    for (int k = 0; k < kVecPerLane; ++k) {
+        const int c = (k * 32 + lane) * 4;
+        if (c < n) {
+            const float4 ww = *reinterpret_cast<const float4*>(w + c);
+            __nv_bfloat162 o0 = __floats2bfloat162_rn((v[4 * k] - mean) * rstd * ww.x, (v[4 * k + 1] - mean) * rstd * ww.y);
+            __nv_bfloat162 o1 = __floats2bfloat162_rn((v[4 * k + 2] - mean) * rstd * ww.z, (v[4 * k + 3] - mean) * rstd * ww.w);
+            uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&o0), *reinterpret_cast<uint32_t*>(&o1));
+            *reinterpret_cast<uint2*>(y + row * n + c) = pk;
+        }
+    }
+}
+
+// wi_out: [rows, 2*I] bf16 (input half then gate half); act: [rows, I] bf16 = gelu(input) * gate
+__global__ void __launch_bounds__(256) geglu_kernel(const __nv_bfloat16* __restrict__ wi_out, __nv_bfloat16* __restrict__ act,
+                                                    long long rows, int I) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long total = rows * (I >> 1);
+    if (idx >= total) return;
+    const long long row = idx / (I >> 1);
+    const int c = static_cast<int>(idx % (I >> 1)) * 2;
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(wi_out + row * 2 * I + c);
+    const __nv_bfloat162 g = *reinterpret_cast<const __nv_bfloat162*>(wi_out + row * 2 * I + I + c);
+    auto gelu = [](float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); };
+    const __nv_bfloat162 o = __floats2bfloat162_rn(gelu(__bfloat162float(a.x)) * __bfloat162float(g.x),
+                                                   gelu(__bfloat162float(a.y)) * __bfloat162float(g.y));
+    *reinterpret_cast<__nv_bfloat162*>(act + row * I + c) = o;
+}
+
+int fail_cuda(cudaError_t e) { return e == cudaSuccess ? RF_OK : RF_ERR_CUDA; }
+
+}  // namespace
+
+extern "C" {
+
+int rf_rope_qkv(void* qkv, const float* cosb, const float* sinb, int64_t tokens, int64_t S, int64_t H, int64_t d,
+                void* stream) {
+    if (qkv == nullptr || cosb == nullptr || sinb == nullptr || d % 2 || S <= 0) return RF_ERR_ARG;
+    const long long total = tokens * 2 * H * (d / 2);
+    if (total == 0) return RF_OK;
+    rope_qkv_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<__nv_bfloat16*>(qkv), cosb, sinb, tokens, static_cast<int>(S), static_cast<int>(H), static_cast<int>(d));
+    return fail_cuda(cudaGetLastError());
+}
+
+int rf_add_layernorm(float* x, const void* delta, const float* w, void* y, int64_t rows, int64_t n, float eps,
+                     void* stream) {
+    if (x == nullptr || (y != nullptr && w == nullptr) || n % 4 || n > 4096) return RF_ERR_ARG;
+    if (rows == 0) return RF_OK;
+    const unsigned grid = static_cast<unsigned>((rows + 3) / 4);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const __nv_bfloat16* dl = static_cast<const __nv_bfloat16*>(delta);
+    __nv_bfloat16* yy = static_cast<__nv_bfloat16*>(y);
+    if (n <= 1024)
+        add_layernorm_kernel<8><<<grid, 128, 0, st>>>(x, dl, w, yy, rows, static_cast<int>(n), eps);
+    else
+        add_layernorm_kernel<32><<<grid, 128, 0, st>>>(x, dl, w, yy, rows, static_cast<int>(n), eps);
+    return fail_cuda(cudaGetLastError());
+}
+
+int rf_geglu(const void* wi_out, void* act, int64_t rows, int64_t I, void* stream) {
+    if (wi_out == nullptr || act == nullptr || I % 2) return RF_ERR_ARG;
+    const long long total = rows * (I / 2);
+    if (total == 0) return RF_OK;
+    geglu_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const __nv_bfloat16*>(wi_out), static_cast<__nv_bfloat16*>(act), rows, static_cast<int>(I));
+    return fail_cuda(cudaGetLastError());
+}
+
+}  // extern "C"

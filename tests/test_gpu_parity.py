@@ -393,3 +393,73 @@ def test_long_sequences_o_n_memory(torch_mod, P):
     assert P.mask_memory_bytes(B, H, S, 2) == 25769803776  # what SDPA would have needed (24 GiB)
     o_ones = P.flash_attention(q, q, torch.ones_like(q), P.AttentionSpec(pad_bias=pb), out_dtype=torch.float32)
     assert (o_ones - 1.0).abs().max().item() <= 1e-2
+
+
+# ------------------------------------------------------------------ classifier (configs 2/3/5)
+def _small_cfg():
+    from paper_2603_12646_b200.classifier import ClassifierConfig
+    return ClassifierConfig(vocab_size=1000, n_layers=6, n_labels=3)
+
+
+def test_encoder_glue_kernels(torch_mod, P):
+    """rf_rope_qkv / rf_add_layernorm / rf_geglu against plain torch fp32 references of the same op."""
+    torch = torch_mod
+    from paper_2603_12646_b200 import capi
+    from paper_2603_12646_b200.classifier import rope_tables
+    lib = capi.load()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    B, S, H, d = 2, 77, 12, 64
+    qkv = torch.randn((B * S, 3, H, d), device="cuda", generator=g).to(torch.bfloat16)
+    ref = qkv.float().clone()
+    cos, sin = rope_tables(S, d, 10000.0, "cuda")
+    capi.check(lib.rf_rope_qkv(qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), B * S, S, H, d, None))
+    pos = torch.arange(B * S, device="cuda") % S
+    c, s_ = cos[pos][:, None, None, :], sin[pos][:, None, None, :]
+    qk = ref[:, :2]
+    want = torch.cat([qk[..., :32] * c - qk[..., 32:] * s_, qk[..., 32:] * c + qk[..., :32] * s_], -1)
+    assert (qkv[:, :2].float() - want).abs().max().item() <= 2e-2   # bf16 rounding of the result
+    assert torch.equal(qkv[:, 2].float(), ref[:, 2])                # V untouched
+    rows, n = 300, 768
+    x = torch.randn((rows, n), device="cuda", generator=g)
+    dl = torch.randn((rows, n), device="cuda", generator=g).to(torch.bfloat16)
+    w = torch.rand((n,), device="cuda", generator=g) + 0.5
+    x0 = x.clone()
+    y = torch.empty((rows, n), device="cuda", dtype=torch.bfloat16)
+    capi.check(lib.rf_add_layernorm(x.data_ptr(), dl.data_ptr(), w.data_ptr(), y.data_ptr(), rows, n, 1e-5, None))
+    xs = x0 + dl.float()
+    assert (x - xs).abs().max().item() <= 1e-6
+    wy = torch.nn.functional.layer_norm(xs, (n,), w, None, 1e-5)
+    assert (y.float() - wy).abs().max().item() <= 3e-2
+    I = 1152
+    wi = torch.randn((rows, 2 * I), device="cuda", generator=g).to(torch.bfloat16)
+    act = torch.empty((rows, I), device="cuda", dtype=torch.bfloat16)
+    capi.check(lib.rf_geglu(wi.data_ptr(), act.data_ptr(), rows, I, None))
+    wa = torch.nn.functional.gelu(wi[:, :I].float()) * wi[:, I:].float()
+    assert (act.float() - wa).abs().max().item() <= 3e-2
+
+
+@pytest.mark.parametrize("S,padded", [(512, False), (1024, True)])
+def test_classifier_logits_match_oracle_model(torch_mod, P, oracle, S, padded):
+    """Logits within 1e-2 of the fp32 oracle model (attention = reference operator) with identical
+    argmax (BASELINE.json north_star).  6-layer slice of the ModernBERT-base shape: layers 0 and 3
+    global, the rest local (63,64); full width (hidden 768, 12 x 64 heads, MLP 1152)."""
+    torch = torch_mod
+    from oracle_model import oracle_forward
+    from paper_2603_12646_b200.classifier import Classifier, init_weights
+    cfg = _small_cfg()
+    weights = init_weights(cfg, seed=1234)
+    g = torch.Generator().manual_seed(S)
+    B = 2
+    ids = torch.randint(0, cfg.vocab_size, (B, S), generator=g)
+    mask = None
+    if padded:
+        mask = torch.ones((B, S))
+        mask[0, S - S // 8:] = 0      # tools/main.cpp:88-98: ones then a zero tail of up to S/8
+        mask[1, S - 5:] = 0
+    model = Classifier(cfg, weights, torch.device("cuda:0"))
+    got = model.forward(ids.cuda(), mask.cuda() if mask is not None else None).cpu().numpy()
+    want = oracle_forward(cfg, weights, ids, mask, oracle)
+    margin = np.sort(want, axis=1)[:, -1] - np.sort(want, axis=1)[:, -2]
+    print("logits", got, want, "oracle top-2 margin", margin)
+    assert np.abs(got - want).max() <= 1e-2
+    assert (got.argmax(1) == want.argmax(1)).all()

@@ -174,6 +174,41 @@ def case_time(name, B, H, S, wl, wr, flags, iters=20, kernel="tcgen05"):
          "tflops": flops / ms / 1e9, "gbs": 4 * B * H * S * 64 * 2 / ms / 1e6})
 
 
+def case_clf(name, S, B=1, iters=5, padded=False):
+    import torch
+    from paper_2603_12646_b200.classifier import Classifier, ClassifierConfig, init_weights
+    cfg = ClassifierConfig()
+    dev = torch.device("cuda:0")
+    model = Classifier(cfg, init_weights(cfg, 7), dev)
+    ids = torch.randint(0, cfg.vocab_size, (B, S), device=dev)
+    mask = None
+    if padded:
+        mask = torch.ones((B, S), device=dev)
+        mask[:, S - S // 8:] = 0
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    for _ in range(2):
+        logits = model.forward(ids, mask)
+    torch.cuda.synchronize()
+    peak = torch.cuda.max_memory_allocated()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        logits = model.forward(ids, mask)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    model.forward(ids, mask, time_layers=True)
+    lm = model.last_layer_ms
+    ga = [x["attention_ms"] for x in lm if x["global"]]
+    la = [x["attention_ms"] for x in lm if not x["global"]]
+    log({"case": name, "S": S, "B": B, "padded": padded, "ms_per_forward": ms, "ms_per_request": ms / B,
+         "weights_MB": model.weight_bytes() / 1e6, "peak_activation_MB": (peak - base) / 1e6,
+         "session_MB": peak / 1e6, "global_attn_ms_avg": sum(ga) / len(ga), "local_attn_ms_avg": sum(la) / len(la),
+         "attn_ms_total": sum(ga) + sum(la), "logits": logits[0].tolist()})
+
+
 CASES = {
     "probe0": lambda: case_probe(0),
     "probe1": lambda: case_probe(1),
@@ -201,6 +236,10 @@ CASES = {
     "time_16k_ts": lambda: case_time("time_16k_ts", 1, 12, 16384, -1, -1, 0, iters=10),
     "time_32k_ts": lambda: case_time("time_32k_ts", 1, 12, 32768, -1, -1, 0, iters=5),
     "time_8k_local_ts": lambda: case_time("time_8k_local_ts", 1, 12, 8192, 63, 64, 0),
+    "clf_8k": lambda: case_clf("clf_8k", 8192),
+    "clf_8k_pad": lambda: case_clf("clf_8k_pad", 8192, padded=True),
+    "clf_16k_b4": lambda: case_clf("clf_16k_b4", 16384, B=4, iters=3),
+    "clf_32k": lambda: case_clf("clf_32k", 32768, iters=3),
     "time_8k_simt": lambda: case_time("time_8k_simt", 1, 12, 8192, -1, -1, 0, iters=3, kernel="simt"),
 }
 
