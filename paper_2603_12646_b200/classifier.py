@@ -126,7 +126,7 @@ class Classifier:
                 pad_bias = pad_bias_from_mask(attention_mask.to(self.device, torch.float32).reshape(B, 1, 1, S))
             x = self.w["tok_emb"][input_ids.reshape(-1)].float()                 # f32 stream [rows, hid]
             h = self._add_layernorm(x, None, self.w["emb_norm"])
-            x = h.float()                                                         # stream = LN(embeddings)
+            x.copy_(h)                                                            # stream = LN(embeddings)
             delta = None
             ev = []
             for i in range(cfg.n_layers):
@@ -136,6 +136,7 @@ class Classifier:
                 if i > 0:
                     h = self._add_layernorm(x, delta, self.w[f"l{i}.attn_norm"])  # x += mlp(i-1); h = LN(x)
                 qkv = h @ self.w[f"l{i}.wqkv"].t()                                # [rows, 3*hid] == [B,S,3,H,d]
+                del h, delta                                                      # keep the live set small (32K)
                 glob = cfg.is_global(i)
                 cos, sin = self._rope_tables(S, glob)
                 capi.check(lib.rf_rope_qkv(qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), rows, S, H, d, self._stream()))
@@ -150,8 +151,11 @@ class Classifier:
                                 out=attn.view(B, S, H, d).permute(0, 2, 1, 3))
                 if time_layers:
                     a1.record()
+                del qkv, q5, qv, kv, vv
                 o = attn.view(rows, hid) @ self.w[f"l{i}.wo"].t()
+                del attn
                 h2 = self._add_layernorm(x, o, self.w[f"l{i}.mlp_norm"])          # x += attn; h2 = LN(x)
+                del o
                 delta = torch.empty((rows, hid), device=self.device, dtype=torch.bfloat16)
                 for r0 in range(0, rows, cfg.mlp_chunk_rows):                     # bounded MLP intermediate
                     r1 = min(rows, r0 + cfg.mlp_chunk_rows)
@@ -159,6 +163,9 @@ class Classifier:
                     act = torch.empty((r1 - r0, cfg.mlp), device=self.device, dtype=torch.bfloat16)
                     capi.check(lib.rf_geglu(wi_out.data_ptr(), act.data_ptr(), r1 - r0, cfg.mlp, self._stream()))
                     torch.matmul(act, self.w[f"l{i}.wo2"].t(), out=delta[r0:r1])
+                    del wi_out, act
+                del h2
+                h = None
                 if time_layers:
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record()
@@ -173,6 +180,33 @@ class Classifier:
                 self.last_layer_ms = [{"layer": i, "global": g_, "layer_ms": e0.elapsed_time(e1), "attention_ms": a0.elapsed_time(a1)}
                                       for i, (g_, e0, e1, a0, a1) in enumerate(ev)]
         return logits
+
+    def capture(self, batch: int, seq_len: int, with_mask: bool):
+        """CUDA-graph the whole forward for a fixed (batch, seq_len): the ~300 launches of a
+        22-layer forward are replayed as one graph, which removes the launch gaps that dominate
+        the HBM-bound local layers.  Returns run(input_ids, attention_mask) -> logits."""
+        ids_buf = torch.zeros((batch, seq_len), dtype=torch.int64, device=self.device)
+        mask_buf = torch.ones((batch, seq_len), dtype=torch.float32, device=self.device) if with_mask else None
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            for _ in range(2):  # warm-up outside capture (cuBLAS workspaces, lazy kernel loads)
+                self.forward(ids_buf, mask_buf)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            out = self.forward(ids_buf, mask_buf)
+
+        def run(input_ids, attention_mask=None):
+            ids_buf.copy_(input_ids, non_blocking=True)
+            if mask_buf is not None:
+                mask_buf.copy_(attention_mask, non_blocking=True)
+            graph.replay()
+            return out
+
+        run.graph = graph
+        return run
 
     def weight_bytes(self) -> int:
         return sum(v.numel() * v.element_size() for v in self.w.values())

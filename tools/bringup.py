@@ -199,11 +199,27 @@ def case_clf(name, S, B=1, iters=5, padded=False):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
+    graph_ms = None
+    try:
+        run = model.capture(B, S, padded)
+        for _ in range(2):
+            lg = run(ids, mask)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            lg = run(ids, mask)
+        e1.record()
+        torch.cuda.synchronize()
+        graph_ms = e0.elapsed_time(e1) / iters
+        graph_diff = (lg - logits).abs().max().item()
+    except Exception as e:  # noqa: BLE001
+        graph_diff = repr(e)[:200]
     model.forward(ids, mask, time_layers=True)
     lm = model.last_layer_ms
     ga = [x["attention_ms"] for x in lm if x["global"]]
     la = [x["attention_ms"] for x in lm if not x["global"]]
     log({"case": name, "S": S, "B": B, "padded": padded, "ms_per_forward": ms, "ms_per_request": ms / B,
+         "graph_ms_per_forward": graph_ms, "graph_vs_eager_maxdiff": graph_diff,
          "weights_MB": model.weight_bytes() / 1e6, "peak_activation_MB": (peak - base) / 1e6,
          "session_MB": peak / 1e6, "global_attn_ms_avg": sum(ga) / len(ga), "local_attn_ms_avg": sum(la) / len(la),
          "attn_ms_total": sum(ga) + sum(la), "logits": logits[0].tolist()})
