@@ -261,6 +261,34 @@ def run_ours(args):
             bytes_l = 4.0 * B * H * S * D * 2
             extra["S8192_local_63_64"] = {"ms": msl, "gbs": bytes_l / msl / 1e6, "frac_of_hbm": bytes_l / msl / 1e6 / peaks["hbm"],
                                           "bound": "hbm"}
+            # classifier forward (configs[1]): ModernBERT-base shape, B=1, S=8192, random-init weights
+            try:
+                from paper_2603_12646_b200.classifier import Classifier, ClassifierConfig, init_weights
+                ccfg = ClassifierConfig()
+                clf = Classifier(ccfg, init_weights(ccfg, 7), torch.device("cuda", local_rank))
+                ids = torch.randint(0, ccfg.vocab_size, (1, S), device="cuda")
+                run = clf.capture(1, S, with_mask=False)
+                for _ in range(3):
+                    run(ids)
+                torch.cuda.synchronize()
+                c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                c0.record()
+                for _ in range(10):
+                    lg = run(ids)
+                c1.record()
+                torch.cuda.synchronize()
+                clf.forward(ids, None, time_layers=True)
+                lm = clf.last_layer_ms
+                extra["classifier_fwd_S8192_B1"] = {
+                    "ms_per_request": c0.elapsed_time(c1) / 10, "layers": ccfg.n_layers,
+                    "attention_ms_total": sum(x["attention_ms"] for x in lm),
+                    "global_attention_ms_avg": sum(x["attention_ms"] for x in lm if x["global"]) / max(1, sum(1 for x in lm if x["global"])),
+                    "local_attention_ms_avg": sum(x["attention_ms"] for x in lm if not x["global"]) / max(1, sum(1 for x in lm if not x["global"])),
+                    "weights_MB": clf.weight_bytes() / 1e6, "cuda_graph": True,
+                    "paper_mi300x_ms": 105.0, "note": "random-init weights, synthetic token ids; paper number is other hardware (PAPER.md:402)"}
+                del clf, run
+            except Exception as e:  # noqa: BLE001
+                extra["classifier_fwd_S8192_B1"] = {"error": repr(e)[:200]}
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
         if os.path.exists(prof):

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -153,7 +154,7 @@ struct Plan {
     int kernel;
     int sched_mode;   // tcgen05 only
     int grid;         // CTAs
-    int64_t total_pairs, pairs_per_head;
+    int64_t total_pairs, pairs_per_head, tiles_per_pair;
     size_t bias_bytes, flag_bytes_bias, part_bytes;
     size_t workspace_bytes() const { return bias_bytes + flag_bytes_bias + part_bytes; }
 };
@@ -174,11 +175,20 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         pl.bias_bytes = align_up(static_cast<size_t>(p->B) * nt * rf::kBlockN * sizeof(float), 256);
         pl.flag_bytes_bias = align_up(static_cast<size_t>(p->B) * nt, 256);
     }
-    // dense global attention over more pairs than SMs: persistent balanced schedule
-    const bool dense = p->pad_bias == nullptr && p->window_left < 0 && p->window_right < 0 && !r.partial &&
-                       r.kv_begin == 0 && r.kv_end == p->S;
+    // more query-tile pairs than SMs: persistent, statically balanced schedule over the flat
+    // (pair x key tile) space.  tiles_per_pair bounds the key tiles any pair touches.
+    {
+        const int64_t t_begin = r.kv_begin / rf::kBlockN;
+        const int64_t t_end = (r.kv_end + rf::kBlockN - 1) / rf::kBlockN;
+        int64_t tiles = t_end - t_begin;
+        if (p->window_left >= 0 && p->window_right >= 0) {
+            const int64_t span = rf::kRowsPerCta + p->window_left + p->window_right;  // keys a pair can see
+            tiles = std::min<int64_t>(tiles, (span + rf::kBlockN - 1) / rf::kBlockN + 1);
+        }
+        pl.tiles_per_pair = std::max<int64_t>(tiles, 1);
+    }
     const int sms = sm_count_or_default();
-    if (dense && pl.total_pairs > sms) {
+    if (!r.partial && pl.total_pairs > sms) {
         pl.sched_mode = 1;
         pl.grid = sms;
         pl.part_bytes = align_up(rf::fa_fwd_sm100_partial_bytes(pl.grid), 256);
@@ -340,6 +350,7 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     f.sched_mode = pl.sched_mode;
     f.total_pairs = static_cast<int>(pl.total_pairs);
     f.pairs_per_head = static_cast<int>(pl.pairs_per_head);
+    f.tiles_per_pair = static_cast<int>(pl.tiles_per_pair);
     if (pl.sched_mode == 1) {
         void* flag_ptr = nullptr;
         size_t flag_bytes = 0;

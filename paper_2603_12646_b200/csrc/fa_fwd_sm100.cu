@@ -117,7 +117,7 @@ __device__ __forceinline__ bool tile_live(const FaParams& p, int b, int n) {
 __device__ __forceinline__ void sched_init(const FaParams& p, Sched& s) {
     s.done = false;
     if (p.sched_mode == 1) {
-        const long long total = static_cast<long long>(p.total_pairs) * p.n_kv_tiles;
+        const long long total = static_cast<long long>(p.total_pairs) * p.tiles_per_pair;
         s.t = total * blockIdx.x / gridDim.x;
         s.t_end = total * (blockIdx.x + 1) / gridDim.x;
     } else {
@@ -127,22 +127,20 @@ __device__ __forceinline__ void sched_init(const FaParams& p, Sched& s) {
 
 template <bool kHasBias>
 __device__ __forceinline__ bool next_item(const FaParams& p, Sched& s, Item& it) {
-    int pair_lin;
+    int pair_lin, k0 = 0, k1 = 0x7fffffff;
     if (p.sched_mode == 1) {
         if (s.t >= s.t_end) return false;
-        const int K = p.n_kv_tiles;
+        const int K = p.tiles_per_pair;  // virtual key tiles per pair (upper bound of any pair's range)
         pair_lin = static_cast<int>(s.t / K);
-        const int k0 = static_cast<int>(s.t - static_cast<long long>(pair_lin) * K);
-        const int k1 = static_cast<int>(min(static_cast<long long>(K), k0 + (s.t_end - s.t)));
+        k0 = static_cast<int>(s.t - static_cast<long long>(pair_lin) * K);
+        k1 = static_cast<int>(min(static_cast<long long>(K), k0 + (s.t_end - s.t)));
         s.t += k1 - k0;
-        it.n0 = k0;
-        it.n1 = k1;
-        it.num_live = k1 - k0;
         it.kind = k0 > 0 ? kItemHeadPart : (k1 < K ? kItemTailPart : kItemFull);
     } else {
         if (s.done) return false;
         s.done = true;
         pair_lin = blockIdx.x;
+        it.kind = kItemFull;
     }
     const int px = pair_lin % p.pairs_per_head;
     const int bh = pair_lin / p.pairs_per_head;
@@ -150,18 +148,19 @@ __device__ __forceinline__ bool next_item(const FaParams& p, Sched& s, Item& it)
     it.b = bh / p.H;
     it.q0 = px * kRowsPerCta;
     it.has_b = it.q0 + kBlockM < p.S;
-    if (p.sched_mode != 1) {
-        // key-tile range of this pair (union over its rows of window and split range)
-        const int rows_end = min(it.q0 + kRowsPerCta, p.S);
-        int j_lo = p.kv_begin, j_hi = p.kv_end;
-        if (p.wl >= 0) j_lo = max(j_lo, it.q0 - p.wl);
-        if (p.wr >= 0) j_hi = min(j_hi, rows_end + p.wr);
-        it.n0 = j_lo >> 7;
-        it.n1 = (j_hi > j_lo) ? ((j_hi + kBlockN - 1) >> 7) : it.n0;
-        it.num_live = 0;
-        for (int n = it.n0; n < it.n1; ++n) it.num_live += tile_live<kHasBias>(p, it.b, n) ? 1 : 0;
-        it.kind = kItemFull;
-    }
+    // key-tile range of this pair (union over its rows of window and split range) ...
+    const int rows_end = min(it.q0 + kRowsPerCta, p.S);
+    int j_lo = p.kv_begin, j_hi = p.kv_end;
+    if (p.wl >= 0) j_lo = max(j_lo, it.q0 - p.wl);
+    if (p.wr >= 0) j_hi = min(j_hi, rows_end + p.wr);
+    const int pn0 = j_lo >> 7;
+    const int pn1 = (j_hi > j_lo) ? ((j_hi + kBlockN - 1) >> 7) : pn0;
+    // ... cut to this item's slice of it (mode 1: virtual tile v is real tile pn0 + v; slices past
+    // the pair's last tile are empty)
+    it.n0 = min(pn0 + k0, pn1);
+    it.n1 = (k1 >= pn1 - pn0) ? pn1 : pn0 + k1;
+    it.num_live = 0;
+    for (int n = it.n0; n < it.n1; ++n) it.num_live += tile_live<kHasBias>(p, it.b, n) ? 1 : 0;
     return true;
 }
 
@@ -172,6 +171,27 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
 }
 __device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
+
+// O rows (32 columns of this thread's lane) *= alpha.  QK^T runs ahead of PV (rotating S buffers),
+// so "S ready" does not imply that PV of the previous tile has finished.  The V-empty barrier of
+// that tile is committed after both of its PVs: wait for its phase first (it is at most one phase
+// away, so the parity wait is exact).
+__device__ __noinline__ void rescale_o_rows(uint32_t t_o, float alpha, uint32_t v_empty_bar, uint32_t parity) {
+    mbar_wait(v_empty_bar, parity);
+    tc_fence_after();
+    uint32_t o[32];
+    tmem_ld32(t_o, o);
+    tc_wait_ld();
+#pragma unroll
+    for (int u = 0; u < 32; u += 2) {
+        float a0 = __uint_as_float(o[u]), a1 = __uint_as_float(o[u + 1]);
+        fmul2(a0, a1, alpha);
+        o[u] = __float_as_uint(a0);
+        o[u + 1] = __float_as_uint(a1);
+    }
+    tmem_st32(t_o, o);
+    tc_wait_st();
 }
 
 template <bool kBf16, bool kHasBias>
@@ -421,7 +441,8 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         uint32_t bars_r = bars;
         asm volatile("mov.u32 %0, %0;" : "+r"(bars_r));
 
-        uint32_t oi = 0;    // items this warpgroup worked on so far (O barrier phase)
+        uint32_t oi = 0;    // items this warpgroup worked on so far (O-full barrier phase)
+        uint32_t vc = 0;    // V tiles consumed by the tensor pipe in earlier items (V ring position)
         uint32_t g = x;     // sequence index 2*t + x of this warpgroup's next tile
         uint32_t par_bits = 0;  // bit s = phase parity of the next use of S buffer s (both tiles' uses counted)
         uint32_t xpar = 0;  // exchange double buffer
@@ -573,21 +594,12 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     l_run = l_run * alpha + (sum0 + sum1);
                     m_ref = m_new;
 
-                    // O_X *= alpha for rows whose reference max moved (PV of the previous tile has
-                    // completed: this S buffer was committed after it on the in-order tensor pipe).
-                    // Each half rescales its own 32 of the 64 output columns.
+                    // O_X *= alpha for rows whose reference max moved (rare after the first tiles thanks
+                    // to the lazy threshold): kept out of line so the hot loop stays compact.
                     if (it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
-                        uint32_t o[32];
-                        tmem_ld32(t_o, o);
-                        tc_wait_ld();
-#pragma unroll
-                        for (int u = 0; u < 32; u += 2) {
-                            float a0 = __uint_as_float(o[u]), a1 = __uint_as_float(o[u + 1]);
-                            fmul2(a0, a1, alpha);
-                            o[u] = __float_as_uint(a0);
-                            o[u + 1] = __float_as_uint(a1);
-                        }
-                        tmem_st32(t_o, o);
+                        const uint32_t vprev = vc + static_cast<uint32_t>(it) - 1u;
+                        rescale_o_rows(t_o, alpha, bars_r + 8u * (kBarVEmpty + vprev % kStagesV),
+                                       (vprev / kStagesV) & 1u);
                     }
                     tc_wait_st();
                     tc_fence_before();
@@ -607,8 +619,9 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 // tile B sits this item out: account for tile A's uses of the shared S buffers
                 for (int i = 0; i < num_live; ++i) par_bits ^= 1u << ((g - 1u + 2u * i) % kSBufs);
             }
-            // keep the sequence counter of both warpgroups in step even when tile B sat this item out
+            // keep the sequence counters of both warpgroups in step even when tile B sat this item out
             g += 2u * static_cast<uint32_t>(num_live);
+            vc += static_cast<uint32_t>(num_live);
 
             if (active) {
                 // ---------------- epilogue ----------------
@@ -624,7 +637,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const int col0 = hf * kOutCols;
                 float o[kOutCols];
                 if (num_live > 0) {
-                    mbar_wait(bars_r + 8u * (kBarOFull + x), oi & 1);
+                    mbar_wait(bars_r + 8u * (kBarOFull + x), oi & 1u);
                     tc_fence_after();
                     tmem_ld32(t_o, reinterpret_cast<uint32_t(&)[32]>(o));
                     tc_wait_ld();

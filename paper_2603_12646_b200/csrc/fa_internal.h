@@ -43,6 +43,7 @@ struct FaParams {
     int sched_mode;
     int total_pairs;     // B * H * pairs_per_head
     int pairs_per_head;  // ceil(S / 256)
+    int tiles_per_pair;  // mode 1: upper bound of the key tiles any pair touches (virtual tiles per pair)
     float* part_o;       // mode 1 workspace: partials of pairs cut between two CTAs
     float* part_ml;
     int* part_flag;
