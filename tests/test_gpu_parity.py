@@ -489,3 +489,21 @@ def test_classifier_logits_match_oracle_model(torch_mod, P, oracle, S, padded):
     print("logits", got, want, "oracle top-2 margin", margin)
     assert np.abs(got - want).max() <= 1e-2
     assert (got.argmax(1) == want.argmax(1)).all()
+
+
+def test_cpp_mirror_attention_test(torch_mod):
+    """Builds and runs tests/cpp/attention_test.cpp: the C++ mirror of the reference interface
+    (include/routefast_b200/attention.hpp) against an independently coded f64 reference."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "tests", "cpp", "attention_test")
+    libdir = os.path.join(root, "paper_2603_12646_b200")
+    if not os.path.exists(exe):
+        cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+        subprocess.run([cxx, "-std=c++17", "-O2", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "tests", "cpp", "attention_test.cpp"), "-o", exe,
+                        "-L", libdir, "-l:librf_fa.so", f"-Wl,-rpath,{libdir}"], check=True)
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(res.stdout[-2000:], res.stderr[-2000:])
+    assert res.returncode == 0 and "all checks passed" in res.stdout
