@@ -60,3 +60,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
 if __name__ == "__main__":
     import sys
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+
+
+def build_variant(name: str, defines: dict) -> str:
+    """Developer aid: an experimental build of the same ABI with -D overrides (kernel tuning);
+    select it at run time with RF_FA_LIB=<path>."""
+    out = os.path.join(HERE, f"librf_fa_{name}.so")
+    cmd = [nvcc_path()] + NVCC_FLAGS + [f"-D{k}={v}" for k, v in defines.items()] + ["-o", out] + sources()
+    env = dict(os.environ)
+    env.pop("CC", None)
+    env.pop("CXX", None)
+    res = subprocess.run(cmd, capture_output=True, text=True, env=env)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    return out

@@ -67,6 +67,38 @@ constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;    // + 128 * buffer
 constexpr uint32_t kColO = 384;  // + 64 * X
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P <= 2^8 before a rescale is forced
+// Ping-pong of the exponential phases: on every SM sub-partition the two warps of tile A and the two
+// warps of tile B take strict turns on the MUFU pipe (A0, B0, A1, B1, ...), so that one tile's
+// max / exchange / TMEM traffic always overlaps the other tile's exponentials instead of all four
+// warps convoying through the same phase.
+#ifndef RF_FA_PINGPONG
+#define RF_FA_PINGPONG 0
+#endif
+constexpr bool kPingPong = RF_FA_PINGPONG != 0;
+// Developer build only (-DRF_FA_TRACE=1): softmax warps of CTA 0 stamp the SM clock at their phase
+// boundaries into the debug_scores buffer, [16 warps][64 tiles][8 stamps] u32 (tools/trace_phases.py).
+#ifndef RF_FA_TRACE
+#define RF_FA_TRACE 0
+#endif
+// Developer build only (-DRF_FA_MMAONLY=1): the softmax warps skip their work (results are garbage);
+// what remains is the TMA + UMMA pipeline, i.e. the tensor-pipe floor of this tiling.
+#ifndef RF_FA_MMAONLY
+#define RF_FA_MMAONLY 0
+#endif
+// 1: the softmax warps check the V(i) / K(i+2) TMA barriers (while they wait for S) so that the UMMA
+// warp's steady-state loop has two barrier waits per key tile; 0: the UMMA warp waits for them itself.
+#ifndef RF_FA_VK_IN_SOFTMAX
+#define RF_FA_VK_IN_SOFTMAX 0
+#endif
+#if RF_FA_TRACE
+#define RF_STAMP(slot)                                                                               \
+    do {                                                                                             \
+        if (blockIdx.x == 0 && lane == 0 && trace_n < 64 && p.debug_scores != nullptr)               \
+            reinterpret_cast<uint32_t*>(p.debug_scores)[(warp * 64 + trace_n) * 8 + (slot)] = clock(); \
+    } while (0)
+#else
+#define RF_STAMP(slot) do { } while (0)
+#endif
 
 // dynamic shared memory map (offsets from a 1024B-aligned base)
 struct Smem {
@@ -74,7 +106,7 @@ struct Smem {
     static constexpr uint32_t k = q + 2 * kTileBytes;                  // kStagesK tiles
     static constexpr uint32_t v = k + kStagesK * kTileBytes;           // kStagesV tiles
     static constexpr uint32_t bars = v + kStagesV * kTileBytes;        // barrier block
-    static constexpr uint32_t bar_bytes = 256;
+    static constexpr uint32_t bar_bytes = 512;
     static constexpr uint32_t xchg = bars + bar_bytes;                 // row-max exchange: [2 parity][2 tile][2 half][128] f32
     static constexpr uint32_t xchg_bytes = 2 * 2 * 2 * kBlockM * 4;
 };
@@ -89,7 +121,8 @@ enum : uint32_t {
     kBarSFull = kBarVEmpty + kStagesV,   // [kSBufs] one per S buffer: no phase can be skipped
     kBarPFull = kBarSFull + kSBufs,      // [kSBufs]
     kBarOFull = kBarPFull + kSBufs,      // [2]
-    kNumBars = kBarOFull + 2,
+    kBarTurn = kBarOFull + 2,            // [2 tiles][4 quadrants] exp-phase turn of (tile, SM sub-partition)
+    kNumBars = kBarTurn + 8,
 };
 static_assert(kNumBars * 8 + 8 <= Smem::bar_bytes, "barrier block too small");
 
@@ -230,6 +263,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             mbar_init(bar(kBarPFull + s), 2 * kBlockM);
         }
         for (int x = 0; x < 2; ++x) mbar_init(bar(kBarOFull + x), 1);
+        for (int i = 0; i < 8; ++i) mbar_init(bar(kBarTurn + i), 64);  // both warps of the other tile arrive
         fence_barrier_init();
     }
     if (warp == kMmaWarp) {
@@ -327,39 +361,51 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             __syncwarp();
         };
 
-        uint32_t qi = 0, kc = 0, vc = 0, tc = 0;  // items / K tiles / V tiles / tiles consumed so far
+        // Loop state is kept incremental (no divisions) and small: this warp runs on 32 registers.
+        // K and V tiles live at the same ring positions in every item (kc == vc == tiles so far).
+        uint32_t qi = 0;        // items with work so far (Q barrier phase)
+        uint32_t kc = 0;        // key tiles consumed in earlier items (K ring position, parity)
+        uint32_t ks = 0;        // K ring stage of the item's tile 0
+        uint32_t vs = 0;        // V ring stage of the item's tile 0
+        uint32_t vp = 0;        // ... and the phase parity of that use
+        uint32_t sa = 0;        // S buffer of tile A of the item's key tile 0 (tile B: sa + 1 mod 3)
         uint32_t par_bits = 0;  // bit s = phase parity of the next use of S buffer s (S-full / P-full barriers)
+        auto inc_mod = [](uint32_t v, uint32_t add, uint32_t mod) {
+            v += add;
+            return v >= mod ? v - mod : v;
+        };
+        // pins a prepared operand word in a register before a barrier wait (keeps the descriptor
+        // arithmetic off the wait -> first UMMA critical path)
+        auto pin = [](uint32_t& v) { asm volatile("" : "+r"(v)); };
+        const uint32_t q_lo = kLboK | (sb16 + Smem::q / 16);
+        const uint32_t k_lo = kLboK | (sb16 + Smem::k / 16);
+        const uint32_t v_lo = kLboV | (sb16 + Smem::v / 16);
+        constexpr uint32_t kTile16 = kTileBytes / 16;
+
         while (next_item<kHasBias>(p, sched, item)) {
             const int num_live = item.num_live;
             if (num_live == 0) continue;
             const bool has_b = item.has_b;
 
-            // tile g = 2*t + x of the A,B,A,B,... sequence lives in S buffer g % 3
-            auto sbuf = [&](int i, int x) { return (2 * (tc + i) + x) % kSBufs; };
-
             // S = Q_X * K^T : both operands K-major (head dim contiguous), 128B swizzle,
             // 8-row core-matrix groups 1024 B apart; a K=16 step advances 32 B inside the atom.
-            auto issue_qk = [&](int x, int i) {
-                const uint32_t qlo = kLboK | (sb16 + (Smem::q + x * kTileBytes) / 16);
-                const uint32_t klo = kLboK | (sb16 + (Smem::k + ((kc + i) % kStagesK) * kTileBytes) / 16);
-                const uint32_t td = tmem_base + kColS + sbuf(i, x) * kBlockN;
-                const uint32_t sbar = bar(kBarSFull + sbuf(i, x));
+            auto issue_qk = [&](uint32_t x, uint32_t kstage, uint32_t buf) {
+                const uint32_t qlo = q_lo + x * kTile16;
+                const uint32_t klo = k_lo + kstage * kTile16;
+                const uint32_t td = tmem_base + kColS + buf * kBlockN;
                 if (leader) {
 #pragma unroll
                     for (int kk = 0; kk < kHeadDim / 16; ++kk)
                         mma_ss(td, desc(qlo + kk * 2), desc(klo + kk * 2), idesc_qk, kk > 0 ? 1u : 0u);
-                    tc_commit(sbar);
+                    tc_commit(bar(kBarSFull + buf));
                 }
                 __syncwarp();
             };
             // O_X += P * V : B operand V is [key][d] with d contiguous = MN-major, 128B swizzle;
             // 8-key groups 1024 B apart (SBO); a K=16 step advances 16 keys = 2048 B.
             // A = P from TMEM: 16 bf16 per row per step = 8 packed 32-bit columns.
-            auto issue_pv = [&](int x, int i) {
-                const uint32_t vlo = kLboV | (sb16 + (Smem::v + ((vc + i) % kStagesV) * kTileBytes) / 16);
+            auto issue_pv = [&](uint32_t x, uint32_t vlo, uint32_t ta, uint32_t acc0) {
                 const uint32_t td = tmem_base + kColO + x * kHeadDim;
-                const uint32_t ta = tmem_base + kColS + sbuf(i, x) * kBlockN;
-                const uint32_t acc0 = i > 0 ? 1u : 0u;
                 if (leader) {
 #pragma unroll
                     for (int kk = 0; kk < kBlockN / 16; ++kk)
@@ -367,59 +413,99 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 }
                 __syncwarp();
             };
-            auto wait_k = [&](int i) {
-                mbar_wait(bar(kBarKFull + (kc + i) % kStagesK), ((kc + i) / kStagesK) & 1);
+            // K/V-full barriers are waited for by THIS warp only for the item's first two key tiles;
+            // in the steady state the softmax warps check them before they publish P (see there), so
+            // that this loop has exactly two waits per key tile.
+            auto wait_k = [&](uint32_t i) {
+                mbar_wait(bar(kBarKFull + ((kc + i) & (kStagesK - 1))), ((kc + i) / kStagesK) & 1);
                 tc_fence_after();
             };
-            // every QK^T that reads K tile i has been issued; the last one of the item also frees Q
-            auto release_k = [&](int i) {
-                commit(bar(kBarKEmpty + (kc + i) % kStagesK));
-                if (i == num_live - 1) commit(bar(kBarQEmpty));
+            static_assert((kStagesK & (kStagesK - 1)) == 0, "K ring depth must be a power of two");
+            // every QK^T that reads the K tile in `kstage` has been issued; the item's last one also frees Q
+            auto release_k = [&](uint32_t kstage, bool last_of_item) {
+                commit(bar(kBarKEmpty + kstage));
+                if (last_of_item) commit(bar(kBarQEmpty));
             };
 
             // prologue: S_A(0), S_B(0), and already S_A(1) into the third buffer
+            uint32_t buf_a = sa;                        // S buffer of A(i); B(i) uses the next one
+            uint32_t ks1 = inc_mod(ks, 1, kStagesK);    // K stage of tile i+1
+            uint32_t vsi = vs, vpi = vp;                // V stage of tile i and its phase parity
             mbar_wait(bar(kBarQFull), qi & 1);
             wait_k(0);
-            issue_qk(0, 0);
-            if (has_b) issue_qk(1, 0);
-            release_k(0);
+            issue_qk(0, ks, buf_a);
+            if (has_b) issue_qk(1, ks, inc_mod(buf_a, 1, kSBufs));
+            release_k(ks, num_live == 1);
             if (num_live > 1) {
                 wait_k(1);
-                issue_qk(0, 1);
-                if (!has_b) release_k(1);
+                issue_qk(0, ks1, inc_mod(buf_a, 2, kSBufs));
+                if (!has_b) release_k(ks1, num_live == 2);
             }
 
             for (int i = 0; i < num_live; ++i) {
                 const bool last = i + 1 == num_live;
-                mbar_wait(bar(kBarVFull + (vc + i) % kStagesV), ((vc + i) / kStagesV) & 1);
+                const uint32_t buf_b = inc_mod(buf_a, 1, kSBufs), buf_c = inc_mod(buf_a, 2, kSBufs);
+                const uint32_t ks2 = inc_mod(ks1, 1, kStagesK);
+#if RF_FA_TRACE
+                const int trace_n = i;
+#endif
+                RF_STAMP(0);
                 // ---- P_A(i) ready: O_A += P_A V; its S buffer is then free for S_B(i+1) ----
-                const uint32_t buf_a = sbuf(i, 0), buf_b = sbuf(i, 1);
-                mbar_wait(bar(kBarPFull + buf_a), (par_bits >> buf_a) & 1u);
+                uint32_t vlo = v_lo + vsi * kTile16;
+                uint32_t ta = tmem_base + kColS + buf_a * kBlockN;
+                pin(vlo);
+                pin(ta);
+                RF_STAMP(1);
+                if (!RF_FA_VK_IN_SOFTMAX)  // V(i) was requested tiles ago: check it in the shadow of the P wait
+                    mbar_wait2(bar(kBarVFull + vsi), vpi, bar(kBarPFull + buf_a), (par_bits >> buf_a) & 1u);
+                else
+                    mbar_wait(bar(kBarPFull + buf_a), (par_bits >> buf_a) & 1u);  // implies V(i) has landed
                 tc_fence_after();
-                issue_pv(0, i);
+                RF_STAMP(2);
+                issue_pv(0, vlo, ta, i > 0 ? 1u : 0u);
                 if (last) commit(bar(kBarOFull + 0));
                 if (has_b) {
                     if (!last) {
-                        issue_qk(1, i + 1);  // K(i+1) was waited for when S_A(i+1) was issued
-                        release_k(i + 1);
+                        issue_qk(1, ks1, buf_a);  // K(i+1) was waited for when S_A(i+1) was issued
+                        release_k(ks1, i + 2 == num_live);
                     }
+                    RF_STAMP(3);
                     // ---- P_B(i) ready: O_B += P_B V; its S buffer is then free for S_A(i+2) ----
-                    mbar_wait(bar(kBarPFull + buf_b), (par_bits >> buf_b) & 1u);
+                    ta = tmem_base + kColS + buf_b * kBlockN;
+                    pin(ta);
+                    if (!RF_FA_VK_IN_SOFTMAX && i + 2 < num_live)  // K(i+2) for the S_A(i+2) issued right after
+                        mbar_wait2(bar(kBarKFull + ks2), ((kc + i + 2) / kStagesK) & 1,
+                                   bar(kBarPFull + buf_b), (par_bits >> buf_b) & 1u);
+                    else
+                        mbar_wait(bar(kBarPFull + buf_b), (par_bits >> buf_b) & 1u);  // implies K(i+2) has landed
                     tc_fence_after();
-                    issue_pv(1, i);
+                    RF_STAMP(4);
+                    issue_pv(1, vlo, ta, i > 0 ? 1u : 0u);
                     if (last) commit(bar(kBarOFull + 1));
                 }
                 par_bits ^= (1u << buf_a) ^ (has_b ? (1u << buf_b) : 0u);
-                commit(bar(kBarVEmpty + (vc + i) % kStagesV));
+                commit(bar(kBarVEmpty + vsi));
+                RF_STAMP(5);
                 if (i + 2 < num_live) {
-                    wait_k(i + 2);
-                    issue_qk(0, i + 2);
-                    if (!has_b) release_k(i + 2);
+                    if (!RF_FA_VK_IN_SOFTMAX && !has_b) wait_k(i + 2);
+                    RF_STAMP(6);
+                    issue_qk(0, ks2, buf_b);
+                    if (!has_b) release_k(ks2, i + 3 == num_live);
+                }
+                RF_STAMP(7);
+                buf_a = buf_c;
+                ks1 = ks2;
+                if (++vsi == kStagesV) {
+                    vsi = 0;
+                    vpi ^= 1u;
                 }
             }
+            // ring positions of the next item's tile 0
             kc += num_live;
-            vc += num_live;
-            tc += num_live;
+            ks = (ks + num_live) & (kStagesK - 1);
+            vs = vsi;
+            vp = vpi;
+            sa = buf_a;
             ++qi;
         }
     } else if (warp < kNumSoftmaxWarps) {
@@ -446,6 +532,13 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         uint32_t g = x;     // sequence index 2*t + x of this warpgroup's next tile
         uint32_t par_bits = 0;  // bit s = phase parity of the next use of S buffer s (both tiles' uses counted)
         uint32_t xpar = 0;  // exchange double buffer
+#if RF_FA_TRACE
+        int trace_n = 0;
+#endif
+        // exp-phase turns: this pair's n-th phase follows the other tile's (n-1)-th (tile A) / n-th (tile B)
+        const uint32_t turn_mine = bars_r + 8u * (kBarTurn + x * 4 + (warp & 3));
+        const uint32_t turn_other = bars_r + 8u * (kBarTurn + (x ^ 1) * 4 + (warp & 3));
+        uint32_t tn = static_cast<uint32_t>(x) + 1u;  // parity of the next turn wait is tn & 1
 
         while (next_item<kHasBias>(p, sched, item)) {
             const int b = item.b, h = item.h;
@@ -479,15 +572,30 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     }
                     const int kv0 = n * kBlockN;
                     const uint32_t t_s = t_sbase + sb * kBlockN;
+                    // The UMMA warp issues PV_A(i) right after P_A(i) and QK_A(i+2) right after P_B(i)
+                    // without looking at the TMA barriers itself: this warp checks that V(i) / K(i+2)
+                    // have landed (both were requested tiles ago) while it would otherwise idle waiting
+                    // for S, long before it publishes P.
+                    if (RF_FA_VK_IN_SOFTMAX) {
+                        const uint32_t tv = vc + static_cast<uint32_t>(it);
+                        if (x == 0) mbar_wait(bars_r + 8u * (kBarVFull + tv % kStagesV), (tv / kStagesV) & 1u);
+                        if ((x == 1 || !item.has_b) && it + 2 < num_live)
+                            mbar_wait(bars_r + 8u * (kBarKFull + ((tv + 2u) & (kStagesK - 1))),
+                                      ((tv + 2u) / kStagesK) & 1u);
+                    }
+                    RF_STAMP(0);
                     mbar_wait(bars_r + 8u * (kBarSFull + sb), (par_bits >> sb) & 1u);
                     tc_fence_after();
+                    RF_STAMP(1);
 
+#if !RF_FA_MMAONLY
                     uint32_t su[kHalfN];
 #pragma unroll
                     for (int cb = 0; cb < kHalfN / 32; ++cb)
                         tmem_ld32(t_s + hf * kHalfN + cb * 32, reinterpret_cast<uint32_t(&)[32]>(su[cb * 32]));
                     tc_wait_ld();
-                    if (p.debug_scores != nullptr && it == 0) {
+                    RF_STAMP(2);
+                    if (!RF_FA_TRACE && p.debug_scores != nullptr && it == 0) {
                         float* dst = p.debug_scores +
                                      ((static_cast<size_t>(blockIdx.x) * 2 + x) * kBlockM + r) * kBlockN + hf * kHalfN;
 #pragma unroll
@@ -548,8 +656,10 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     // (P aliases the first 64 columns of the S buffer, which belong to half 0).
                     float* xrow = xrow_base + xpar * (4 * kBlockM);
                     xrow[hf * kBlockM] = my_max;
+                    RF_STAMP(3);
                     named_bar_sync(bar_id, kPairThreads);
                     const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
+                    RF_STAMP(4);
 
                     // lazy running max: move the reference only when it would grow by > 2^8
                     const float m_new = (tile_max > m_ref + kRescaleThreshold) ? tile_max : m_ref;
@@ -585,10 +695,16 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             tmem_st16(t_s + hf * (kHalfN / 2) + cb * 16, pk);
                         }
                     };
+                    if (kPingPong) mbar_wait(turn_mine, tn & 1u);
                     if (kEmuEvery > 0 && full)
                         exp_store(std::true_type{});
                     else
                         exp_store(std::false_type{});
+                    if (kPingPong) {
+                        mbar_arrive(turn_other);
+                        ++tn;
+                    }
+                    RF_STAMP(5);
                     float sum0, sum1;
                     unpk2(sum2, sum0, sum1);
                     l_run = l_run * alpha + (sum0 + sum1);
@@ -602,8 +718,14 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                                        (vprev / kStagesV) & 1u);
                     }
                     tc_wait_st();
+#endif  // !RF_FA_MMAONLY
+                    RF_STAMP(6);
                     tc_fence_before();
                     mbar_arrive(bars_r + 8u * (kBarPFull + sb));
+                    RF_STAMP(7);
+#if RF_FA_TRACE
+                    ++trace_n;
+#endif
                     ++it;
                     xpar ^= 1u;
                     // this tile index used buffer sb for this warpgroup and, if the other tile is
@@ -617,7 +739,14 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 }
             } else if (num_live > 0) {
                 // tile B sits this item out: account for tile A's uses of the shared S buffers
-                for (int i = 0; i < num_live; ++i) par_bits ^= 1u << ((g - 1u + 2u * i) % kSBufs);
+                for (int i = 0; i < num_live; ++i) {
+                    par_bits ^= 1u << ((g - 1u + 2u * i) % kSBufs);
+                    if (kPingPong) {  // keep the turn protocol going: pass every turn straight back
+                        mbar_wait(turn_mine, tn & 1u);
+                        mbar_arrive(turn_other);
+                        ++tn;
+                    }
+                }
             }
             // keep the sequence counters of both warpgroups in step even when tile B sat this item out
             g += 2u * static_cast<uint32_t>(num_live);

@@ -56,6 +56,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
+// Two barriers at once: both try_waits are in flight together, so the (long) latency of a
+// phase check is paid once, not twice.
+__device__ __forceinline__ void mbar_wait2(uint32_t bar_a, uint32_t parity_a, uint32_t bar_b, uint32_t parity_b) {
+    uint32_t spins = 0;
+    for (;;) {
+        const uint32_t oa = mbar_try_wait(bar_a, parity_a);
+        const uint32_t ob = mbar_try_wait(bar_b, parity_b);
+        if (oa & ob) break;
+        if (++spins > RF_MBAR_SPIN_LIMIT) __trap();
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // TMA (cp.async.bulk.tensor), 4-D tiled tensor maps
 // ------------------------------------------------------------------------------------------
