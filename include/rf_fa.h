@@ -159,17 +159,23 @@ int rf_cast_to_f32(const void* src, float* dst, int64_t n, int32_t src_dtype, vo
 
 /*
  * Host-buffer entry point with the reference's exact calling convention: f32 host tensors
- * [B,H,S,d] in, f32 host tensor out (routefast::flash_attention on Tensor objects).  Copies
- * H2D, casts to `compute_dtype` on device, runs rf_fa_fwd, copies O back.  All device memory
- * is allocated and freed inside the call (stateless like the reference).  `tile` is accepted
- * for signature parity and validated (tile < 1 -> RF_ERR_SHAPE, attention.cpp:110); the
- * kernel's tiling is fixed.  pad_bias_dims: the 4 dims of the bias tensor as the caller holds
- * it (checked against [B,1,1,S]), or NULL when pad_bias is NULL.
+ * [B,H,S,d] in, f32 host tensor out (routefast::flash_attention on Tensor objects).  The call is
+ * PCIe-bound, so it is pipelined: (batch, head-range) chunks -- independent units of the op,
+ * attention.cpp:138-142 -- go H2D -> cast to `compute_dtype` -> rf_fa_fwd -> D2H round-robin over
+ * four streams, overlapping upload, kernel and download.  Page-locked host buffers get the full
+ * overlap; pageable ones work too (O is then fetched with one copy at the end).  Device memory
+ * is allocated (stream-ordered pool) and freed inside the call and no result state is retained,
+ * like the reference; only the four streams are cached per calling thread and device
+ * (rf_fa_host_release destroys the calling thread's).  `tile` is accepted for signature parity
+ * and validated (tile < 1 -> RF_ERR_SHAPE, attention.cpp:110); the kernel's tiling is fixed.
+ * pad_bias_dims: the 4 dims of the bias tensor as the caller holds it (checked against
+ * [B,1,1,S]), or NULL when pad_bias is NULL.
  */
 int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, int64_t B, int64_t H,
                    int64_t S, int64_t d, double scale, int64_t window_left, int64_t window_right,
                    const float* pad_bias, const int64_t* pad_bias_dims, int64_t tile,
                    int32_t compute_dtype, int32_t device, rf_fa_stats* stats);
+void rf_fa_host_release(void);
 
 /* The interpreter's FusedFlashAttention case (interpreter.cpp:308-318) on host tensors:
  * n_inputs is 3 or 4 (4th = pad_bias), each with its rank and dims; attrs default to scale 0.0,

@@ -194,7 +194,13 @@ def _host_call(q, k, v, spec: AttentionSpec, tile, stats, device_index, compute_
         if pb.ndim != 4:
             raise ShapeMismatch(capi.RF_ERR_SHAPE, "pad_bias must be [B,1,1,S]")
         dims = (C.c_int64 * 4)(*pb.shape)
-    out = np.empty_like(qn)
+    # page-locked result buffer from torch's caching host allocator (reused across calls once the
+    # caller drops the previous result): lets the library download O chunk by chunk, overlapped
+    # with the uploads; the ndarray keeps the tensor alive through its base
+    if qn.size and torch.cuda.is_available():
+        out = torch.empty(qn.shape, dtype=torch.float32, pin_memory=True).numpy()
+    else:
+        out = np.empty_like(qn)  # no device: the library call below fails loudly with RF_ERR_CUDA
     st = capi.RfFaStats()
     rc = lib.rf_fa_fwd_host(qn.ctypes.data_as(f32p), kn.ctypes.data_as(f32p), vn.ctypes.data_as(f32p),
                             out.ctypes.data_as(f32p), B, H, S, d, float(spec.scale), int(spec.window_left),

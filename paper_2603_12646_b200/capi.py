@@ -18,7 +18,7 @@ RF_KERNEL_AUTO, RF_KERNEL_TCGEN05, RF_KERNEL_SIMT = 0, 1, 2
 EXPORTS = [
     "rf_last_error", "rf_abi_version", "rf_fa_params_init", "rf_fa_validate", "rf_fa_fwd_workspace_bytes",
     "rf_fa_stats_query", "rf_fa_fwd", "rf_fa_merge", "rf_fa_rescale_partial", "rf_fa_normalize",
-    "rf_pad_bias_from_mask", "rf_cast_f32_to", "rf_cast_to_f32", "rf_fa_fwd_host",
+    "rf_pad_bias_from_mask", "rf_cast_f32_to", "rf_cast_to_f32", "rf_fa_fwd_host", "rf_fa_host_release",
     "rf_fused_flash_attention_op", "rf_mask_memory_bytes", "rf_fa_memory_bytes", "rf_device_check",
     "rf_rope_qkv", "rf_add_layernorm", "rf_geglu",
 ]
@@ -109,6 +109,8 @@ def load(build_if_missing: bool = True):
     lib.rf_fa_memory_bytes.restype = u64
     lib.rf_fa_memory_bytes.argtypes = [u64] * 6
     lib.rf_device_check.argtypes = [i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
+    lib.rf_fa_host_release.argtypes = []
+    lib.rf_fa_host_release.restype = None
     for name in ("rf_fa_validate", "rf_fa_fwd_workspace_bytes", "rf_fa_stats_query", "rf_fa_fwd", "rf_fa_merge",
                  "rf_fa_rescale_partial", "rf_fa_normalize", "rf_pad_bias_from_mask", "rf_cast_f32_to",
                  "rf_cast_to_f32", "rf_fa_fwd_host", "rf_fused_flash_attention_op", "rf_device_check",

@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/rf_fa.h"
@@ -96,6 +98,18 @@ int validate(const rf_fa_params* p, Resolved* r) {
         return fail(RF_ERR_ARG, "kv range must satisfy 0 <= kv_begin <= kv_end <= S");
     return RF_OK;
 }
+
+// Streams (and the one event) of the host entry point, cached per calling thread and device:
+// creating and destroying four streams costs ~0.3 ms per call otherwise.  They carry no data
+// between calls; rf_fa_host_release() destroys the calling thread's.
+constexpr int kHostStreams = 4;
+constexpr int kMaxDevices = 64;
+struct HostCtx {
+    cudaStream_t streams[kHostStreams] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ready = nullptr;
+    int n = 0;
+};
+thread_local HostCtx g_host_ctx[kMaxDevices];
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
 bool strides_ok_tma(const int64_t s[3]) { return s[0] > 0 && s[1] > 0 && s[2] > 0 && s[0] % 8 == 0 && s[1] % 8 == 0 && s[2] % 8 == 0; }
@@ -486,22 +500,71 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
         }
     }
-    cudaStream_t stream = nullptr;
-    e = cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
 
-    float* d_f32 = nullptr;   // staging for one f32 input at a time, then reused as the f32 output
-    uint16_t* d_qkv = nullptr;
+    // The call is PCIe-bound (3 f32 tensors in, 1 out), so it is pipelined over (batch, head-range)
+    // chunks -- every (b, h) slice is an independent unit of the op (attention.cpp:138-142):
+    // chunk c runs H2D -> cast -> attention -> D2H on stream c % kStreams, so the upload of the
+    // next chunk, the kernel of this one and the download of the previous one overlap.  Small
+    // problems run as one chunk.
+    // RF_FA_HOST_TIMING=1 prints the host-side timeline of the call to stderr (developer aid)
+    static const bool host_timing = std::getenv("RF_FA_HOST_TIMING") != nullptr;
+    const auto t_begin = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (host_timing)
+            std::fprintf(stderr, "[rf_fa_fwd_host] %-10s %8.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count());
+    };
+    constexpr int kStreams = kHostStreams;
+    const size_t nb32 = static_cast<size_t>(n) * sizeof(float);
+    const size_t slice_elems = static_cast<size_t>(S) * d;          // one (b, h) slice
+    const size_t slice_in_bytes = 3 * slice_elems * sizeof(float);
+    int64_t hpc = H;                                                // heads per chunk
+    bool per_batch = false;                                         // chunks never cross a batch
+    if (static_cast<size_t>(B) * H * slice_in_bytes >= (16u << 20)) {
+        per_batch = true;
+        hpc = std::max<int64_t>(1, static_cast<int64_t>(((8u << 20) + slice_in_bytes - 1) / slice_in_bytes));
+        hpc = std::max<int64_t>(hpc, (B * H + 63) / 64);            // at most ~64 chunks
+        hpc = std::min<int64_t>(hpc, H);
+    }
+    const int64_t chunks_per_batch = per_batch ? (H + hpc - 1) / hpc : 1;
+    const int64_t n_chunks = per_batch ? B * chunks_per_batch : 1;
+    const int64_t cb = per_batch ? 1 : B;                           // batches per chunk
+    const int n_streams = static_cast<int>(std::min<int64_t>(kStreams, n_chunks));
+    const size_t chunk_elems = static_cast<size_t>(cb) * hpc * slice_elems;  // largest chunk, per tensor
+
+    // A download into pageable host memory blocks the calling thread until it has finished, which
+    // would serialise the pipeline chunk by chunk: in that case O is kept on the device and fetched
+    // with one copy at the end.  Page-locked (or registered) host memory gets per-chunk downloads.
+    bool out_pinned = false;
+    {
+        cudaPointerAttributes attr;
+        if (cudaPointerGetAttributes(&attr, out) == cudaSuccess)
+            out_pinned = attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeManaged;
+        else
+            cudaGetLastError();
+    }
+    float* d_out_full = nullptr;
+
+    if (device < 0 || device >= kMaxDevices) return fail(RF_ERR_ARG, "device index out of range");
+    HostCtx& ctx = g_host_ctx[device];
+    cudaStream_t* streams = ctx.streams;
+    float* d_f32[kStreams] = {nullptr, nullptr, nullptr, nullptr};    // f32 staging: 3 inputs, then reused for O
+    uint16_t* d_qkv[kStreams] = {nullptr, nullptr, nullptr, nullptr}; // 16-bit Q, K, V of the chunk
+    void* d_ws[kStreams] = {nullptr, nullptr, nullptr, nullptr};
     float* d_bias = nullptr;
-    void* d_ws = nullptr;
+    cudaEvent_t& bias_ready = ctx.ready;
     int rc = RF_OK;
     auto cleanup = [&]() {
-        if (d_f32) cudaFreeAsync(d_f32, stream);
-        if (d_qkv) cudaFreeAsync(d_qkv, stream);
-        if (d_bias) cudaFreeAsync(d_bias, stream);
-        if (d_ws) cudaFreeAsync(d_ws, stream);
-        cudaStreamSynchronize(stream);
-        cudaStreamDestroy(stream);
+        for (int i = 0; i < kStreams; ++i) {
+            if (streams[i] == nullptr) continue;
+            if (d_f32[i]) cudaFreeAsync(d_f32[i], streams[i]);
+            if (d_qkv[i]) cudaFreeAsync(d_qkv[i], streams[i]);
+            if (d_ws[i]) cudaFreeAsync(d_ws[i], streams[i]);
+            if (i == 0 && d_bias) cudaFreeAsync(d_bias, streams[0]);
+            if (i == 0 && d_out_full) cudaFreeAsync(d_out_full, streams[0]);
+        }
+        for (int i = 0; i < kStreams; ++i)
+            if (streams[i] != nullptr) cudaStreamSynchronize(streams[i]);
     };
 #define RF_TRY_CUDA(call, what)            \
     do {                                   \
@@ -512,47 +575,115 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
             return rc;                     \
         }                                  \
     } while (0)
+#define RF_TRY_RC(call)       \
+    do {                      \
+        rc = (call);          \
+        if (rc != RF_OK) {    \
+            cleanup();        \
+            return rc;        \
+        }                     \
+    } while (0)
 
-    const size_t nb32 = static_cast<size_t>(n) * sizeof(float);
-    RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_f32), 3 * nb32, stream), "cudaMallocAsync");
-    RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_qkv), 3 * static_cast<size_t>(n) * 2, stream),
-                "cudaMallocAsync");
-    const float* host_in[3] = {q, k, v};
-    for (int t = 0; t < 3; ++t) {
-        RF_TRY_CUDA(cudaMemcpyAsync(d_f32 + static_cast<size_t>(t) * n, host_in[t], nb32, cudaMemcpyHostToDevice, stream),
-                    "H2D copy");
-    }
-    RF_TRY_CUDA(rf::launch_cast_from_f32(d_f32, d_qkv, 3 * n, compute_dtype, stream), "cast launch");
-    if (pad_bias != nullptr) {
-        RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bias), static_cast<size_t>(B) * S * sizeof(float), stream),
-                    "cudaMallocAsync");
-        RF_TRY_CUDA(cudaMemcpyAsync(d_bias, pad_bias, static_cast<size_t>(B) * S * sizeof(float),
-                                    cudaMemcpyHostToDevice, stream),
-                    "H2D copy");
-    }
-    p.q = d_qkv;
-    p.k = d_qkv + n;
-    p.v = d_qkv + 2 * n;
-    p.out = d_f32;  // inputs are already cast; reuse the first staging slab for O (f32)
-    p.pad_bias = d_bias;
+    for (int i = 0; i < n_streams; ++i)
+        if (streams[i] == nullptr)
+            RF_TRY_CUDA(cudaStreamCreateWithFlags(&streams[i], cudaStreamNonBlocking), "cudaStreamCreate");
+
+    // the params of the largest chunk size the workspace of every stream
+    p.B = cb;
+    p.H = hpc;
+    p.q = p.k = p.v = reinterpret_cast<const void*>(uintptr_t{256});  // placeholders for the size query only
+    p.out = reinterpret_cast<void*>(uintptr_t{256});
+    p.pad_bias = pad_bias != nullptr ? reinterpret_cast<const float*>(uintptr_t{256}) : nullptr;
     size_t ws = 0;
-    rc = rf_fa_fwd_workspace_bytes(&p, &ws);
-    if (rc != RF_OK) {
-        cleanup();
-        return rc;
+    RF_TRY_RC(rf_fa_fwd_workspace_bytes(&p, &ws));
+    for (int i = 0; i < n_streams; ++i) {
+        RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_f32[i]), 3 * chunk_elems * sizeof(float), streams[i]),
+                    "cudaMallocAsync");
+        RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_qkv[i]), 3 * chunk_elems * 2, streams[i]),
+                    "cudaMallocAsync");
+        if (ws > 0) RF_TRY_CUDA(cudaMallocAsync(&d_ws[i], ws, streams[i]), "cudaMallocAsync");
     }
-    if (ws > 0) RF_TRY_CUDA(cudaMallocAsync(&d_ws, ws, stream), "cudaMallocAsync");
-    if (stats) rf_fa_stats_query(&p, stats);
-    rc = rf_fa_fwd(&p, d_ws, ws, stream);
-    if (rc != RF_OK) {
-        cleanup();
-        return rc;
+    if (!out_pinned && n_chunks > 1)
+        RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_out_full), nb32, streams[0]), "cudaMallocAsync");
+    if ((pad_bias != nullptr || d_out_full != nullptr) && bias_ready == nullptr)
+        RF_TRY_CUDA(cudaEventCreateWithFlags(&bias_ready, cudaEventDisableTiming), "cudaEventCreate");
+    if (pad_bias != nullptr) {
+        const size_t nb = static_cast<size_t>(B) * S * sizeof(float);
+        RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bias), nb, streams[0]), "cudaMallocAsync");
+        RF_TRY_CUDA(cudaMemcpyAsync(d_bias, pad_bias, nb, cudaMemcpyHostToDevice, streams[0]), "H2D copy");
     }
-    RF_TRY_CUDA(cudaMemcpyAsync(out, d_f32, nb32, cudaMemcpyDeviceToHost, stream), "D2H copy");
-    RF_TRY_CUDA(cudaStreamSynchronize(stream), "stream sync");
+    if (pad_bias != nullptr || d_out_full != nullptr) {  // stream 0 allocated the shared buffers (and uploads the bias)
+        RF_TRY_CUDA(cudaEventRecord(bias_ready, streams[0]), "cudaEventRecord");
+        for (int i = 1; i < n_streams; ++i) RF_TRY_CUDA(cudaStreamWaitEvent(streams[i], bias_ready, 0), "cudaStreamWaitEvent");
+    }
+    if (stats) {
+        rf_fa_params full = p;
+        full.B = B;
+        full.H = H;
+        rf_fa_stats_query(&full, stats);
+        stats->workspace_bytes = static_cast<uint64_t>(ws) * n_streams;
+    }
+
+    lap("setup");
+    const float* host_in[3] = {q, k, v};
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        const int si = static_cast<int>(c % n_streams);
+        cudaStream_t st = streams[si];
+        const int64_t b0 = per_batch ? c / chunks_per_batch : 0;
+        const int64_t h0 = per_batch ? (c % chunks_per_batch) * hpc : 0;
+        const int64_t nh = per_batch ? std::min<int64_t>(hpc, H - h0) : H;
+        const size_t off = (static_cast<size_t>(b0) * H + h0) * slice_elems;      // first element of the chunk
+        const size_t ne = static_cast<size_t>(cb) * nh * slice_elems;            // elements per tensor
+        for (int t = 0; t < 3; ++t)
+            RF_TRY_CUDA(cudaMemcpyAsync(d_f32[si] + static_cast<size_t>(t) * ne, host_in[t] + off, ne * sizeof(float),
+                                        cudaMemcpyHostToDevice, st),
+                        "H2D copy");
+        RF_TRY_CUDA(rf::launch_cast_from_f32(d_f32[si], d_qkv[si], static_cast<long long>(3 * ne), compute_dtype, st),
+                    "cast launch");
+        p.B = cb;
+        p.H = nh;
+        p.q = d_qkv[si];
+        p.k = d_qkv[si] + ne;
+        p.v = d_qkv[si] + 2 * ne;
+        // inputs are already cast: the first staging slab is reused for O (f32)
+        p.out = d_out_full != nullptr ? d_out_full + off : d_f32[si];
+        p.pad_bias = d_bias != nullptr ? d_bias + static_cast<size_t>(b0) * S : nullptr;
+        RF_TRY_RC(rf_fa_fwd(&p, d_ws[si], ws, st));
+        if (d_out_full == nullptr)
+            RF_TRY_CUDA(cudaMemcpyAsync(out + off, d_f32[si], ne * sizeof(float), cudaMemcpyDeviceToHost, st), "D2H copy");
+    }
+    lap("enqueued");
+    for (int i = 0; i < n_streams; ++i) RF_TRY_CUDA(cudaStreamSynchronize(streams[i]), "stream sync");
+    lap("synced");
+    if (d_out_full != nullptr) RF_TRY_CUDA(cudaMemcpy(out, d_out_full, nb32, cudaMemcpyDeviceToHost), "D2H copy");
 #undef RF_TRY_CUDA
+#undef RF_TRY_RC
     cleanup();
+    lap("cleanup");
     return RF_OK;
+}
+
+void rf_fa_host_release(void) {
+    for (int dev = 0; dev < kMaxDevices; ++dev) {
+        HostCtx& ctx = g_host_ctx[dev];
+        bool any = ctx.ready != nullptr;
+        for (int i = 0; i < kHostStreams; ++i) any = any || ctx.streams[i] != nullptr;
+        if (!any) continue;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(dev);
+        for (int i = 0; i < kHostStreams; ++i)
+            if (ctx.streams[i] != nullptr) {
+                cudaStreamSynchronize(ctx.streams[i]);
+                cudaStreamDestroy(ctx.streams[i]);
+                ctx.streams[i] = nullptr;
+            }
+        if (ctx.ready != nullptr) {
+            cudaEventDestroy(ctx.ready);
+            ctx.ready = nullptr;
+        }
+        cudaSetDevice(cur);
+    }
 }
 
 int rf_fused_flash_attention_op(const float* const* inputs, const int64_t* const* input_dims,
