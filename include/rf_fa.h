@@ -48,7 +48,12 @@ typedef enum rf_status {
     RF_ERR_ARG = 3,         /* null pointer, bad enum, bad stride/alignment */
     RF_ERR_CUDA = 4,        /* CUDA runtime/driver failure, or no sm_100 device */
     RF_ERR_WORKSPACE = 5,   /* workspace missing or too small */
-    RF_ERR_UNSUPPORTED = 6  /* valid in the reference but not implemented on this path */
+    RF_ERR_UNSUPPORTED = 6, /* valid in the reference but not implemented on this path */
+    /* graph layer (rf_graph.h) */
+    RF_ERR_SCHEMA = 7,         /* reference: SchemaError (graph.hpp:17-20) */
+    RF_ERR_VALIDATION = 8,     /* reference: ValidationError (graph.hpp:23-26) */
+    RF_ERR_NO_MASK_INPUT = 9,  /* reference: NoAttentionMaskInput (rewrite.hpp:19-22) */
+    RF_ERR_UNSUPPORTED_OP = 10 /* reference: UnsupportedOp (interpreter.hpp:14-17) */
 } rf_status;
 
 typedef enum rf_dtype { RF_DTYPE_BF16 = 0, RF_DTYPE_F16 = 1, RF_DTYPE_F32 = 2 } rf_dtype;

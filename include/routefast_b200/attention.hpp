@@ -33,9 +33,13 @@ public:
     using std::runtime_error::runtime_error;
 };
 
-// Dense row-major f32 tensor on the host (tensor.hpp:24-40).
+enum class DType { f32, f16 };  // graph.hpp:28
+
+// Dense row-major tensor on the host (tensor.hpp:24-40); f16 is stored as f32 values that went
+// through a binary16 round trip.
 struct Tensor {
     std::vector<int64_t> shape;
+    DType dtype = DType::f32;
     std::vector<float> data;
 
     Tensor() = default;

@@ -50,7 +50,10 @@ def build(force: bool = False) -> None:
     ref_possible = os.path.isdir("/root/reference/proj/core/src")
     need_ref = ref_possible and (force or not os.path.exists(REF_SO) or (
         os.path.getmtime(REF_SO) < os.path.getmtime(os.path.join(HERE, "ref_shim.cpp"))))
-    targets = (["oracle"] if need else []) + (["ref"] if need_ref else [])
+    graph_so = os.path.join(HERE, "_ref", "libref_graph.so")
+    need_refgraph = ref_possible and (force or not os.path.exists(graph_so) or (
+        os.path.getmtime(graph_so) < os.path.getmtime(os.path.join(HERE, "ref_graph_shim.cpp"))))
+    targets = (["oracle"] if need else []) + (["ref"] if need_ref else []) + (["refgraph"] if need_refgraph else [])
     if targets:
         subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 

@@ -21,6 +21,11 @@ EXPORTS = [
     "rf_pad_bias_from_mask", "rf_cast_f32_to", "rf_cast_to_f32", "rf_fa_fwd_host", "rf_fa_host_release",
     "rf_fused_flash_attention_op", "rf_mask_memory_bytes", "rf_fa_memory_bytes", "rf_device_check",
     "rf_rope_qkv", "rf_add_layernorm", "rf_geglu",
+    # include/rf_graph.h
+    "rf_graph_free", "rf_graph_normalize", "rf_graph_infer_shapes", "rf_graph_topological_order",
+    "rf_graph_find_patterns", "rf_graph_rewrite", "rf_graph_dce", "rf_graph_interpret", "rf_graph_result_count",
+    "rf_graph_result_name", "rf_graph_result_rank", "rf_graph_result_dims", "rf_graph_result_data",
+    "rf_graph_result_is_f16", "rf_graph_result_stats", "rf_graph_result_free",
 ]
 
 

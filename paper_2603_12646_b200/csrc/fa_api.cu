@@ -253,6 +253,10 @@ void fill_fa_params(const rf_fa_params* p, const Resolved& r, rf::FaParams* f) {
 
 }  // namespace
 
+namespace rf {
+int set_last_error(int code, const std::string& message) { return fail(code, message); }
+}  // namespace rf
+
 extern "C" {
 
 const char* rf_last_error(void) { return g_last_error.c_str(); }

@@ -5,7 +5,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+
 namespace rf {
+
+// sets the calling thread's rf_last_error() text and returns `code` (shared by fa_api.cu and the graph C ABI)
+int set_last_error(int code, const std::string& message);
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kMaskThreshold = -30000.0f;  // reference attention.hpp:16

@@ -1,5 +1,5 @@
 """CPU tests of the drop-in boundary: the C-ABI library loads, exports every symbol
-include/rf_fa.h declares, validates like the reference, and fails loudly without a GPU."""
+include/rf_fa.h and include/rf_graph.h declare, validates like the reference, and fails loudly without a GPU."""
 import ctypes as C
 import os
 import re
@@ -17,9 +17,12 @@ def lib():
 
 
 def header_functions():
-    text = open(os.path.join(ROOT, "include", "rf_fa.h")).read()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(rf_[a-z0-9_]+)\s*\(", text)))
+    names = set()
+    for header in ("rf_fa.h", "rf_graph.h"):
+        text = open(os.path.join(ROOT, "include", header)).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        names |= set(re.findall(r"\b(rf_[a-z0-9_]+)\s*\(", text))
+    return sorted(names)
 
 
 def test_library_exports_every_declared_symbol(lib):
