@@ -16,6 +16,10 @@
 #include "../../include/rf_fa.h"
 #include "fa_internal.h"
 
+#ifndef RF_FA_DEFAULT_V2
+#define RF_FA_DEFAULT_V2 0
+#endif
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -166,6 +170,7 @@ int sm_count_or_default() {
 
 struct Plan {
     int kernel;
+    bool local;       // tcgen05 only: the narrow-window kernel takes the call
     int sched_mode;   // tcgen05 only
     int grid;         // CTAs
     int64_t total_pairs, pairs_per_head, tiles_per_pair;
@@ -183,6 +188,20 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
     }
     pl.pairs_per_head = (p->S + rf::kRowsPerCta - 1) / rf::kRowsPerCta;
     pl.total_pairs = pl.pairs_per_head * p->H * p->B;
+    // narrow sliding window (the reference's local layers): one 256-key strip per query tile, no
+    // workspace.  RF_FA_LOCAL=0 routes these calls to the general kernel (A/B measurements).
+    static const bool local_enabled = [] {
+        const char* env = std::getenv("RF_FA_LOCAL");
+        return env == nullptr || env[0] != '0';
+    }();
+    if (local_enabled && !r.partial && r.kv_begin == 0 && r.kv_end == p->S && p->window_left >= 0 &&
+        p->window_right >= 0 && p->window_left + p->window_right < rf::kBlockN &&
+        rf::fa_fwd_sm100_local_covers(static_cast<int>(p->window_left), static_cast<int>(p->window_right))) {
+        pl.local = true;
+        const int64_t tiles = static_cast<int64_t>(p->B) * p->H * ((p->S + rf::kBlockM - 1) / rf::kBlockM);
+        pl.grid = static_cast<int>(std::min<int64_t>(tiles, sm_count_or_default()));
+        return pl;
+    }
     pl.grid = static_cast<int>(pl.total_pairs);
     if (p->pad_bias != nullptr) {
         const size_t nt = static_cast<size_t>(n_kv_tiles(p->S));
@@ -350,6 +369,16 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
 
     // ---- tcgen05 path ----
     const Plan pl = make_plan(p, r, kernel);
+    if (pl.local) {
+        CUtensorMap tmq, tmk, tmv;
+        if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
+        if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
+        if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
+        cudaError_t e = rf::launch_fa_fwd_sm100_local(tmq, tmk, tmv, f, p->pad_bias, p->dtype == RF_DTYPE_BF16, pl.grid,
+                                                      stream);
+        if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100_local launch");
+        return RF_OK;
+    }
     const size_t need = pl.workspace_bytes();
     if (need > 0) {
         if (workspace == nullptr || workspace_bytes < need)
@@ -380,7 +409,13 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
-    cudaError_t e = rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream);
+    // RF_FA_V2=0|1 selects the pipeline variant at run time (kernel tuning; both are full implementations)
+    static const bool use_v2 = [] {
+        const char* env = std::getenv("RF_FA_V2");
+        return env != nullptr ? env[0] == '1' : RF_FA_DEFAULT_V2 != 0;
+    }();
+    cudaError_t e = use_v2 ? rf::launch_fa_fwd_sm100_v2(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream)
+                           : rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100 launch");
     return RF_OK;
 }

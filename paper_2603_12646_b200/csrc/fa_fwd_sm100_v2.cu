@@ -1,0 +1,809 @@
+// fa_fwd_sm100_v2.cu -- FusedFlashAttention forward for sm_100a (B200), head_dim 64: the
+// decoupled-pipeline variant of fa_fwd_sm100.cu (same semantics, same work distribution, same
+// softmax arithmetic and epilogue; see that file for the operator contract).
+//
+// What changes is the synchronisation structure.  In fa_fwd_sm100.cu three S accumulators rotate
+// between the two query tiles and P aliases S, so S_A(i+2) can only be issued after P_B(i) was
+// consumed: the softmax warps wait for S and the UMMA warp waits for P, ~450 clk each per key tile
+// (profiles/r01_trace_phases_8k.json).  Here every query tile owns a private S accumulator that is
+// handed back to the tensor pipe as soon as its softmax warps hold it in registers, and P lives in
+// its own TMEM columns:
+//     S_A [0,128)  S_B [128,256)  P_A [256,320)  P_B [320,384)  O_A [384,448)  O_B [448,512)
+// so Q K^T of key tile i+1 runs underneath the exponentials of tile i, and the two query tiles have
+// no barrier in common.  Each tile has its own UMMA-issuing warp (17: tile A, 18: tile B):
+//     issuer X, tile i:  wait {S_X free(i), K(i+1)} -> QK_X(i+1) ; wait {P_X full(i), V(i)} -> PV_X(i)
+//     softmax X, tile i: wait S_X full -> tcgen05.ld -> S_X free -> max/exchange/exp -> (P_X free) ->
+//                        tcgen05.st P -> P_X full
+// K/V/Q ring slots are released by BOTH issuers (arrival count 2).  When the pair has only tile A
+// (ragged last pair), issuer B still passes every ring slot on (plain arrives behind the full
+// barriers) so that all phases advance uniformly.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "fa_internal.h"
+#include "ptx.cuh"
+
+namespace rf {
+namespace {
+
+using namespace rfptx;
+
+constexpr int kHeadDim = 64;
+constexpr int kStagesK = 4;                         // K ring depth (K runs two tiles ahead of V)
+constexpr int kStagesV = 3;                         // V ring depth
+constexpr int kTileBytes = kBlockN * kHeadDim * 2;  // 16 KiB: one 128 x 64 16-bit tile
+constexpr int kNumSoftmaxWarps = 16;
+constexpr int kProducerWarp = 16;
+constexpr int kMmaWarp = 17;         // issuer of tile A; tile B: kMmaWarp + 1
+constexpr int kThreads = 640;        // 5 warpgroups: 4 softmax + 1 (producer, MMA, 2 idle warps)
+constexpr int kHalfN = kBlockN / 2;  // key columns per softmax thread
+constexpr int kRegsSoftmax = 112;
+#ifndef RF_FA_EMU_EVERY
+#define RF_FA_EMU_EVERY 8
+#endif
+constexpr int kEmuEvery = RF_FA_EMU_EVERY;  // every n-th element pair uses the FMA-pipe exp2 (0 = MUFU only)
+constexpr int kRegsOther = 32;       // 128*32 + 512*112 == 640*96: the CTA register pool balances exactly
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColS = 0;    // + 128 * X
+constexpr uint32_t kColP = 256;  // + 64 * X
+constexpr uint32_t kColO = 384;  // + 64 * X
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: P <= 2^8 before a rescale is forced
+// The two query tiles have no barrier in common, and left alone their softmax warps drift into
+// phase: all four warps of an SM sub-partition then queue on the MUFU pipe together and idle it
+// together (exp phase 2100 clk instead of 1300, profiles/).  With RF_FA_V2_TURNS the two warps of
+// tile A and the two of tile B of each sub-partition take strict turns on the exponential phase.
+#ifndef RF_FA_V2_TURNS
+#define RF_FA_V2_TURNS 1
+#endif
+constexpr bool kTurns = RF_FA_V2_TURNS != 0;
+// Developer build only (-DRF_FA_TRACE=1): softmax warps of CTA 0 stamp the SM clock at their phase
+// boundaries into the debug_scores buffer, [16 warps][64 tiles][8 stamps] u32 (tools/trace_phases.py).
+#ifndef RF_FA_TRACE
+#define RF_FA_TRACE 0
+#endif
+// Developer build only (-DRF_FA_MMAONLY=1): the softmax warps skip their work (results are garbage);
+// what remains is the TMA + UMMA pipeline, i.e. the tensor-pipe floor of this tiling.
+#ifndef RF_FA_MMAONLY
+#define RF_FA_MMAONLY 0
+#endif
+#if RF_FA_TRACE
+#define RF_STAMP(slot)                                                                               \
+    do {                                                                                             \
+        if (blockIdx.x == 0 && lane == 0 && trace_n < 64 && p.debug_scores != nullptr)               \
+            reinterpret_cast<uint32_t*>(p.debug_scores)[(warp * 64 + trace_n) * 8 + (slot)] = clock(); \
+    } while (0)
+#else
+#define RF_STAMP(slot) do { } while (0)
+#endif
+
+// dynamic shared memory map (offsets from a 1024B-aligned base)
+struct Smem {
+    static constexpr uint32_t q = 0;                                   // 2 tiles
+    static constexpr uint32_t k = q + 2 * kTileBytes;                  // kStagesK tiles
+    static constexpr uint32_t v = k + kStagesK * kTileBytes;           // kStagesV tiles
+    static constexpr uint32_t bars = v + kStagesV * kTileBytes;        // barrier block
+    static constexpr uint32_t bar_bytes = 512;
+    static constexpr uint32_t xchg = bars + bar_bytes;                 // row-max exchange: [2 parity][2 tile][2 half][128] f32
+    static constexpr uint32_t xchg_bytes = 2 * 2 * 2 * kBlockM * 4;
+};
+// barrier indices inside the barrier block (8 bytes each)
+enum : uint32_t {
+    kBarQFull = 0,
+    kBarQEmpty = 1,                      // count 2: both issuers
+    kBarKFull = 2,                       // [kStagesK]
+    kBarKEmpty = kBarKFull + kStagesK,   // [kStagesK] count 2
+    kBarVFull = kBarKEmpty + kStagesK,   // [kStagesV]
+    kBarVEmpty = kBarVFull + kStagesV,   // [kStagesV] count 2
+    kBarSFull = kBarVEmpty + kStagesV,   // [2] S_X holds Q_X K^T of the next tile
+    kBarSFree = kBarSFull + 2,           // [2] count 8: S_X is in the registers of all 8 softmax warps of tile X
+    kBarPFull = kBarSFree + 2,           // [2] count 256
+    kBarPFree = kBarPFull + 2,           // [2] PV_X has consumed P_X (and updated O_X)
+    kBarOFull = kBarPFree + 2,           // [2]
+    kBarTurn = kBarOFull + 2,            // [2 tiles][4 quadrants] exp-phase turn of (tile, SM sub-partition), count 64
+    kNumBars = kBarTurn + 8,
+};
+static_assert(kNumBars * 8 + 8 <= Smem::bar_bytes, "barrier block too small");
+
+enum : int { kItemFull = 0, kItemHeadPart = 1, kItemTailPart = 2 };
+
+// One unit of work of a CTA: a query-tile pair and a range of key tiles.
+struct Item {
+    int b, h, q0;
+    int n0, n1;    // key tiles [n0, n1)
+    int num_live;  // tiles in the range that are not fully padded
+    int kind;
+    bool has_b;
+};
+
+struct Sched {
+    long long t, t_end;  // mode 1: flat (pair, key tile) cursor
+    bool done;           // mode 0
+};
+
+template <bool kHasBias>
+__device__ __forceinline__ bool tile_live(const FaParams& p, int b, int n) {
+    return !kHasBias || p.tile_flags[b * p.n_kv_tiles + n] != kTileSkip;
+}
+
+__device__ __forceinline__ void sched_init(const FaParams& p, Sched& s) {
+    s.done = false;
+    if (p.sched_mode == 1) {
+        const long long total = static_cast<long long>(p.total_pairs) * p.tiles_per_pair;
+        s.t = total * blockIdx.x / gridDim.x;
+        s.t_end = total * (blockIdx.x + 1) / gridDim.x;
+    } else {
+        s.t = s.t_end = 0;
+    }
+}
+
+template <bool kHasBias>
+__device__ __forceinline__ bool next_item(const FaParams& p, Sched& s, Item& it) {
+    int pair_lin, k0 = 0, k1 = 0x7fffffff;
+    if (p.sched_mode == 1) {
+        if (s.t >= s.t_end) return false;
+        const int K = p.tiles_per_pair;  // virtual key tiles per pair (upper bound of any pair's range)
+        pair_lin = static_cast<int>(s.t / K);
+        k0 = static_cast<int>(s.t - static_cast<long long>(pair_lin) * K);
+        k1 = static_cast<int>(min(static_cast<long long>(K), k0 + (s.t_end - s.t)));
+        s.t += k1 - k0;
+        it.kind = k0 > 0 ? kItemHeadPart : (k1 < K ? kItemTailPart : kItemFull);
+    } else {
+        if (s.done) return false;
+        s.done = true;
+        pair_lin = blockIdx.x;
+        it.kind = kItemFull;
+    }
+    const int px = pair_lin % p.pairs_per_head;
+    const int bh = pair_lin / p.pairs_per_head;
+    it.h = bh % p.H;
+    it.b = bh / p.H;
+    it.q0 = px * kRowsPerCta;
+    it.has_b = it.q0 + kBlockM < p.S;
+    // key-tile range of this pair (union over its rows of window and split range) ...
+    const int rows_end = min(it.q0 + kRowsPerCta, p.S);
+    int j_lo = p.kv_begin, j_hi = p.kv_end;
+    if (p.wl >= 0) j_lo = max(j_lo, it.q0 - p.wl);
+    if (p.wr >= 0) j_hi = min(j_hi, rows_end + p.wr);
+    const int pn0 = j_lo >> 7;
+    const int pn1 = (j_hi > j_lo) ? ((j_hi + kBlockN - 1) >> 7) : pn0;
+    // ... cut to this item's slice of it (mode 1: virtual tile v is real tile pn0 + v; slices past
+    // the pair's last tile are empty)
+    it.n0 = min(pn0 + k0, pn1);
+    it.n1 = (k1 >= pn1 - pn0) ? pn1 : pn0 + k1;
+    it.num_live = 0;
+    for (int n = it.n0; n < it.n1; ++n) it.num_live += tile_live<kHasBias>(p, it.b, n) ? 1 : 0;
+    return true;
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
+
+// O rows (32 columns of this thread's lane) *= alpha.  The caller has already seen the P-free
+// barrier of the previous tile, i.e. PV of that tile has finished updating O.
+__device__ __noinline__ void rescale_o_rows(uint32_t t_o, float alpha) {
+    tc_fence_after();
+    uint32_t o[32];
+    tmem_ld32(t_o, o);
+    tc_wait_ld();
+#pragma unroll
+    for (int u = 0; u < 32; u += 2) {
+        float a0 = __uint_as_float(o[u]), a1 = __uint_as_float(o[u + 1]);
+        fmul2(a0, a1, alpha);
+        o[u] = __float_as_uint(a0);
+        o[u + 1] = __float_as_uint(a1);
+    }
+    tmem_st32(t_o, o);
+    tc_wait_st();
+}
+
+template <bool kBf16, bool kHasBias>
+__global__ void __launch_bounds__(kThreads, 1)
+fa_fwd_sm100_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const FaParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
+    asm volatile("mov.u32 %0, %0;" : "+r"(smem_base));  // keep in a register: do not rematerialise
+    const uint32_t bars = smem_base + Smem::bars;
+    auto bar = [&](uint32_t i) { return bars + 8u * i; };
+    volatile uint32_t* tmem_slot =
+        reinterpret_cast<volatile uint32_t*>(smem_gen + Smem::bars + 8 * kNumBars);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    // ---------------- prologue ----------------
+    if (warp == kProducerWarp && lane == 0) {
+        prefetch_tensormap(&tm_q);
+        prefetch_tensormap(&tm_k);
+        prefetch_tensormap(&tm_v);
+        mbar_init(bar(kBarQFull), 1);
+        mbar_init(bar(kBarQEmpty), 2);
+        for (int s = 0; s < kStagesK; ++s) {
+            mbar_init(bar(kBarKFull + s), 1);
+            mbar_init(bar(kBarKEmpty + s), 2);
+        }
+        for (int s = 0; s < kStagesV; ++s) {
+            mbar_init(bar(kBarVFull + s), 1);
+            mbar_init(bar(kBarVEmpty + s), 2);
+        }
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(bar(kBarSFull + x), 1);
+            mbar_init(bar(kBarSFree + x), 8);
+            mbar_init(bar(kBarPFull + x), 2 * kBlockM);
+            mbar_init(bar(kBarPFree + x), 1);
+            mbar_init(bar(kBarOFull + x), 1);
+        }
+        for (int i = 0; i < 8; ++i) mbar_init(bar(kBarTurn + i), 64);  // both warps of the other tile arrive
+        fence_barrier_init();
+    }
+    if (warp == kMmaWarp) {
+        tmem_alloc(smem_u32(const_cast<uint32_t*>(tmem_slot)), kTmemCols);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    Sched sched;
+    sched_init(p, sched);
+    Item item;
+
+    static_assert(128 * kRegsOther + 512 * kRegsSoftmax <= kThreads * 96, "setmaxnreg pool must balance");
+    if (warp >= kNumSoftmaxWarps) setmaxnreg_dec<kRegsOther>();
+
+    if (warp == kProducerWarp) {
+        // =============================== TMA producer ===============================
+        // warp-uniform control flow; only the TMA / expect_tx instructions are predicated
+        const bool leader = elect_one() != 0;
+        uint32_t qi = 0;  // items with work so far (Q barrier phase)
+        uint32_t kc = 0;  // K tiles loaded so far (ring position)
+        uint32_t vc = 0;  // V tiles loaded so far
+        while (next_item<kHasBias>(p, sched, item)) {
+            if (item.num_live == 0) continue;
+            const int b = item.b, h = item.h;
+            mbar_wait(bar(kBarQEmpty), (qi & 1) ^ 1);
+            if (leader) {
+                mbar_arrive_expect_tx(bar(kBarQFull), item.has_b ? 2 * kTileBytes : kTileBytes);
+                tma_load_4d(smem_base + Smem::q, &tm_q, bar(kBarQFull), 0, item.q0, h, b);
+                if (item.has_b)
+                    tma_load_4d(smem_base + Smem::q + kTileBytes, &tm_q, bar(kBarQFull), 0, item.q0 + kBlockM, h, b);
+            }
+            __syncwarp();
+            ++qi;
+            // K runs two tiles ahead of V: QK^T of tile t+2 is issued while tile t is in softmax
+            auto load_k = [&](int n) {
+                const uint32_t st = kc % kStagesK;
+                mbar_wait(bar(kBarKEmpty + st), ((kc / kStagesK) & 1) ^ 1);
+                if (leader) {
+                    mbar_arrive_expect_tx(bar(kBarKFull + st), kTileBytes);
+                    tma_load_4d(smem_base + Smem::k + st * kTileBytes, &tm_k, bar(kBarKFull + st), 0, n * kBlockN, h, b);
+                }
+                __syncwarp();
+                ++kc;
+            };
+            auto load_v = [&](int n) {
+                const uint32_t st = vc % kStagesV;
+                mbar_wait(bar(kBarVEmpty + st), ((vc / kStagesV) & 1) ^ 1);
+                if (leader) {
+                    mbar_arrive_expect_tx(bar(kBarVFull + st), kTileBytes);
+                    tma_load_4d(smem_base + Smem::v + st * kTileBytes, &tm_v, bar(kBarVFull + st), 0, n * kBlockN, h, b);
+                }
+                __syncwarp();
+                ++vc;
+            };
+            auto next_live = [&](int n) {
+                while (n < item.n1 && !tile_live<kHasBias>(p, b, n)) ++n;
+                return n;
+            };
+            int nk = next_live(item.n0);
+            for (int pre = 0; pre < 2 && nk < item.n1; ++pre) {
+                load_k(nk);
+                nk = next_live(nk + 1);
+            }
+            for (int n = next_live(item.n0); n < item.n1; n = next_live(n + 1)) {
+                if (nk < item.n1) {
+                    load_k(nk);
+                    nk = next_live(nk + 1);
+                }
+                load_v(n);
+            }
+        }
+    } else if (warp == kMmaWarp || warp == kMmaWarp + 1) {
+        // =============================== UMMA issuers (one per query tile) ===============================
+        // Warp-uniform control flow; only the tcgen05 instructions are predicated on one elected lane
+        // (a divergent `if (lane == 0)` makes ptxas wrap every UTCHMMA in an ELECT / R2UR loop).
+        const uint32_t x = static_cast<uint32_t>(warp - kMmaWarp);  // 0 = tile A, 1 = tile B
+        const bool leader = elect_one() != 0;
+        constexpr uint32_t fmt = kBf16 ? 1u : 0u;
+        constexpr uint32_t idesc_qk = make_idesc_f16(fmt, 0, 0, kBlockM, kBlockN);
+        constexpr uint32_t idesc_pv = make_idesc_f16(fmt, 0, 1, kBlockM, kHeadDim);
+        // descriptor high words are constants; the low word is (address >> 4) | LBO field
+        constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (kSwizzle128B << 29);  // SBO, version, swizzle
+        constexpr uint32_t kLboK = (16u >> 4) << 16;                                    // K-major operands
+        constexpr uint32_t kLboV = (static_cast<uint32_t>(kTileBytes) >> 4) << 16;      // MN-major V
+        constexpr uint32_t kTile16 = kTileBytes / 16;
+        const uint32_t sb16 = smem_base >> 4;
+        auto desc = [&](uint32_t lo) { return (static_cast<uint64_t>(kDescHi) << 32) | lo; };
+        auto commit = [&](uint32_t b_) {
+            if (leader) tc_commit(b_);
+            __syncwarp();
+        };
+        auto arrive = [&](uint32_t b_) {  // ring slot passed on without having been read (tile B absent)
+            if (leader) mbar_arrive(b_);
+            __syncwarp();
+        };
+        const uint32_t q_lo = (kLboK | (sb16 + Smem::q / 16)) + x * kTile16;
+        const uint32_t k_lo = kLboK | (sb16 + Smem::k / 16);
+        const uint32_t v_lo = kLboV | (sb16 + Smem::v / 16);
+        const uint32_t t_s = tmem_base + kColS + x * kBlockN;
+        const uint32_t t_p = tmem_base + kColP + x * kHeadDim;
+        const uint32_t t_o = tmem_base + kColO + x * kHeadDim;
+        const uint32_t b_sfull = bar(kBarSFull + x), b_sfree = bar(kBarSFree + x);
+        const uint32_t b_pfull = bar(kBarPFull + x), b_pfree = bar(kBarPFree + x);
+
+        uint32_t qi = 0;  // items with work so far (Q barrier phase)
+        uint32_t kc = 0;  // key tiles of earlier items: K ring position kc & 3, phase (kc >> 2) & 1
+        uint32_t vs = 0, vp = 0;  // V ring stage of the next tile and the phase parity of that use
+        uint32_t nt = 0;  // key tiles this issuer has run so far: phase parity of its S / P barriers
+
+        while (next_item<kHasBias>(p, sched, item)) {
+            const int num_live = item.num_live;
+            if (num_live == 0) continue;
+            mbar_wait(bar(kBarQFull), qi & 1);
+            tc_fence_after();
+            if (x == 1 && !item.has_b) {
+                // this pair has no second query tile: hand every ring slot on, in step with the loads
+                for (int i = 0; i < num_live; ++i) {
+                    mbar_wait(bar(kBarKFull + ((kc + i) & (kStagesK - 1))), ((kc + i) / kStagesK) & 1);
+                    arrive(bar(kBarKEmpty + ((kc + i) & (kStagesK - 1))));
+                    mbar_wait(bar(kBarVFull + vs), vp);
+                    arrive(bar(kBarVEmpty + vs));
+                    if (++vs == kStagesV) {
+                        vs = 0;
+                        vp ^= 1u;
+                    }
+                }
+                arrive(bar(kBarQEmpty));
+                kc += num_live;
+                ++qi;
+                continue;
+            }
+            // S_X = Q_X K^T of key tile i: both operands K-major, 128B swizzle, a K=16 step advances
+            // 32 B inside the swizzle atom.  The caller has seen "S_X free" and "K(i) full".
+            auto issue_qk = [&](int i) {
+                const uint32_t kstage = (kc + i) & (kStagesK - 1);
+                const uint32_t klo = k_lo + kstage * kTile16;
+                if (leader) {
+#pragma unroll
+                    for (int kk = 0; kk < kHeadDim / 16; ++kk)
+                        mma_ss(t_s, desc(q_lo + kk * 2), desc(klo + kk * 2), idesc_qk, kk > 0 ? 1u : 0u);
+                    tc_commit(b_sfull);
+                    tc_commit(bar(kBarKEmpty + kstage));
+                    if (i + 1 == num_live) tc_commit(bar(kBarQEmpty));  // the item's last read of Q_X
+                }
+                __syncwarp();
+            };
+            // tile 0 of the item: the previous tile's S (if any) must have been read
+            mbar_wait2(b_sfree, (nt & 1u) ^ 1u, bar(kBarKFull + (kc & (kStagesK - 1))), (kc / kStagesK) & 1);
+            tc_fence_after();
+            issue_qk(0);
+            for (int i = 0; i < num_live; ++i) {
+                const bool last = i + 1 == num_live;
+#if RF_FA_TRACE
+                const int trace_n = i;
+#endif
+                RF_STAMP(0);
+                if (!last) {
+                    // S_X(i) is in registers -> Q K^T of tile i+1 runs underneath the exponentials of tile i
+                    mbar_wait2(b_sfree, nt & 1u, bar(kBarKFull + ((kc + i + 1) & (kStagesK - 1))),
+                               ((kc + i + 1) / kStagesK) & 1);
+                    tc_fence_after();
+                    RF_STAMP(1);
+                    issue_qk(i + 1);
+                }
+                RF_STAMP(2);
+                // O_X += P_X V(i): A = P from TMEM (16 bf16 per row per K step = 8 packed columns),
+                // B = V [key][d], d contiguous = MN-major; a K=16 step advances 16 keys = 2048 B
+                uint32_t vlo = v_lo + vs * kTile16;
+                asm volatile("" : "+r"(vlo));
+                mbar_wait2(b_pfull, nt & 1u, bar(kBarVFull + vs), vp);
+                tc_fence_after();
+                RF_STAMP(3);
+                if (leader) {
+#pragma unroll
+                    for (int kk = 0; kk < kBlockN / 16; ++kk)
+                        mma_ts(t_o, t_p + kk * 8, desc(vlo + kk * 128), idesc_pv, (kk > 0 || i > 0) ? 1u : 0u);
+                    tc_commit(b_pfree);
+                    tc_commit(bar(kBarVEmpty + vs));
+                    if (last) tc_commit(bar(kBarOFull + x));
+                }
+                __syncwarp();
+                RF_STAMP(4);
+                if (++vs == kStagesV) {
+                    vs = 0;
+                    vp ^= 1u;
+                }
+                ++nt;
+            }
+            kc += num_live;
+            ++qi;
+        }
+    } else if (warp < kNumSoftmaxWarps) {
+        // =============================== softmax / epilogue ===============================
+        setmaxnreg_inc<kRegsSoftmax>();
+        const int x = warp >> 3;               // 0 = tile A, 1 = tile B
+        const int hf = (warp >> 2) & 1;        // which half of the tile's key columns this thread owns
+        const int r = (warp & 3) * 32 + lane;  // row inside the tile == TMEM lane
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint32_t t_o = tmem_base + lane_base + kColO + x * kHeadDim + hf * (kHeadDim / 2);
+        const uint32_t t_s = tmem_base + lane_base + kColS + x * kBlockN;
+        const uint32_t t_p = tmem_base + lane_base + kColP + x * kHeadDim + hf * (kHalfN / 2);
+        const int kv_end_eff = min(p.kv_end, p.S);
+        const float c = p.scale_log2;
+        float* xchg = reinterpret_cast<float*>(smem_gen + Smem::xchg);
+        float* xrow_base = xchg + (x * 2) * kBlockM + r;
+        // named barrier shared by the two warps that own the same 32 rows (ids 1..8)
+        const uint32_t bar_id = 1 + x * 4 + (warp & 3);
+        constexpr uint32_t kPairThreads = 64;
+        uint32_t bars_r = bars;
+        asm volatile("mov.u32 %0, %0;" : "+r"(bars_r));
+
+        uint32_t oi = 0;    // items this warpgroup worked on so far (O-full barrier phase)
+        uint32_t nt = 0;    // key tiles this warpgroup has processed so far: phase parity of its S / P barriers
+        uint32_t xpar = 0;  // exchange double buffer
+#if RF_FA_TRACE
+        int trace_n = 0;
+#endif
+        const uint32_t b_sfull = bars_r + 8u * (kBarSFull + x), b_sfree = bars_r + 8u * (kBarSFree + x);
+        const uint32_t b_pfull = bars_r + 8u * (kBarPFull + x), b_pfree = bars_r + 8u * (kBarPFree + x);
+        // exp-phase turns: this pair's n-th phase follows the other tile's (n-1)-th (tile A) / n-th (tile B)
+        const uint32_t turn_mine = bars_r + 8u * (kBarTurn + x * 4 + (warp & 3));
+        const uint32_t turn_other = bars_r + 8u * (kBarTurn + (x ^ 1) * 4 + (warp & 3));
+        uint32_t tn = static_cast<uint32_t>(x) + 1u;  // parity of the next turn wait is tn & 1
+
+        while (next_item<kHasBias>(p, sched, item)) {
+            const int b = item.b, h = item.h;
+            const int num_live = item.num_live;
+            const bool active = (x == 0) || item.has_b;
+            const int tile_r_lo = item.q0 + x * kBlockM;
+            const int tile_r_hi = tile_r_lo + kBlockM - 1;
+            const int row = tile_r_lo + r;
+
+            float m_ref = -CUDART_INF_F;
+            float l_run = 0.f;  // this thread's share of the row sum (its 64 columns of every tile)
+
+            if (active && num_live > 0) {
+                // key tiles [nf0, nf1) need no window / range predicate for any row of this query tile
+                int nf0, nf1;
+                {
+                    int lo_key = p.kv_begin, hi_key = kv_end_eff - kBlockN;  // bounds on the tile's first key
+                    if (p.wl >= 0) lo_key = max(lo_key, tile_r_hi - p.wl);
+                    if (p.wr >= 0) hi_key = min(hi_key, tile_r_lo + p.wr - (kBlockN - 1));
+                    nf0 = (lo_key + kBlockN - 1) >> 7;
+                    nf1 = hi_key >= 0 ? (hi_key >> 7) + 1 : 0;
+                }
+                const uint8_t* flags_row = kHasBias ? p.tile_flags + b * p.n_kv_tiles : nullptr;
+                int it = 0;
+                for (int n = item.n0; n < item.n1; ++n) {
+                    uint8_t flag = kTileFull;
+                    if (kHasBias) {
+                        flag = flags_row[n];
+                        if (flag == kTileSkip) continue;
+                    }
+                    const int kv0 = n * kBlockN;
+                    RF_STAMP(0);
+                    mbar_wait(b_sfull, nt & 1u);
+                    tc_fence_after();
+                    RF_STAMP(1);
+
+#if !RF_FA_MMAONLY
+                    uint32_t su[kHalfN];
+#pragma unroll
+                    for (int cb = 0; cb < kHalfN / 32; ++cb)
+                        tmem_ld32(t_s + hf * kHalfN + cb * 32, reinterpret_cast<uint32_t(&)[32]>(su[cb * 32]));
+                    tc_wait_ld();
+                    // S_X is in registers (tcgen05.ld / wait::ld are warp-wide): hand the accumulator back,
+                    // Q K^T of the next key tile starts now
+                    tc_fence_before();
+                    if (lane == 0) mbar_arrive(b_sfree);
+                    RF_STAMP(2);
+                    if (!RF_FA_TRACE && p.debug_scores != nullptr && it == 0) {
+                        float* dst = p.debug_scores +
+                                     ((static_cast<size_t>(blockIdx.x) * 2 + x) * kBlockM + r) * kBlockN + hf * kHalfN;
+#pragma unroll
+                        for (int j = 0; j < kHalfN; ++j) dst[j] = __uint_as_float(su[j]);
+                    }
+
+                    // tile class (warp-uniform): "full" tiles need no per-element predicate
+                    const bool full = (n >= nf0) && (n < nf1) && (flag == kTileFull);
+
+                    float my_max;
+                    float mul;
+                    if (full) {
+                        float mx[4];
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) mx[q4] = __uint_as_float(su[q4]);
+#pragma unroll
+                        for (int j = 4; j < kHalfN; j += 8) {
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4) {
+                                const int j0 = j + 2 * q4;
+                                if (j0 + 1 < kHalfN)
+                                    mx[q4] = max3(mx[q4], __uint_as_float(su[j0]), __uint_as_float(su[j0 + 1]));
+                            }
+                        }
+                        my_max = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * c;  // scale > 0 (host-checked)
+                        mul = c;
+                    } else {
+                        // live columns of this row inside the tile: [lo, hi]
+                        int lo = p.kv_begin, hi = kv_end_eff - 1;
+                        if (p.wl >= 0) lo = max(lo, row - p.wl);
+                        if (p.wr >= 0) hi = min(hi, row + p.wr);
+                        lo -= kv0 + hf * kHalfN;
+                        hi -= kv0 + hf * kHalfN;
+                        const float* brow = (kHasBias && flag == kTileMixed)
+                                                ? p.bias2 + static_cast<size_t>(b) * p.bias_stride + kv0 + hf * kHalfN
+                                                : nullptr;
+                        float mx = -CUDART_INF_F;
+#pragma unroll
+                        for (int j4 = 0; j4 < kHalfN; j4 += 4) {
+                            float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (kHasBias && brow != nullptr) bb = __ldg(reinterpret_cast<const float4*>(brow + j4));
+                            const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int j = j4 + u;
+                                const float xs = fmaf(__uint_as_float(su[j]), c, bv[u]);  // bias -inf => masked key
+                                const float xm = (j >= lo && j <= hi) ? xs : -CUDART_INF_F;
+                                su[j] = __float_as_uint(xm);
+                                mx = fmaxf(mx, xm);
+                            }
+                        }
+                        my_max = mx;
+                        mul = 1.0f;
+                    }
+
+                    // row max over both halves: exchange through smem (double-buffered by tile parity).
+                    // The barrier also orders every S read of this tile before any P write below
+                    // (P aliases the first 64 columns of the S buffer, which belong to half 0).
+                    float* xrow = xrow_base + xpar * (4 * kBlockM);
+                    xrow[hf * kBlockM] = my_max;
+                    RF_STAMP(3);
+                    named_bar_sync(bar_id, kPairThreads);
+                    const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
+                    // P_X may be overwritten once PV of the previous tile has consumed it: test now, the
+                    // answer is back before the first store needs it
+                    uint32_t p_free = mbar_try_wait(b_pfree, (nt & 1u) ^ 1u);
+                    RF_STAMP(4);
+
+                    // lazy running max: move the reference only when it would grow by > 2^8
+                    const float m_new = (tile_max > m_ref + kRescaleThreshold) ? tile_max : m_ref;
+                    const float alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
+                    const float neg_m = (m_new == -CUDART_INF_F) ? 0.f : -m_new;
+
+                    // P = 2^(s*mul - m).  On full tiles every kEmuEvery-th element pair takes the FMA-pipe
+                    // polynomial (exp2_poly2) instead of MUFU.EX2 so both pipes share the exponentials;
+                    // edge tiles keep MUFU only, because a masked score (-inf) must give exactly 0.
+                    uint64_t sum2 = 0;  // packed (0.f, 0.f)
+                    const uint64_t mul2 = bc2(mul), negm2 = bc2(neg_m);
+                    auto exp_store = [&](auto emu_tag) {
+                        constexpr bool kEmu = decltype(emu_tag)::value;
+#pragma unroll
+                        for (int cb = 0; cb < kHalfN / 32; ++cb) {
+                            uint32_t pk[16];
+#pragma unroll
+                            for (int u = 0; u < 16; ++u) {
+                                float p0, p1;
+                                unpk2(ffma2v(pk2(__uint_as_float(su[cb * 32 + 2 * u]),
+                                                 __uint_as_float(su[cb * 32 + 2 * u + 1])),
+                                             mul2, negm2),
+                                      p0, p1);
+                                if (kEmu && (u % (kEmuEvery > 0 ? kEmuEvery : 1)) == (kEmuEvery > 0 ? kEmuEvery - 1 : 0)) {
+                                    exp2_poly2(p0, p1);
+                                } else {
+                                    p0 = ex2(p0);
+                                    p1 = ex2(p1);
+                                }
+                                sum2 = fadd2v(sum2, pk2(p0, p1));
+                                pk[u] = pack2<kBf16>(p0, p1);
+                            }
+                            tmem_st16(t_p + cb * 16, pk);
+                        }
+                    };
+                    if (!p_free) mbar_wait(b_pfree, (nt & 1u) ^ 1u);
+                    tc_fence_after();
+                    if (kTurns) mbar_wait(turn_mine, tn & 1u);
+                    if (kEmuEvery > 0 && full)
+                        exp_store(std::true_type{});
+                    else
+                        exp_store(std::false_type{});
+                    if (kTurns) {
+                        mbar_arrive(turn_other);
+                        ++tn;
+                    }
+                    RF_STAMP(5);
+                    float sum0, sum1;
+                    unpk2(sum2, sum0, sum1);
+                    l_run = l_run * alpha + (sum0 + sum1);
+                    m_ref = m_new;
+
+                    // O_X *= alpha for rows whose reference max moved (rare after the first tiles thanks
+                    // to the lazy threshold): kept out of line so the hot loop stays compact.
+                    if (it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o_rows(t_o, alpha);
+                    tc_wait_st();
+#else   // tensor-pipe floor: pass the accumulators straight back
+                    tc_fence_before();
+                    if (lane == 0) mbar_arrive(b_sfree);
+                    mbar_wait(b_pfree, (nt & 1u) ^ 1u);
+#endif  // !RF_FA_MMAONLY
+                    RF_STAMP(6);
+                    tc_fence_before();
+                    mbar_arrive(b_pfull);
+                    RF_STAMP(7);
+#if RF_FA_TRACE
+                    ++trace_n;
+#endif
+                    ++it;
+                    ++nt;
+                    xpar ^= 1u;
+                }
+            } else if (kTurns) {
+                // tile B sits this item out: pass every turn straight back
+                for (int i = 0; i < num_live; ++i) {
+                    mbar_wait(turn_mine, tn & 1u);
+                    mbar_arrive(turn_other);
+                    ++tn;
+                }
+            }
+            if (active) {
+                // ---------------- epilogue ----------------
+                // combine the two halves' row sums, then each half handles its 32 output columns
+                float* lrow = xrow_base;
+                named_bar_sync(bar_id, kPairThreads);  // all max-exchange reads of the last tile are done
+                lrow[hf * kBlockM] = l_run;
+                named_bar_sync(bar_id, kPairThreads);
+                float l_tot = l_run + lrow[(hf ^ 1) * kBlockM];
+                named_bar_sync(bar_id, kPairThreads);  // reads done before the next item reuses the slot
+
+                constexpr int kOutCols = kHeadDim / 2;
+                const int col0 = hf * kOutCols;
+                float o[kOutCols];
+                if (num_live > 0) {
+                    mbar_wait(bars_r + 8u * (kBarOFull + x), oi & 1u);
+                    tc_fence_after();
+                    tmem_ld32(t_o, reinterpret_cast<uint32_t(&)[32]>(o));
+                    tc_wait_ld();
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kOutCols; ++u) o[u] = 0.f;
+                }
+
+                if (item.kind == kItemHeadPart) {
+                    // this CTA owns only the trailing key tiles of the pair: publish an un-normalised
+                    // partial for CTA blockIdx.x - 1, which holds the leading key tiles
+                    const size_t slot = (static_cast<size_t>(blockIdx.x) * 2 + x) * kBlockM + r;
+                    float4* dst = reinterpret_cast<float4*>(p.part_o + slot * kHeadDim + col0);
+#pragma unroll
+                    for (int u = 0; u < kOutCols / 4; ++u)
+                        dst[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+                    if (hf == 0) {
+                        p.part_ml[slot * 2] = m_ref;
+                        p.part_ml[slot * 2 + 1] = l_tot;
+                    }
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) st_release_gpu(p.part_flag + blockIdx.x * kNumSoftmaxWarps + warp, 1);
+                } else {
+                    if (item.kind == kItemTailPart) {
+                        // merge with the partial CTA blockIdx.x + 1 published for the same rows (its
+                        // half-0 warp of the same quadrant wrote m and l, this warp's twin wrote the
+                        // columns); own part first: fixed order, deterministic
+                        const int* flag_o = p.part_flag + (blockIdx.x + 1) * kNumSoftmaxWarps + warp;
+                        const int* flag_ml = p.part_flag + (blockIdx.x + 1) * kNumSoftmaxWarps + (warp & ~4);
+                        uint32_t spins = 0;
+                        while (ld_acquire_gpu(flag_o) == 0 || ld_acquire_gpu(flag_ml) == 0) {
+                            if (++spins > RF_MBAR_SPIN_LIMIT) __trap();
+                        }
+                        const size_t slot = (static_cast<size_t>(blockIdx.x + 1) * 2 + x) * kBlockM + r;
+                        const float m2 = __ldcg(p.part_ml + slot * 2);
+                        const float l2 = __ldcg(p.part_ml + slot * 2 + 1);
+                        const float ms = fmaxf(m_ref, m2);
+                        const float w1 = (m_ref == -CUDART_INF_F) ? 0.f : ex2(m_ref - ms);
+                        const float w2 = (m2 == -CUDART_INF_F) ? 0.f : ex2(m2 - ms);
+                        const float4* src = reinterpret_cast<const float4*>(p.part_o + slot * kHeadDim + col0);
+#pragma unroll
+                        for (int u = 0; u < kOutCols / 4; ++u) {
+                            const float4 t = __ldcg(src + u);
+                            o[4 * u] = o[4 * u] * w1 + t.x * w2;
+                            o[4 * u + 1] = o[4 * u + 1] * w1 + t.y * w2;
+                            o[4 * u + 2] = o[4 * u + 2] * w1 + t.z * w2;
+                            o[4 * u + 3] = o[4 * u + 3] * w1 + t.w * w2;
+                        }
+                        l_tot = l_tot * w1 + l2 * w2;
+                        m_ref = ms;
+                    }
+                    if (row < p.S) {
+                        if (p.o_partial != nullptr) {
+                            const size_t ridx = (static_cast<size_t>(b) * p.H + h) * p.S + row;
+                            float4* dst = reinterpret_cast<float4*>(p.o_partial + ridx * kHeadDim + col0);
+#pragma unroll
+                            for (int u = 0; u < kOutCols / 4; ++u)
+                                dst[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+                            if (hf == 0) {
+                                p.m_partial[ridx] = m_ref;
+                                p.l_partial[ridx] = l_tot;
+                            }
+                        } else {
+                            const float inv = l_tot > 0.f ? 1.0f / l_tot : 0.f;
+                            const size_t off = static_cast<size_t>(b) * p.o_sb + static_cast<size_t>(h) * p.o_sh +
+                                               static_cast<size_t>(row) * p.o_ss + col0;
+                            if (p.out_dtype == 2) {
+                                float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+#pragma unroll
+                                for (int u = 0; u < kOutCols / 4; ++u)
+                                    dst[u] = make_float4(o[4 * u] * inv, o[4 * u + 1] * inv, o[4 * u + 2] * inv,
+                                                         o[4 * u + 3] * inv);
+                            } else {
+                                uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + off);
+#pragma unroll
+                                for (int u = 0; u < kOutCols / 8; ++u) {
+                                    uint32_t w[4];
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        const float a0 = o[8 * u + 2 * e] * inv, a1 = o[8 * u + 2 * e + 1] * inv;
+                                        w[e] = (p.out_dtype == 0) ? pack2<true>(a0, a1) : pack2<false>(a0, a1);
+                                    }
+                                    dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            if (active && num_live > 0) ++oi;
+        }
+    }
+
+    // ---------------- teardown ----------------
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+}  // namespace
+
+size_t fa_fwd_sm100_v2_smem_bytes() {
+    return Smem::xchg + Smem::xchg_bytes + 1024;  // + alignment slack
+}
+
+cudaError_t launch_fa_fwd_sm100_v2(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
+                                const FaParams& p, bool bf16, int grid, cudaStream_t stream) {
+    const bool has_bias = p.tile_flags != nullptr;
+    void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const FaParams) =
+        bf16 ? (has_bias ? fa_fwd_sm100_v2_kernel<true, true> : fa_fwd_sm100_v2_kernel<true, false>)
+             : (has_bias ? fa_fwd_sm100_v2_kernel<false, true> : fa_fwd_sm100_v2_kernel<false, false>);
+    const size_t smem = fa_fwd_sm100_v2_smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kThreads, smem, stream>>>(tmq, tmk, tmv, p);
+    return cudaGetLastError();
+}
+
+}  // namespace rf

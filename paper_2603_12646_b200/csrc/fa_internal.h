@@ -67,6 +67,17 @@ struct SimtParams {
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
                                 const FaParams& p, bool bf16, int grid, cudaStream_t stream);
+// decoupled-pipeline variant (fa_fwd_sm100_v2.cu): same contract, same workspace layout
+cudaError_t launch_fa_fwd_sm100_v2(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
+                                   const FaParams& p, bool bf16, int grid, cudaStream_t stream);
+// narrow-window kernel (fa_fwd_sm100_local.cu): wl + wr <= 127, one 256-key strip per query tile;
+// reads the raw pad_bias [B,S] (nullable), needs no workspace
+bool fa_fwd_sm100_local_covers(int wl, int wr);
+int fa_fwd_sm100_local_grid(const FaParams& p, int sms);
+size_t fa_fwd_sm100_local_smem_bytes();
+cudaError_t launch_fa_fwd_sm100_local(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
+                                      const FaParams& p, const float* pad_bias, bool bf16, int grid,
+                                      cudaStream_t stream);
 size_t fa_fwd_sm100_smem_bytes();
 size_t fa_fwd_sm100_partial_bytes(int grid);
 void fa_fwd_sm100_partial_carve(void* base, int grid, FaParams* p, void** flags, size_t* flag_bytes);
