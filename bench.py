@@ -169,6 +169,33 @@ def time_op(torch, P, sets, spec, steps, warmup, out_sets):
     return e0.elapsed_time(e1) / steps  # ms per step
 
 
+def time_op_graph(torch, P, sets, spec, replays, out_sets):
+    """Device time per op for kernels too short to time through per-call host launches (the local
+    layer runs ~20 us, the Python call path costs more): one pass over the rotating input sets is
+    captured in a CUDA graph and replayed."""
+    n = len(sets)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for i in range(n):
+            P.flash_attention(*sets[i], spec, out=out_sets[i])
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(n):
+            P.flash_attention(*sets[i], spec, out=out_sets[i])
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(replays):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / (replays * n)  # ms per op
+
+
 def make_sets(torch, b, h, s, d, n_sets, seed):
     g = torch.Generator(device="cuda").manual_seed(seed)
     sets, outs = [], []
@@ -230,8 +257,9 @@ def run_ours(args):
     for t_, src in zip(host, sets[0]):
         t_.copy_(src.float())
     hq, hk, hv = [t_.numpy() for t_ in host]
-    for _ in range(3):
-        P.flash_attention(hq, hk, hv, spec, device=local_rank)
+    out_h = None
+    for _ in range(6):  # same hold-the-previous-result pattern as the timed loop: both page-locked result
+        out_h = P.flash_attention(hq, hk, hv, spec, device=local_rank)  # buffers exist before timing starts
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -257,10 +285,17 @@ def run_ours(args):
                 extra[f"S{s2}"] = {"ms": ms2, "tflops": f2 / ms2 / 1e9, "frac_of_peak": f2 / ms2 / 1e9 / peaks["bf16"]}
                 del sets2, outs2
             wl, wr = P.local_window_attrs()
-            msl = time_op(torch, P, sets, P.AttentionSpec(0.0, wl, wr), 50, 5, outs)
+            msl = time_op_graph(torch, P, sets, P.AttentionSpec(0.0, wl, wr), 20, outs)
             bytes_l = 4.0 * B * H * S * D * 2
             extra["S8192_local_63_64"] = {"ms": msl, "gbs": bytes_l / msl / 1e6, "frac_of_hbm": bytes_l / msl / 1e6 / peaks["hbm"],
-                                          "bound": "hbm"}
+                                          "bound": "hbm", "kernel": "fa_fwd_sm100_local_kernel",
+                                          "timing": "CUDA-graph replay over the 6 rotating input sets"}
+            sets4, outs4 = make_sets(torch, 4, H, 16384, D, 2, seed=9)
+            ms4 = time_op_graph(torch, P, sets4, P.AttentionSpec(0.0, wl, wr), 10, outs4)
+            bytes4 = 4.0 * 4 * H * 16384 * D * 2
+            extra["S16384_B4_local_63_64"] = {"ms": ms4, "gbs": bytes4 / ms4 / 1e6, "frac_of_hbm": bytes4 / ms4 / 1e6 / peaks["hbm"],
+                                              "bound": "hbm"}
+            del sets4, outs4
             # classifier forward (configs[1]): ModernBERT-base shape, B=1, S=8192, random-init weights
             try:
                 from paper_2603_12646_b200.classifier import Classifier, ClassifierConfig, init_weights

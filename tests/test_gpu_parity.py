@@ -507,3 +507,48 @@ def test_cpp_mirror_attention_test(torch_mod):
     res = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(res.stdout[-2000:], res.stderr[-2000:])
     assert res.returncode == 0 and "all checks passed" in res.stdout
+
+
+# ------------------------------------------------------------------ narrow-window kernel (fa_fwd_sm100_local.cu)
+@pytest.mark.parametrize("wl,wr", [(63, 64), (127, 0), (0, 127), (100, 27), (0, 0), (5, 9)])
+def test_narrow_window_kernel_grid(torch_mod, P, oracle, wl, wr):
+    """Windows with wl + wr <= 127 take the one-strip-per-query-tile kernel.  Sequence lengths around the
+    128-row tile, random padding masks (dead rows included), additive non-masking bias values, and a
+    batch x head count that gives several CTAs a run of tiles crossing head boundaries."""
+    rng = np.random.default_rng(wl * 131 + wr)
+    worst = 0.0
+    for (B, H, S) in ((1, 1, 1), (2, 2, 5), (1, 2, 127), (1, 2, 128), (2, 1, 129), (1, 3, 300), (2, 12, 1000)):
+        q, k, v = [oracle.round_bf16(rng.uniform(-1, 1, (B, H, S, 64)).astype(np.float32)) for _ in range(3)]
+        masked = rng.uniform(size=(B, 1, 1, S)) < 0.3
+        bias = np.where(rng.uniform(size=(B, 1, 1, S)) < 0.2, rng.uniform(-2, 2, (B, 1, 1, S)), 0.0)
+        pb = np.where(masked, -65504.0, bias).astype(np.float32)
+        for use_pb in (None, pb):
+            err, got, want = run_case(torch_mod, P, oracle, q, k, v, 0.0, wl, wr, use_pb, expect_kernel="tcgen05")
+            worst = max(worst, err)
+            assert err <= TOL, (B, H, S, wl, wr, use_pb is not None, err)
+            # rows with no live key are exactly 0, as in the reference (attention.cpp:175,204-207)
+            assert np.array_equal(got[want == 0.0], want[want == 0.0])
+    print("worst max-abs", worst)
+
+
+def test_narrow_window_kernel_long_padded_tail(torch_mod, P, oracle):
+    """8K local layer with a 1192-token padded tail: queries beyond the valid length whose whole window is
+    padding give 0; output in f32 and through a [B,S,H,d] view."""
+    torch = torch_mod
+    rng = np.random.default_rng(5)
+    B, H, S = 1, 4, 8192
+    q, k, v = [oracle.round_bf16(rng.uniform(-1, 1, (B, H, S, 64)).astype(np.float32)) for _ in range(3)]
+    pb = tail_pad(B, S, [7000])
+    tq, tk, tv = dev_tensors(torch, (q, k, v))
+    tpb = torch.from_numpy(pb).cuda()
+    want = oracle.flash_attention(q, k, v, 0.0, 63, 64, pb, threads=8)
+    got32 = P.flash_attention(tq, tk, tv, P.AttentionSpec(0.0, 63, 64, tpb), out_dtype=torch.float32).cpu().numpy()
+    assert np.abs(got32 - want).max() <= TOL
+    assert not got32[:, :, 7064:].any()
+    # packed [B,S,3,H,d] projections read in place, [B,S,H,d] output written in place
+    qkv = torch.stack([t.permute(0, 2, 1, 3) for t in (tq, tk, tv)], dim=2).contiguous()  # [B,S,3,H,d]
+    out = torch.empty(B, S, H, 64, device="cuda", dtype=torch.bfloat16)
+    P.flash_attention(qkv[:, :, 0].permute(0, 2, 1, 3), qkv[:, :, 1].permute(0, 2, 1, 3), qkv[:, :, 2].permute(0, 2, 1, 3),
+                      P.AttentionSpec(0.0, 63, 64, tpb), out=out.permute(0, 2, 1, 3))
+    torch.cuda.synchronize()
+    assert np.abs(out.permute(0, 2, 1, 3).float().cpu().numpy() - want).max() <= TOL

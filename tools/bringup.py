@@ -174,6 +174,41 @@ def case_time(name, B, H, S, wl, wr, flags, iters=20, kernel="tcgen05"):
          "tflops": flops / ms / 1e9, "gbs": 4 * B * H * S * 64 * 2 / ms / 1e6})
 
 
+def case_time_graph(name, B, H, S, wl, wr, lens=None, iters=20):
+    """Device time per call with the launches replayed from a CUDA graph (no host launch cost)."""
+    import torch
+    import paper_2603_12646_b200 as P
+    q, k, v = make_inputs(B, H, S, 64, seed=1)
+    pb = None
+    if lens is not None:
+        mask = torch.zeros(B, 1, 1, S, device="cuda")
+        for b, n in enumerate(lens):
+            mask[b, ..., :n] = 1
+        pb = P.pad_bias_from_mask(mask)
+    spec = P.AttentionSpec(0.0, wl, wr, pb)
+    out = torch.empty_like(q)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            P.flash_attention(q, k, v, spec, out=out)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(iters):
+            P.flash_attention(q, k, v, spec, out=out)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / (5 * iters)
+    log({"case": name, "B": B, "H": H, "S": S, "wl": wl, "lens": lens, "us_per_call_graph": ms * 1000,
+         "gbs": 4 * B * H * S * 64 * 2 / ms / 1e6})
+
+
 def case_clf(name, S, B=1, iters=5, padded=False):
     import torch
     from paper_2603_12646_b200.classifier import Classifier, ClassifierConfig, init_weights
@@ -252,6 +287,11 @@ CASES = {
     "time_16k_ts": lambda: case_time("time_16k_ts", 1, 12, 16384, -1, -1, 0, iters=10),
     "time_32k_ts": lambda: case_time("time_32k_ts", 1, 12, 32768, -1, -1, 0, iters=5),
     "time_8k_local_ts": lambda: case_time("time_8k_local_ts", 1, 12, 8192, 63, 64, 0),
+    "graph_8k_local": lambda: case_time_graph("graph_8k_local", 1, 12, 8192, 63, 64),
+    "graph_8k_local_pad": lambda: case_time_graph("graph_8k_local_pad", 1, 12, 8192, 63, 64, lens=[7000]),
+    "graph_32k_local": lambda: case_time_graph("graph_32k_local", 1, 12, 32768, 63, 64),
+    "graph_16k_b4_local": lambda: case_time_graph("graph_16k_b4_local", 4, 12, 16384, 63, 64),
+    "graph_8k_global": lambda: case_time_graph("graph_8k_global", 1, 12, 8192, -1, -1),
     "clf_8k": lambda: case_clf("clf_8k", 8192),
     "clf_8k_pad": lambda: case_clf("clf_8k_pad", 8192, padded=True),
     "clf_16k_b4": lambda: case_clf("clf_16k_b4", 16384, B=4, iters=3),
