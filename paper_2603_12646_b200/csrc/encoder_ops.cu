@@ -15,29 +15,42 @@
 namespace {
 
 // qkv: [tokens, 3, H, d] bf16; cos/sin: [S, d/2] f32; token t has position t % S.
-// One thread per (token, q|k, head, pair i): rotates elements (i, i + d/2) -- the "rotate_half"
-// convention of ModernBERT / HF rotary embeddings.
+// Rotates elements (i, i + d/2) -- the "rotate_half" convention of ModernBERT / HF rotary embeddings.
+// One thread per 8 pairs: two 16-byte loads and two 16-byte stores of bf16, cos/sin as float4s, so a
+// warp covers whole 128-byte head rows (HBM-bound: Q and K are read and written once).  d % 16 == 0.
 __global__ void __launch_bounds__(256) rope_qkv_kernel(__nv_bfloat16* __restrict__ qkv, const float* __restrict__ cosb,
                                                        const float* __restrict__ sinb, long long tokens, int S, int H,
                                                        int d) {
     const int half = d >> 1;
+    const int vecs = half >> 3;  // threads per (token, q|k, head) row
     const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const long long total = tokens * 2 * H * half;
+    const long long total = tokens * 2 * H * vecs;
     if (idx >= total) return;
-    const int i = static_cast<int>(idx % half);
-    long long r = idx / half;
+    const int i = static_cast<int>(idx % vecs) * 8;
+    long long r = idx / vecs;
     const int h = static_cast<int>(r % H);
     r /= H;
     const int which = static_cast<int>(r % 2);  // 0 = q, 1 = k
     const long long t = r / 2;
     const int pos = static_cast<int>(t % S);
     __nv_bfloat16* base = qkv + ((t * 3 + which) * H + h) * d;
-    const float x1 = __bfloat162float(base[i]);
-    const float x2 = __bfloat162float(base[i + half]);
-    const float c = cosb[static_cast<long long>(pos) * half + i];
-    const float s = sinb[static_cast<long long>(pos) * half + i];
-    base[i] = __float2bfloat16_rn(x1 * c - x2 * s);
-    base[i + half] = __float2bfloat16_rn(x2 * c + x1 * s);
+    uint4 a = *reinterpret_cast<const uint4*>(base + i);
+    uint4 b = *reinterpret_cast<const uint4*>(base + i + half);
+    const float4* cp = reinterpret_cast<const float4*>(cosb + static_cast<long long>(pos) * half + i);
+    const float4* sp = reinterpret_cast<const float4*>(sinb + static_cast<long long>(pos) * half + i);
+    const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
+    const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    __nv_bfloat162* a2 = reinterpret_cast<__nv_bfloat162*>(&a);
+    __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&b);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 x1 = __bfloat1622float2(a2[e]), x2 = __bfloat1622float2(b2[e]);
+        a2[e] = __floats2bfloat162_rn(x1.x * cs[2 * e] - x2.x * sn[2 * e], x1.y * cs[2 * e + 1] - x2.y * sn[2 * e + 1]);
+        b2[e] = __floats2bfloat162_rn(x2.x * cs[2 * e] + x1.x * sn[2 * e], x2.y * cs[2 * e + 1] + x1.y * sn[2 * e + 1]);
+    }
+    *reinterpret_cast<uint4*>(base + i) = a;
+    *reinterpret_cast<uint4*>(base + i + half) = b;
 }
 
 // x (f32 residual stream, [rows, n]) += delta (bf16, may be null); y = LayerNorm(x) * w -> bf16.
@@ -105,20 +118,27 @@ __global__ void __launch_bounds__(128) add_layernorm_kernel(float* __restrict__ 
     }
 }
 
-// wi_out: [rows, 2*I] bf16 (input half then gate half); act: [rows, I] bf16 = gelu(input) * gate
+// wi_out: [rows, 2*I] bf16 (input half then gate half); act: [rows, I] bf16 = gelu(input) * gate.
+// One thread per 8 outputs (16-byte loads / store); I % 8 == 0.
 __global__ void __launch_bounds__(256) geglu_kernel(const __nv_bfloat16* __restrict__ wi_out, __nv_bfloat16* __restrict__ act,
                                                     long long rows, int I) {
     const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const long long total = rows * (I >> 1);
+    const int vecs = I >> 3;
+    const long long total = rows * vecs;
     if (idx >= total) return;
-    const long long row = idx / (I >> 1);
-    const int c = static_cast<int>(idx % (I >> 1)) * 2;
-    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(wi_out + row * 2 * I + c);
-    const __nv_bfloat162 g = *reinterpret_cast<const __nv_bfloat162*>(wi_out + row * 2 * I + I + c);
+    const long long row = idx / vecs;
+    const int c = static_cast<int>(idx % vecs) * 8;
+    uint4 a = *reinterpret_cast<const uint4*>(wi_out + row * 2 * I + c);
+    const uint4 g = *reinterpret_cast<const uint4*>(wi_out + row * 2 * I + I + c);
     auto gelu = [](float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); };
-    const __nv_bfloat162 o = __floats2bfloat162_rn(gelu(__bfloat162float(a.x)) * __bfloat162float(g.x),
-                                                   gelu(__bfloat162float(a.y)) * __bfloat162float(g.y));
-    *reinterpret_cast<__nv_bfloat162*>(act + row * I + c) = o;
+    __nv_bfloat162* a2 = reinterpret_cast<__nv_bfloat162*>(&a);
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 x = __bfloat1622float2(a2[e]), y = __bfloat1622float2(g2[e]);
+        a2[e] = __floats2bfloat162_rn(gelu(x.x) * y.x, gelu(x.y) * y.y);
+    }
+    *reinterpret_cast<uint4*>(act + row * I + c) = a;
 }
 
 int fail_cuda(cudaError_t e) { return e == cudaSuccess ? RF_OK : RF_ERR_CUDA; }
@@ -129,8 +149,8 @@ extern "C" {
 
 int rf_rope_qkv(void* qkv, const float* cosb, const float* sinb, int64_t tokens, int64_t S, int64_t H, int64_t d,
                 void* stream) {
-    if (qkv == nullptr || cosb == nullptr || sinb == nullptr || d % 2 || S <= 0) return RF_ERR_ARG;
-    const long long total = tokens * 2 * H * (d / 2);
+    if (qkv == nullptr || cosb == nullptr || sinb == nullptr || d % 16 || S <= 0) return RF_ERR_ARG;
+    const long long total = tokens * 2 * H * (d / 16);
     if (total == 0) return RF_OK;
     rope_qkv_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<__nv_bfloat16*>(qkv), cosb, sinb, tokens, static_cast<int>(S), static_cast<int>(H), static_cast<int>(d));
@@ -153,8 +173,8 @@ int rf_add_layernorm(float* x, const void* delta, const float* w, void* y, int64
 }
 
 int rf_geglu(const void* wi_out, void* act, int64_t rows, int64_t I, void* stream) {
-    if (wi_out == nullptr || act == nullptr || I % 2) return RF_ERR_ARG;
-    const long long total = rows * (I / 2);
+    if (wi_out == nullptr || act == nullptr || I % 8) return RF_ERR_ARG;
+    const long long total = rows * (I / 8);
     if (total == 0) return RF_OK;
     geglu_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const __nv_bfloat16*>(wi_out), static_cast<__nv_bfloat16*>(act), rows, static_cast<int>(I));
