@@ -12,6 +12,7 @@ constexpr int kUnroll = 8;    // body repeats per loop iteration
 
 enum Op {
     kFfma, kFfmaImm, kFfma2, kFadd2, kFmnmx, kFmnmx3, kF2fp, kLea, kShlAdd, kImad, kMufu, kHfma2, kHfma2Bf16,
+    kMufuBf16x2, kMufuF16x2, kMufuF16, kPrmt, kHadd2Bf16,
     kMixMufuFfma2,   // 1 MUFU : 1 FFMA2
     kMixFfma2Fmnmx,  // 1 FFMA2 : 1 FMNMX
     kMixFfma2Lea,    // 1 FFMA2 : 1 LEA
@@ -40,6 +41,15 @@ __device__ __forceinline__ void body(uint32_t (&r)[kChains], uint64_t (&w)[kChai
         }
         if (kOp == kImad) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(r[c]) : "r"(a), "r"(b));
         if (kOp == kMufu) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+r"(r[c]));
+        if (kOp == kMufuBf16x2) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(r[c]));
+        if (kOp == kMufuF16x2) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(r[c]));
+        if (kOp == kMufuF16) {
+            unsigned short hs = static_cast<unsigned short>(r[c]);
+            asm volatile("ex2.approx.f16 %0, %0;" : "+h"(hs));
+            r[c] = hs;
+        }
+        if (kOp == kPrmt) asm volatile("prmt.b32 %0, %0, %1, 0x5410;" : "+r"(r[c]) : "r"(a));
+        if (kOp == kHadd2Bf16) asm volatile("add.rn.bf16x2 %0, %0, %1;" : "+r"(r[c]) : "r"(a));
         if (kOp == kHfma2) asm volatile("fma.rn.f16x2 %0, %0, %1, %2;" : "+r"(r[c]) : "r"(a), "r"(b));
         if (kOp == kHfma2Bf16) asm volatile("fma.rn.bf16x2 %0, %0, %1, %2;" : "+r"(r[c]) : "r"(a), "r"(b));
         if (kOp == kMixMufuFfma2) {
@@ -147,6 +157,11 @@ int main() {
     run<kShlAdd>("SHL ; IADD", in, out, clk);
     run<kImad>("IMAD", in, out, clk);
     run<kMufu>("MUFU.EX2", in, out, clk);
+    run<kMufuBf16x2>("ex2.bf16x2 (2 MUFU + PRMT, counted as 1)", in, out, clk);
+    run<kMufuF16x2>("ex2.f16x2 (2 MUFU + PRMT, counted as 1)", in, out, clk);
+    run<kMufuF16>("ex2.f16 scalar", in, out, clk);
+    run<kPrmt>("PRMT", in, out, clk);
+    run<kHadd2Bf16>("HADD2.BF16", in, out, clk);
     run<kHfma2>("HFMA2 f16x2", in, out, clk);
     run<kHfma2Bf16>("HFMA2 bf16x2", in, out, clk);
     run<kMixMufuFfma2>("mix MUFU+FFMA2", in, out, clk);
