@@ -552,3 +552,34 @@ def test_narrow_window_kernel_long_padded_tail(torch_mod, P, oracle):
                       P.AttentionSpec(0.0, 63, 64, tpb), out=out.permute(0, 2, 1, 3))
     torch.cuda.synchronize()
     assert np.abs(out.permute(0, 2, 1, 3).float().cpu().numpy() - want).max() <= TOL
+
+
+# ------------------------------------------------------------------ memory model, measured
+def test_classifier_session_32k_under_800mb_by_driver(torch_mod, P):
+    """BASELINE target: a 32K-token classifier session in O(n) memory, < 800 MB.  Measured as the driver
+    sees it (cudaMemGetInfo before loading the model vs after the forward; the allocator keeps its
+    high-water mark reserved), beside the reference's memory model for the same shape."""
+    torch = torch_mod
+    from paper_2603_12646_b200.classifier import Classifier, ClassifierConfig, init_weights
+    S = 32768
+    P.flash_attention(*[torch.zeros(1, 1, 128, 64, device="cuda", dtype=torch.bfloat16)] * 3)  # modules loaded
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    free0, _ = torch.cuda.mem_get_info()
+    cfg = ClassifierConfig()
+    clf = Classifier(cfg, init_weights(cfg, 7), torch.device("cuda:0"))
+    ids = torch.randint(0, cfg.vocab_size, (1, S), device="cuda")
+    mask = torch.ones(1, S, device="cuda")
+    mask[:, S - S // 8:] = 0
+    logits = clf.forward(ids, mask)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    session = free0 - free1
+    print("32K session bytes (driver view):", session)
+    assert torch.isfinite(logits).all()
+    assert session < 800e6, session
+    # what materialised S x S scores alone would have taken for ONE layer (attention.cpp:244-247): 24 GiB
+    assert P.mask_memory_bytes(1, cfg.heads, S, 2) == 25769803776
+    assert P.fa_memory_bytes(1, cfg.heads, S, cfg.head_dim, 64, 2) == 50528256
+    del clf, logits
+    torch.cuda.empty_cache()
