@@ -322,8 +322,27 @@ def run_ours(args):
                     "weights_MB": clf.weight_bytes() / 1e6, "cuda_graph": True,
                     "paper_mi300x_ms": 105.0, "note": "random-init weights, synthetic token ids; paper number is other hardware (PAPER.md:402)"}
                 del clf, run
+                # the same forward through the native session (rf_clf.h): host token ids in, host logits out,
+                # cuBLAS GEMMs + this library's kernels, no Python between the launches
+                from paper_2603_12646_b200.classifier import NativeClassifier
+                nat = NativeClassifier(ccfg, init_weights(ccfg, 7), device=local_rank)
+                ids_h = ids.cpu()
+                for _ in range(3):
+                    nat.forward(ids_h)
+                t_n = time.perf_counter()
+                dev_ms = []
+                for _ in range(10):
+                    nat.forward(ids_h)
+                    dev_ms.append(nat.last_forward_ms)
+                wall_ms = (time.perf_counter() - t_n) / 10 * 1e3
+                wb, ab = nat.session_bytes()
+                extra["classifier_native_S8192_B1"] = {
+                    "ms_per_request_wall": wall_ms, "ms_per_request_device": sorted(dev_ms)[len(dev_ms) // 2],
+                    "api": "rf_clf_forward(host ids) -> host logits", "weights_MB": wb / 1e6, "arena_MB": ab / 1e6}
+                nat.close()
             except Exception as e:  # noqa: BLE001
-                extra["classifier_fwd_S8192_B1"] = {"error": repr(e)[:200]}
+                extra.setdefault("classifier_fwd_S8192_B1", {"error": repr(e)[:200]})
+                extra["classifier_error"] = repr(e)[:200]
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
         if os.path.exists(prof):

@@ -26,7 +26,19 @@ EXPORTS = [
     "rf_graph_find_patterns", "rf_graph_rewrite", "rf_graph_dce", "rf_graph_interpret", "rf_graph_result_count",
     "rf_graph_result_name", "rf_graph_result_rank", "rf_graph_result_dims", "rf_graph_result_data",
     "rf_graph_result_is_f16", "rf_graph_result_stats", "rf_graph_result_free",
+    # include/rf_clf.h
+    "rf_clf_config_default", "rf_clf_weight_elems", "rf_clf_create", "rf_clf_forward", "rf_clf_session_bytes",
+    "rf_clf_last_forward_ms", "rf_clf_destroy",
 ]
+
+
+class RfClfConfig(C.Structure):
+    _fields_ = [
+        ("vocab_size", C.c_int32), ("hidden", C.c_int32), ("n_layers", C.c_int32), ("heads", C.c_int32),
+        ("head_dim", C.c_int32), ("mlp", C.c_int32), ("global_every", C.c_int32), ("local_window", C.c_int32),
+        ("n_labels", C.c_int32), ("mlp_chunk_rows", C.c_int32), ("rope_theta_global", C.c_float),
+        ("rope_theta_local", C.c_float), ("eps", C.c_float),
+    ]
 
 
 class RfFaParams(C.Structure):
@@ -116,6 +128,20 @@ def load(build_if_missing: bool = True):
     lib.rf_device_check.argtypes = [i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
     lib.rf_fa_host_release.argtypes = []
     lib.rf_fa_host_release.restype = None
+    lib.rf_clf_config_default.argtypes = [C.POINTER(RfClfConfig)]
+    lib.rf_clf_config_default.restype = None
+    lib.rf_clf_weight_elems.argtypes = [C.POINTER(RfClfConfig)]
+    lib.rf_clf_weight_elems.restype = C.c_size_t
+    lib.rf_clf_create.argtypes = [C.POINTER(RfClfConfig), f32p, C.c_size_t, i32, C.POINTER(vp)]
+    lib.rf_clf_create.restype = C.c_int
+    lib.rf_clf_forward.argtypes = [vp, C.POINTER(i64), f32p, i64, i64, f32p]
+    lib.rf_clf_forward.restype = C.c_int
+    lib.rf_clf_session_bytes.argtypes = [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
+    lib.rf_clf_session_bytes.restype = C.c_int
+    lib.rf_clf_last_forward_ms.argtypes = [vp]
+    lib.rf_clf_last_forward_ms.restype = C.c_float
+    lib.rf_clf_destroy.argtypes = [vp]
+    lib.rf_clf_destroy.restype = None
     for name in ("rf_fa_validate", "rf_fa_fwd_workspace_bytes", "rf_fa_stats_query", "rf_fa_fwd", "rf_fa_merge",
                  "rf_fa_rescale_partial", "rf_fa_normalize", "rf_pad_bias_from_mask", "rf_cast_f32_to",
                  "rf_cast_to_f32", "rf_fa_fwd_host", "rf_fused_flash_attention_op", "rf_device_check",

@@ -210,3 +210,75 @@ class Classifier:
 
     def weight_bytes(self) -> int:
         return sum(v.numel() * v.element_size() for v in self.w.values())
+
+
+# ------------------------------------------------------------------------------------------------
+# native session (include/rf_clf.h): the same forward without Python in the loop
+# ------------------------------------------------------------------------------------------------
+WEIGHT_ORDER_HEAD = ("tok_emb", "emb_norm", "final_norm", "head_dense", "head_norm", "cls_w", "cls_b")
+WEIGHT_ORDER_LAYER = ("attn_norm", "wqkv", "wo", "mlp_norm", "wi", "wo2")
+
+
+def pack_weights(cfg: ClassifierConfig, weights: Dict[str, torch.Tensor]) -> torch.Tensor:
+    """One contiguous f32 blob in the tensor order rf_clf_create expects (rf_clf.h)."""
+    parts = [weights[k].reshape(-1).float() for k in WEIGHT_ORDER_HEAD]
+    for i in range(cfg.n_layers):
+        parts += [weights[f"l{i}.{k}"].reshape(-1).float() for k in WEIGHT_ORDER_LAYER]
+    return torch.cat(parts).contiguous()
+
+
+class NativeClassifier:
+    """rf_clf session: token ids (host) -> logits (host) in one C call.  Same weights, same data path and
+    the same kernels as `Classifier`; the GEMMs go to cuBLAS directly instead of through torch."""
+
+    def __init__(self, cfg: ClassifierConfig, weights: Dict[str, torch.Tensor], device: int = 0):
+        import ctypes as C
+        self._C = C
+        self.cfg = cfg
+        self.lib = capi.load()
+        c = capi.RfClfConfig()
+        self.lib.rf_clf_config_default(C.byref(c))
+        c.vocab_size, c.hidden, c.n_layers, c.heads, c.head_dim = cfg.vocab_size, cfg.hidden, cfg.n_layers, cfg.heads, cfg.head_dim
+        c.mlp, c.global_every, c.local_window, c.n_labels = cfg.mlp, cfg.global_every, cfg.local_window, cfg.n_labels
+        c.mlp_chunk_rows = cfg.mlp_chunk_rows
+        c.rope_theta_global, c.rope_theta_local, c.eps = cfg.rope_theta_global, cfg.rope_theta_local, cfg.eps
+        blob = pack_weights(cfg, weights)
+        assert blob.numel() == self.lib.rf_clf_weight_elems(C.byref(c))
+        self._h = C.c_void_p()
+        capi.check(self.lib.rf_clf_create(C.byref(c), C.cast(blob.data_ptr(), C.POINTER(C.c_float)), blob.numel(), device,
+                                          C.byref(self._h)))
+
+    def forward(self, input_ids, attention_mask=None) -> torch.Tensor:
+        """input_ids [B,S] int64 (CPU tensor / ndarray), attention_mask [B,S] or None -> logits [B,n_labels] f32 (CPU)."""
+        C = self._C
+        ids = torch.as_tensor(input_ids).to("cpu", torch.int64).contiguous()
+        B, S = ids.shape
+        m = None
+        if attention_mask is not None:
+            m = torch.as_tensor(attention_mask).to("cpu", torch.float32).contiguous()
+        out = torch.empty((B, self.cfg.n_labels), dtype=torch.float32)
+        capi.check(self.lib.rf_clf_forward(self._h, C.cast(ids.data_ptr(), C.POINTER(C.c_int64)),
+                                           C.cast(m.data_ptr(), C.POINTER(C.c_float)) if m is not None else None,
+                                           B, S, C.cast(out.data_ptr(), C.POINTER(C.c_float))))
+        return out
+
+    @property
+    def last_forward_ms(self) -> float:
+        return float(self.lib.rf_clf_last_forward_ms(self._h))
+
+    def session_bytes(self):
+        C = self._C
+        w, a = C.c_size_t(), C.c_size_t()
+        capi.check(self.lib.rf_clf_session_bytes(self._h, C.byref(w), C.byref(a)))
+        return int(w.value), int(a.value)
+
+    def close(self):
+        if self._h:
+            self.lib.rf_clf_destroy(self._h)
+            self._h = self._C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

@@ -1,0 +1,559 @@
+// clf_runtime.cu -- native classifier session (include/rf_clf.h): token ids -> logits for the
+// ModernBERT-style encoder built on the FusedFlashAttention operator, without Python in the loop.
+//
+// Same data path as paper_2603_12646_b200/classifier.py (which stays as the torch-hosted mirror):
+//   x = LN(emb[ids])                                   embed_gather + rf_add_layernorm
+//   per layer: h = LN(x += mlp_prev); qkv = h Wqkv^T   library GEMM -> [B,S,3,H,d]
+//              rope(q, k) in place                     rf_rope_qkv
+//              attn = FusedFlashAttention(q, k, v)     rf_fa_fwd on strided views, [B,S,H*d] out
+//              x += attn Wo^T; h2 = LN(x)              library GEMM + rf_add_layernorm
+//              x += (gelu(h2 Wi_a) * h2 Wi_g) Wo2^T    library GEMMs + rf_geglu, in row chunks
+//   logits = head(LN(x)[CLS])                          clf_head_kernel
+// The pad-bias chain is built once per forward and shared by every layer (reference rewrite.cpp:303-318);
+// layer i is global iff i % global_every == 0, else local_window -> (w/2-1, w/2) (rewrite.cpp:355-361).
+//
+// Memory: the session owns the weights and one activation arena with fixed slots that are recycled
+// inside a layer: x (f32 stream), `big` (qkv, later the MLP intermediate), two ping-pong slots of one
+// bf16 activation each, the attention workspace, RoPE tables, ids, mask/bias.  The arena only grows.
+//
+// cuBLAS is resolved with dlopen/dlsym (four entry points) so that librf_fa.so itself has no link-time
+// dependency on it; a missing library is RF_ERR_CUDA at session creation, never a fallback.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/rf_clf.h"
+#include "fa_internal.h"
+
+namespace {
+
+int fail(int code, const std::string& msg) { return rf::set_last_error(code, msg); }
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(RF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- the four cuBLAS entry points, by hand (cublas_v2.h is not included: no link-time dependency) ----
+typedef void* cublasHandle_t;
+typedef int (*cublasCreate_fn)(cublasHandle_t*);
+typedef int (*cublasDestroy_fn)(cublasHandle_t);
+typedef int (*cublasSetStream_fn)(cublasHandle_t, cudaStream_t);
+typedef int (*cublasGemmEx_fn)(cublasHandle_t, int, int, int, int, int, const void*, const void*, int, int, const void*,
+                               int, int, const void*, void*, int, int, int, int);
+constexpr int kCublasOpN = 0, kCublasOpT = 1;
+constexpr int kCudaR16BF = 14;          // CUDA_R_16BF
+constexpr int kCublasCompute32F = 68;   // CUBLAS_COMPUTE_32F
+constexpr int kCublasGemmDefault = -1;  // CUBLAS_GEMM_DEFAULT
+
+struct Cublas {
+    void* dl = nullptr;
+    cublasCreate_fn create = nullptr;
+    cublasDestroy_fn destroy = nullptr;
+    cublasSetStream_fn set_stream = nullptr;
+    cublasGemmEx_fn gemm_ex = nullptr;
+    bool load(std::string* why) {
+        for (const char* name : {"libcublas.so.12", "libcublas.so", "/usr/local/cuda/lib64/libcublas.so.12"}) {
+            dl = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (dl != nullptr) break;
+        }
+        if (dl == nullptr) {
+            *why = "cuBLAS not found (dlopen libcublas.so.12)";
+            return false;
+        }
+        create = reinterpret_cast<cublasCreate_fn>(dlsym(dl, "cublasCreate_v2"));
+        destroy = reinterpret_cast<cublasDestroy_fn>(dlsym(dl, "cublasDestroy_v2"));
+        set_stream = reinterpret_cast<cublasSetStream_fn>(dlsym(dl, "cublasSetStream_v2"));
+        gemm_ex = reinterpret_cast<cublasGemmEx_fn>(dlsym(dl, "cublasGemmEx"));
+        if (!create || !destroy || !set_stream || !gemm_ex) {
+            *why = "cuBLAS entry points missing";
+            return false;
+        }
+        return true;
+    }
+};
+
+// ---- kernels of the session that the operator library did not have yet ----
+
+// x[row, :] = float(tok_emb[ids[row], :]); one warp per row, 16-byte loads.
+__global__ void __launch_bounds__(128) embed_gather_kernel(const __nv_bfloat16* __restrict__ emb,
+                                                           const long long* __restrict__ ids, float* __restrict__ x,
+                                                           long long rows, int hidden, int vocab) {
+    const long long row = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const int lane = threadIdx.x & 31;
+    long long id = ids[row];
+    id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
+    const __nv_bfloat16* src = emb + id * hidden;
+    float* dst = x + row * hidden;
+    for (int c = lane * 8; c < hidden; c += 256) {
+        const uint4 v = *reinterpret_cast<const uint4*>(src + c);
+        const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+        float4 a, b;
+        float2 t = __bfloat1622float2(v2[0]); a.x = t.x; a.y = t.y;
+        t = __bfloat1622float2(v2[1]); a.z = t.x; a.w = t.y;
+        t = __bfloat1622float2(v2[2]); b.x = t.x; b.y = t.y;
+        t = __bfloat1622float2(v2[3]); b.z = t.x; b.w = t.y;
+        *reinterpret_cast<float4*>(dst + c) = a;
+        *reinterpret_cast<float4*>(dst + c + 4) = b;
+    }
+}
+
+// x (f32) = float(h (bf16)): the stream restarts from the bf16-rounded LN(embeddings), as classifier.py does
+__global__ void __launch_bounds__(256) bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ h, float* __restrict__ x,
+                                                          long long n8) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n8) return;
+    const uint4 v = reinterpret_cast<const uint4*>(h)[i];
+    const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+    float4 a, b;
+    float2 t = __bfloat1622float2(v2[0]); a.x = t.x; a.y = t.y;
+    t = __bfloat1622float2(v2[1]); a.z = t.x; a.w = t.y;
+    t = __bfloat1622float2(v2[2]); b.x = t.x; b.y = t.y;
+    t = __bfloat1622float2(v2[3]); b.z = t.x; b.w = t.y;
+    reinterpret_cast<float4*>(x)[2 * i] = a;
+    reinterpret_cast<float4*>(x)[2 * i + 1] = b;
+}
+
+// Classification head for one sequence per CTA: pooled = hf[b, 0, :] (CLS); t = gelu(bf16(pooled Wd^T));
+// t = LN(t) * head_norm; logits = t Wc^T + b.  hidden <= 1024.
+__global__ void __launch_bounds__(256) clf_head_kernel(const __nv_bfloat16* __restrict__ hf, long long S, int hidden,
+                                                       const __nv_bfloat16* __restrict__ wd, const float* __restrict__ head_norm,
+                                                       const __nv_bfloat16* __restrict__ wc, const float* __restrict__ bc,
+                                                       int n_labels, float eps, float* __restrict__ logits) {
+    __shared__ float pooled[1024];
+    __shared__ float t[1024];
+    __shared__ float red[2][8];
+    const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const __nv_bfloat16* row = hf + static_cast<long long>(b) * S * hidden;
+    for (int c = tid; c < hidden; c += blockDim.x) pooled[c] = __bfloat162float(row[c]);
+    __syncthreads();
+    // dense: one warp per output feature, lanes stride over the input features
+    for (int j = warp; j < hidden; j += 8) {
+        const __nv_bfloat16* wr = wd + static_cast<long long>(j) * hidden;
+        float acc = 0.f;
+        for (int c = lane * 2; c < hidden; c += 64) {
+            const float2 w2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(wr + c));
+            acc += pooled[c] * w2.x + pooled[c + 1] * w2.y;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            const float v = __bfloat162float(__float2bfloat16_rn(acc));  // the GEMM output is bf16
+            t[j] = 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+        }
+    }
+    __syncthreads();
+    float s = 0.f;
+    for (int c = tid; c < hidden; c += blockDim.x) s += t[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[0][warp] = s;
+    __syncthreads();
+    float mean = 0.f;
+    for (int w = 0; w < 8; ++w) mean += red[0][w];
+    mean /= hidden;
+    float v = 0.f;
+    for (int c = tid; c < hidden; c += blockDim.x) v += (t[c] - mean) * (t[c] - mean);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[1][warp] = v;
+    __syncthreads();
+    float var = 0.f;
+    for (int w = 0; w < 8; ++w) var += red[1][w];
+    const float rstd = rsqrtf(var / hidden + eps);
+    for (int c = tid; c < hidden; c += blockDim.x) pooled[c] = (t[c] - mean) * rstd * head_norm[c];
+    __syncthreads();
+    for (int k = warp; k < n_labels; k += 8) {
+        const __nv_bfloat16* wr = wc + static_cast<long long>(k) * hidden;
+        float acc = 0.f;
+        for (int c = lane; c < hidden; c += 32) acc += pooled[c] * __bfloat162float(wr[c]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) logits[b * n_labels + k] = acc + bc[k];
+    }
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct LayerW {
+    const float* attn_norm;
+    const __nv_bfloat16* wqkv;
+    const __nv_bfloat16* wo;
+    const float* mlp_norm;
+    const __nv_bfloat16* wi;
+    const __nv_bfloat16* wo2;
+};
+
+}  // namespace
+
+struct rf_clf {
+    rf_clf_config cfg{};
+    int device = 0;
+    Cublas blas;
+    cublasHandle_t handle = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // weights: one bf16 block and one f32 block
+    void* w16 = nullptr;
+    void* w32 = nullptr;
+    size_t w16_bytes = 0, w32_bytes = 0;
+    const __nv_bfloat16 *tok_emb = nullptr, *head_dense = nullptr, *cls_w = nullptr;
+    const float *emb_norm = nullptr, *final_norm = nullptr, *head_norm = nullptr, *cls_b = nullptr;
+    std::vector<LayerW> layers;
+    // activation arena
+    void* arena = nullptr;
+    size_t arena_bytes = 0;
+    // RoPE tables are part of the arena layout; recomputed when S changes
+    int64_t rope_S = 0;
+    float last_ms = 0.f;
+};
+
+namespace {
+
+struct Layout {
+    size_t x, big, slot[2], ws, rope[4], ids, mask, bias, logits, total;
+    size_t ws_bytes;
+};
+
+Layout make_layout(const rf_clf_config& c, int64_t B, int64_t S, size_t attn_ws) {
+    Layout L{};
+    const size_t rows = static_cast<size_t>(B) * S, hid = c.hidden;
+    const size_t chunk = std::min<size_t>(rows, static_cast<size_t>(c.mlp_chunk_rows));
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = off;
+        off += align_up(bytes, 256);
+        return at;
+    };
+    L.x = take(rows * hid * 4);
+    L.big = take(std::max(rows * 3 * hid * 2, chunk * 3 * static_cast<size_t>(c.mlp) * 2));  // qkv | wi_out + act
+    L.slot[0] = take(rows * hid * 2);
+    L.slot[1] = take(rows * hid * 2);
+    L.ws_bytes = attn_ws;
+    L.ws = take(attn_ws);
+    for (int i = 0; i < 4; ++i) L.rope[i] = take(static_cast<size_t>(S) * (c.head_dim / 2) * 4);  // cos/sin x global/local
+    L.ids = take(rows * 8);
+    L.mask = take(rows * 4);
+    L.bias = take(rows * 4);
+    L.logits = take(static_cast<size_t>(B) * c.n_labels * 4);
+    L.total = off;
+    return L;
+}
+
+int check_cfg(const rf_clf_config* c) {
+    if (c == nullptr) return fail(RF_ERR_ARG, "config is null");
+    if (c->hidden != c->heads * c->head_dim) return fail(RF_ERR_SHAPE, "hidden must equal heads * head_dim");
+    if (c->head_dim != 64) return fail(RF_ERR_HEAD_DIM, "the classifier session needs head_dim 64");
+    if (c->hidden % 8 || c->hidden > 1024 || c->mlp % 8 || c->n_layers < 1 || c->vocab_size < 1 || c->n_labels < 1 ||
+        c->global_every < 1 || c->local_window < 2 || c->mlp_chunk_rows < 1)
+        return fail(RF_ERR_ARG, "bad classifier config");
+    return RF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void rf_clf_config_default(rf_clf_config* c) {
+    if (c == nullptr) return;
+    c->vocab_size = 50368;
+    c->hidden = 768;
+    c->n_layers = 22;
+    c->heads = 12;
+    c->head_dim = 64;
+    c->mlp = 1152;
+    c->global_every = 3;
+    c->local_window = 128;
+    c->n_labels = 3;
+    c->mlp_chunk_rows = 8192;
+    c->rope_theta_global = 160000.0f;
+    c->rope_theta_local = 10000.0f;
+    c->eps = 1e-5f;
+}
+
+size_t rf_clf_weight_elems(const rf_clf_config* c) {
+    if (c == nullptr) return 0;
+    const size_t hid = c->hidden, mlp = c->mlp;
+    size_t n = static_cast<size_t>(c->vocab_size) * hid + hid + hid + hid * hid + hid + static_cast<size_t>(c->n_labels) * hid +
+               c->n_labels;
+    n += static_cast<size_t>(c->n_layers) * (hid + 3 * hid * hid + hid * hid + hid + 2 * mlp * hid + hid * mlp);
+    return n;
+}
+
+int rf_clf_create(const rf_clf_config* cfg, const float* weights, size_t n_elems, int32_t device, rf_clf** out) {
+    int rc = check_cfg(cfg);
+    if (rc != RF_OK) return rc;
+    if (weights == nullptr || out == nullptr) return fail(RF_ERR_ARG, "null pointer");
+    if (n_elems != rf_clf_weight_elems(cfg))
+        return fail(RF_ERR_SHAPE, "weight blob has " + std::to_string(n_elems) + " elements, expected " +
+                                      std::to_string(rf_clf_weight_elems(cfg)));
+    int32_t sms = 0, major = 0, minor = 0;
+    rc = rf_device_check(device, &sms, &major, &minor);
+    if (rc != RF_OK) return rc;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    rf_clf* s = new rf_clf();
+    s->cfg = *cfg;
+    s->device = device;
+    std::string why;
+    if (!s->blas.load(&why)) {
+        delete s;
+        return fail(RF_ERR_CUDA, why);
+    }
+    auto bail = [&](int code, const std::string& msg) {
+        rf_clf_destroy(s);
+        return fail(code, msg);
+    };
+    if ((e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking)) != cudaSuccess) return bail(RF_ERR_CUDA, "cudaStreamCreate");
+    cudaEventCreate(&s->ev0);
+    cudaEventCreate(&s->ev1);
+    if (s->blas.create(&s->handle) != 0) return bail(RF_ERR_CUDA, "cublasCreate failed");
+    s->blas.set_stream(s->handle, s->stream);
+
+    // split the blob: matrices -> bf16 block, vectors -> f32 block
+    const size_t hid = cfg->hidden, mlp = cfg->mlp, V = cfg->vocab_size, NL = cfg->n_labels;
+    struct Item { size_t n; bool mat; };
+    std::vector<Item> items = {{V * hid, true}, {hid, false}, {hid, false}, {hid * hid, true}, {hid, false}, {NL * hid, true}, {NL, false}};
+    for (int i = 0; i < cfg->n_layers; ++i) {
+        items.push_back({hid, false});
+        items.push_back({3 * hid * hid, true});
+        items.push_back({hid * hid, true});
+        items.push_back({hid, false});
+        items.push_back({2 * mlp * hid, true});
+        items.push_back({hid * mlp, true});
+    }
+    size_t n16 = 0, n32 = 0;
+    for (const Item& it : items) (it.mat ? n16 : n32) += align_up(it.n, 128);
+    s->w16_bytes = n16 * 2;
+    s->w32_bytes = n32 * 4;
+    if ((e = cudaMalloc(&s->w16, s->w16_bytes)) != cudaSuccess) return bail(RF_ERR_CUDA, "cudaMalloc(weights)");
+    if ((e = cudaMalloc(&s->w32, s->w32_bytes)) != cudaSuccess) return bail(RF_ERR_CUDA, "cudaMalloc(weights)");
+    // upload f32 through a staging buffer and cast on the device (same rounding as torch's .to(bfloat16))
+    size_t max_mat = 0;
+    for (const Item& it : items) if (it.mat) max_mat = std::max(max_mat, it.n);
+    float* stage = nullptr;
+    if ((e = cudaMalloc(&stage, max_mat * 4)) != cudaSuccess) return bail(RF_ERR_CUDA, "cudaMalloc(staging)");
+    std::vector<const void*> ptrs;
+    size_t o16 = 0, o32 = 0, src = 0;
+    for (const Item& it : items) {
+        if (it.mat) {
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(s->w16) + o16;
+            cudaMemcpyAsync(stage, weights + src, it.n * 4, cudaMemcpyHostToDevice, s->stream);
+            rf::launch_cast_from_f32(stage, dst, static_cast<long long>(it.n), RF_DTYPE_BF16, s->stream);
+            ptrs.push_back(dst);
+            o16 += align_up(it.n, 128);
+        } else {
+            float* dst = static_cast<float*>(s->w32) + o32;
+            cudaMemcpyAsync(dst, weights + src, it.n * 4, cudaMemcpyHostToDevice, s->stream);
+            ptrs.push_back(dst);
+            o32 += align_up(it.n, 128);
+        }
+        src += it.n;
+    }
+    e = cudaStreamSynchronize(s->stream);
+    cudaFree(stage);
+    if (e != cudaSuccess) return bail(RF_ERR_CUDA, std::string("weight upload: ") + cudaGetErrorString(e));
+    size_t k = 0;
+    s->tok_emb = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+    s->emb_norm = static_cast<const float*>(ptrs[k++]);
+    s->final_norm = static_cast<const float*>(ptrs[k++]);
+    s->head_dense = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+    s->head_norm = static_cast<const float*>(ptrs[k++]);
+    s->cls_w = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+    s->cls_b = static_cast<const float*>(ptrs[k++]);
+    for (int i = 0; i < cfg->n_layers; ++i) {
+        LayerW lw;
+        lw.attn_norm = static_cast<const float*>(ptrs[k++]);
+        lw.wqkv = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+        lw.wo = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+        lw.mlp_norm = static_cast<const float*>(ptrs[k++]);
+        lw.wi = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+        lw.wo2 = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+        s->layers.push_back(lw);
+    }
+    *out = s;
+    return RF_OK;
+}
+
+int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_mask, int64_t B, int64_t S, float* logits) {
+    if (s == nullptr || input_ids == nullptr || logits == nullptr) return fail(RF_ERR_ARG, "null pointer");
+    if (B < 1 || S < 1) return fail(RF_ERR_SHAPE, "B and S must be positive");
+    const rf_clf_config& c = s->cfg;
+    cudaError_t e = cudaSetDevice(s->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    const int64_t rows = B * S;
+    const int hid = c.hidden, H = c.heads, d = c.head_dim;
+    cudaStream_t st = s->stream;
+
+    // attention call template: q/k/v are strided views of the packed [B,S,3,H,d] GEMM output, O is [B,S,H,d]
+    rf_fa_params fp;
+    rf_fa_params_init(&fp);
+    fp.B = B; fp.H = H; fp.S = S; fp.d = d;
+    const int64_t tok = 3ll * hid;
+    const int64_t qs[3] = {S * tok, d, tok};
+    for (int i = 0; i < 3; ++i) fp.q_stride[i] = fp.k_stride[i] = fp.v_stride[i] = qs[i];
+    fp.o_stride[0] = S * static_cast<int64_t>(hid); fp.o_stride[1] = d; fp.o_stride[2] = hid;
+    // workspace: the larger of the global and the local layer's needs (the pointers only matter for alignment checks)
+    size_t ws_need = 0;
+    {
+        rf_fa_params probe = fp;
+        probe.q = probe.k = probe.v = reinterpret_cast<const void*>(uintptr_t{256});
+        probe.out = reinterpret_cast<void*>(uintptr_t{256});
+        probe.pad_bias = attention_mask != nullptr ? reinterpret_cast<const float*>(uintptr_t{256}) : nullptr;
+        size_t need = 0;
+        int rc = rf_fa_fwd_workspace_bytes(&probe, &need);
+        if (rc != RF_OK) return rc;
+        ws_need = need;
+        probe.window_left = c.local_window / 2 - 1;
+        probe.window_right = c.local_window / 2;
+        rc = rf_fa_fwd_workspace_bytes(&probe, &need);
+        if (rc != RF_OK) return rc;
+        ws_need = std::max(ws_need, need);
+    }
+    const Layout L = make_layout(c, B, S, ws_need);
+    if (L.total > s->arena_bytes) {
+        if (s->arena != nullptr) cudaFree(s->arena);
+        s->arena = nullptr;
+        s->arena_bytes = 0;
+        s->rope_S = 0;
+        if ((e = cudaMalloc(&s->arena, L.total)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(arena)");
+        s->arena_bytes = L.total;
+    }
+    uint8_t* base = static_cast<uint8_t*>(s->arena);
+    float* x = reinterpret_cast<float*>(base + L.x);
+    __nv_bfloat16* big = reinterpret_cast<__nv_bfloat16*>(base + L.big);
+    __nv_bfloat16* slot[2] = {reinterpret_cast<__nv_bfloat16*>(base + L.slot[0]), reinterpret_cast<__nv_bfloat16*>(base + L.slot[1])};
+    long long* ids = reinterpret_cast<long long*>(base + L.ids);
+    float* mask = reinterpret_cast<float*>(base + L.mask);
+    float* bias = reinterpret_cast<float*>(base + L.bias);
+    float* dlogits = reinterpret_cast<float*>(base + L.logits);
+    float* rope[4];
+    for (int i = 0; i < 4; ++i) rope[i] = reinterpret_cast<float*>(base + L.rope[i]);
+
+    // RoPE tables (cos, sin) x (global, local), f64 on the host like classifier.py's rope_tables.  The arena
+    // layout depends on (B, S): recompute whenever the shape differs from the previous forward.
+    if (s->rope_S != B * (1ll << 32) + S) {
+        const int half = d / 2;
+        std::vector<float> tab(static_cast<size_t>(S) * half);
+        for (int kind = 0; kind < 2; ++kind) {
+            const double theta = kind == 0 ? c.rope_theta_global : c.rope_theta_local;
+            for (int f = 0; f < 2; ++f) {
+                for (int64_t p = 0; p < S; ++p)
+                    for (int i = 0; i < half; ++i) {
+                        const double ang = static_cast<double>(p) / pow(theta, (2.0 * i) / d);
+                        tab[static_cast<size_t>(p) * half + i] = static_cast<float>(f == 0 ? cos(ang) : sin(ang));
+                    }
+                if ((e = cudaMemcpyAsync(rope[kind * 2 + f], tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+                    return cuda_fail(e, "rope upload");
+                cudaStreamSynchronize(st);  // tab is reused
+            }
+        }
+        s->rope_S = B * (1ll << 32) + S;
+    }
+
+    cudaEventRecord(s->ev0, st);
+    if ((e = cudaMemcpyAsync(ids, input_ids, rows * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "ids upload");
+    const float* pad_bias = nullptr;
+    if (attention_mask != nullptr) {
+        if ((e = cudaMemcpyAsync(mask, attention_mask, rows * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "mask upload");
+        int rc = rf_pad_bias_from_mask(mask, bias, rows, st);  // one shared chain per forward (rewrite.cpp:303-318)
+        if (rc != RF_OK) return rc;
+        pad_bias = bias;
+    }
+    fp.pad_bias = pad_bias;
+
+    auto gemm = [&](const __nv_bfloat16* a, const __nv_bfloat16* w, __nv_bfloat16* y, int64_t m, int n, int k) {
+        // y[m, n] = a[m, k] @ w[n, k]^T, row-major == column-major y^T[n, m] = w^T(k x n)^T * a^T(k x m)
+        const float alpha = 1.f, beta = 0.f;
+        const int r = s->blas.gemm_ex(s->handle, kCublasOpT, kCublasOpN, n, static_cast<int>(m), k, &alpha, w, kCudaR16BF, k, a,
+                                      kCudaR16BF, k, &beta, y, kCudaR16BF, n, kCublasCompute32F, kCublasGemmDefault);
+        return r == 0 ? RF_OK : fail(RF_ERR_CUDA, "cublasGemmEx failed, status " + std::to_string(r));
+    };
+#define RF_TRY(expr)               \
+    do {                           \
+        const int rc_ = (expr);    \
+        if (rc_ != RF_OK) return rc_; \
+    } while (0)
+
+    // embeddings -> f32 stream; h = LN(x) * emb_norm; the stream restarts from the bf16-rounded h
+    embed_gather_kernel<<<static_cast<unsigned>((rows + 3) / 4), 128, 0, st>>>(s->tok_emb, ids, x, rows, hid, c.vocab_size);
+    int cur = 0;  // slot that holds the current bf16 GEMM operand (h)
+    RF_TRY(rf_add_layernorm(x, nullptr, s->emb_norm, slot[cur], rows, hid, c.eps, st));
+    bf16_to_f32_kernel<<<static_cast<unsigned>((rows * hid / 8 + 255) / 256), 256, 0, st>>>(slot[cur], x, rows * hid / 8);
+
+    const int64_t chunk = std::min<int64_t>(rows, c.mlp_chunk_rows);
+    for (int i = 0; i < c.n_layers; ++i) {
+        const LayerW& w = s->layers[i];
+        // (for i > 0 the LN that produced h also added the previous layer's MLP output into x: see the loop tail)
+        __nv_bfloat16* h = slot[cur];
+        RF_TRY(gemm(h, w.wqkv, big, rows, 3 * hid, hid));                       // qkv [rows, 3*hid] == [B,S,3,H,d]
+        const bool glob = i % c.global_every == 0;
+        RF_TRY(rf_rope_qkv(big, rope[glob ? 0 : 2], rope[glob ? 1 : 3], rows, S, H, d, st));
+        __nv_bfloat16* attn = slot[cur ^ 1];
+        fp.q = big;
+        fp.k = big + hid;
+        fp.v = big + 2 * hid;
+        fp.out = attn;
+        fp.window_left = glob ? -1 : c.local_window / 2 - 1;                    // rewrite.cpp:355-361
+        fp.window_right = glob ? -1 : c.local_window / 2;
+        RF_TRY(rf_fa_fwd(&fp, base + L.ws, L.ws_bytes, st));
+        __nv_bfloat16* o = slot[cur];                                            // h is dead
+        RF_TRY(gemm(attn, w.wo, o, rows, hid, hid));
+        __nv_bfloat16* h2 = slot[cur ^ 1];                                       // attn is dead
+        RF_TRY(rf_add_layernorm(x, o, w.mlp_norm, h2, rows, hid, c.eps, st));    // x += attn out; h2 = LN(x)
+        __nv_bfloat16* delta = slot[cur];                                        // o is dead
+        for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+            const int64_t r1 = std::min(rows, r0 + chunk);
+            __nv_bfloat16* wi_out = big;                                         // qkv is dead
+            __nv_bfloat16* act = big + static_cast<size_t>(chunk) * 2 * c.mlp;
+            RF_TRY(gemm(h2 + r0 * hid, w.wi, wi_out, r1 - r0, 2 * c.mlp, hid));
+            RF_TRY(rf_geglu(wi_out, act, r1 - r0, c.mlp, st));
+            RF_TRY(gemm(act, w.wo2, delta + r0 * hid, r1 - r0, hid, c.mlp));
+        }
+        // x += mlp out; h = LN(x) with the next layer's attn_norm (or the final norm)
+        const float* next_norm = i + 1 < c.n_layers ? s->layers[i + 1].attn_norm : s->final_norm;
+        RF_TRY(rf_add_layernorm(x, delta, next_norm, slot[cur ^ 1], rows, hid, c.eps, st));  // h2 is dead
+        cur ^= 1;
+    }
+    clf_head_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(slot[cur], S, hid, s->head_dense, s->head_norm, s->cls_w, s->cls_b,
+                                                              c.n_labels, c.eps, dlogits);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "classifier kernels");
+    if ((e = cudaMemcpyAsync(logits, dlogits, static_cast<size_t>(B) * c.n_labels * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        return cuda_fail(e, "logits download");
+    cudaEventRecord(s->ev1, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "classifier forward");
+    cudaEventElapsedTime(&s->last_ms, s->ev0, s->ev1);
+#undef RF_TRY
+    return RF_OK;
+}
+
+int rf_clf_session_bytes(const rf_clf* s, size_t* weight_bytes, size_t* arena_bytes) {
+    if (s == nullptr) return fail(RF_ERR_ARG, "session is null");
+    if (weight_bytes != nullptr) *weight_bytes = s->w16_bytes + s->w32_bytes;
+    if (arena_bytes != nullptr) *arena_bytes = s->arena_bytes;
+    return RF_OK;
+}
+
+float rf_clf_last_forward_ms(const rf_clf* s) { return s != nullptr ? s->last_ms : 0.f; }
+
+void rf_clf_destroy(rf_clf* s) {
+    if (s == nullptr) return;
+    cudaSetDevice(s->device);
+    if (s->handle != nullptr && s->blas.destroy != nullptr) s->blas.destroy(s->handle);
+    if (s->arena != nullptr) cudaFree(s->arena);
+    if (s->w16 != nullptr) cudaFree(s->w16);
+    if (s->w32 != nullptr) cudaFree(s->w32);
+    if (s->ev0 != nullptr) cudaEventDestroy(s->ev0);
+    if (s->ev1 != nullptr) cudaEventDestroy(s->ev1);
+    if (s->stream != nullptr) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+}  // extern "C"

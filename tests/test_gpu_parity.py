@@ -583,3 +583,58 @@ def test_classifier_session_32k_under_800mb_by_driver(torch_mod, P):
     assert P.fa_memory_bytes(1, cfg.heads, S, cfg.head_dim, 64, 2) == 50528256
     del clf, logits
     torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ native classifier session (rf_clf.h)
+@pytest.mark.parametrize("S,padded", [(512, False), (1024, True), (300, True)])
+def test_native_classifier_session_matches_oracle_and_torch_hosted(torch_mod, P, oracle, S, padded):
+    """rf_clf_forward (ids -> logits in one C call: cuBLAS GEMMs + this library's kernels) against the fp32
+    oracle model (<= 1e-2, identical argmax) and against the torch-hosted Classifier (same kernels, GEMMs
+    through torch): the two differ only by the library GEMM's internal summation order."""
+    torch = torch_mod
+    from oracle_model import oracle_forward
+    from paper_2603_12646_b200.classifier import Classifier, NativeClassifier, init_weights
+    cfg = _small_cfg()
+    weights = init_weights(cfg, seed=4321)
+    g = torch.Generator().manual_seed(S + 1)
+    B = 2
+    ids = torch.randint(0, cfg.vocab_size, (B, S), generator=g)
+    mask = None
+    if padded:
+        mask = torch.ones((B, S))
+        mask[0, S - S // 8:] = 0
+        mask[1, S - 5:] = 0
+    native = NativeClassifier(cfg, weights, device=0)
+    got = native.forward(ids, mask).numpy()
+    again = native.forward(ids, mask).numpy()
+    assert np.array_equal(got, again)  # run-to-run deterministic, arena reused
+    want = oracle_forward(cfg, weights, ids, mask, oracle)
+    hosted = Classifier(cfg, weights, torch.device("cuda:0")).forward(
+        ids.cuda(), mask.cuda() if mask is not None else None).cpu().numpy()
+    print("native", got, "oracle", want, "torch-hosted", hosted, "ms", native.last_forward_ms)
+    assert np.abs(got - want).max() <= 1e-2
+    assert (got.argmax(1) == want.argmax(1)).all()
+    assert np.abs(got - hosted).max() <= 5e-3
+    wbytes, abytes = native.session_bytes()
+    assert wbytes > 0 and abytes > 0
+    # a different shape on the same session (arena regrows / RoPE tables are rebuilt)
+    ids2 = torch.randint(0, cfg.vocab_size, (1, 2 * S), generator=g)
+    got2 = native.forward(ids2).numpy()
+    hosted2 = Classifier(cfg, weights, torch.device("cuda:0")).forward(ids2.cuda()).cpu().numpy()
+    assert np.abs(got2 - hosted2).max() <= 5e-3
+    native.close()
+
+
+def test_native_classifier_errors(torch_mod, P):
+    import ctypes as C
+    from paper_2603_12646_b200 import capi
+    lib = capi.load()
+    c = capi.RfClfConfig()
+    lib.rf_clf_config_default(C.byref(c))
+    assert (c.hidden, c.n_layers, c.heads, c.head_dim, c.mlp, c.local_window) == (768, 22, 12, 64, 1152, 128)
+    h = C.c_void_p()
+    one = (C.c_float * 1)(0.0)
+    assert lib.rf_clf_create(C.byref(c), one, 1, 0, C.byref(h)) == capi.RF_ERR_SHAPE   # wrong blob size
+    c.head_dim = 32
+    c.hidden = 384
+    assert lib.rf_clf_create(C.byref(c), one, 1, 0, C.byref(h)) == capi.RF_ERR_HEAD_DIM
