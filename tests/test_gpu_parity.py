@@ -638,3 +638,22 @@ def test_native_classifier_errors(torch_mod, P):
     c.head_dim = 32
     c.hidden = 384
     assert lib.rf_clf_create(C.byref(c), one, 1, 0, C.byref(h)) == capi.RF_ERR_HEAD_DIM
+
+
+def test_cpp_model_backed_classifier_set(torch_mod):
+    """Builds and runs tests/cpp/classifiers_test.cpp: the model-backed ClassifierSet behind the reference's
+    pluggable classifier interface (include/routefast_b200/classifiers.hpp over rf_clf.h), driven in
+    StreamHandler's call order (stream.cpp:438-443)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "tests", "cpp", "classifiers_test")
+    libdir = os.path.join(root, "paper_2603_12646_b200")
+    src = os.path.join(root, "tests", "cpp", "classifiers_test.cpp")
+    if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
+        cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+        subprocess.run([cxx, "-std=c++17", "-O2", "-I", os.path.join(root, "include"), src, "-o", exe,
+                        "-L", libdir, "-l:librf_fa.so", f"-Wl,-rpath,{libdir}"], check=True)
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(res.stdout[-2000:], res.stderr[-2000:])
+    assert res.returncode == 0 and "all checks passed" in res.stdout
