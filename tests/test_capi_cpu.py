@@ -1,5 +1,5 @@
 """CPU tests of the drop-in boundary: the C-ABI library loads, exports every symbol
-include/rf_fa.h and include/rf_graph.h declare, validates like the reference, and fails loudly without a GPU."""
+include/rf_fa.h, include/rf_graph.h and include/rf_clf.h declare, validates like the reference, and fails loudly without a GPU."""
 import ctypes as C
 import os
 import re
@@ -18,7 +18,7 @@ def lib():
 
 def header_functions():
     names = set()
-    for header in ("rf_fa.h", "rf_graph.h"):
+    for header in ("rf_fa.h", "rf_graph.h", "rf_clf.h"):
         text = open(os.path.join(ROOT, "include", header)).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         names |= set(re.findall(r"\b(rf_[a-z0-9_]+)\s*\(", text))
@@ -154,3 +154,29 @@ def test_memory_model_and_window_attrs():
     assert P.AttentionSpec().effective_scale(64) == 0.125               # attention.cpp:34-36
     assert P.AttentionSpec(scale=0.5).effective_scale(64) == 0.5
     assert (P.kMaskValue, P.kMaskThreshold) == (-65504.0, -30000.0)
+
+
+def test_classifier_session_fails_loudly_without_gpu(lib):
+    """rf_clf.h: config defaults and blob size are host logic; creating a session without a CUDA device is
+    an error (RF_ERR_CUDA), never a CPU path."""
+    import ctypes as C
+    from paper_2603_12646_b200 import capi
+    c = capi.RfClfConfig()
+    lib.rf_clf_config_default(C.byref(c))
+    assert (c.vocab_size, c.hidden, c.n_layers, c.heads, c.head_dim, c.mlp, c.n_labels) == (50368, 768, 22, 12, 64, 1152, 3)
+    per_layer = 768 + 3 * 768 * 768 + 768 * 768 + 768 + 2 * 1152 * 768 + 768 * 1152
+    assert lib.rf_clf_weight_elems(C.byref(c)) == 50368 * 768 + 3 * 768 + 768 * 768 + 3 * 768 + 3 + 22 * per_layer
+    h = C.c_void_p()
+    one = (C.c_float * 1)(0.0)
+    assert lib.rf_clf_create(C.byref(c), one, 1, 0, C.byref(h)) == capi.RF_ERR_SHAPE
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:  # noqa: BLE001
+        has_gpu = False
+    if not has_gpu:
+        c.vocab_size, c.n_layers = 16, 1
+        n = lib.rf_clf_weight_elems(C.byref(c))
+        blob = (C.c_float * n)()
+        assert lib.rf_clf_create(C.byref(c), blob, n, 0, C.byref(h)) == capi.RF_ERR_CUDA
+        assert not h.value
