@@ -168,6 +168,16 @@ int sm_count_or_default() {
     return 148;
 }
 
+// RF_FA_V2=0|1 selects the pipeline variant of the dense kernel at run time (kernel tuning; both are full
+// implementations)
+bool use_v2_kernel() {
+    static const bool use_v2 = [] {
+        const char* env = std::getenv("RF_FA_V2");
+        return env != nullptr ? env[0] == '1' : RF_FA_DEFAULT_V2 != 0;
+    }();
+    return use_v2;
+}
+
 struct Plan {
     int kernel;
     bool local;       // tcgen05 only: the narrow-window kernel takes the call
@@ -225,6 +235,14 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         pl.sched_mode = 1;
         pl.grid = sms;
         pl.part_bytes = align_up(rf::fa_fwd_sm100_partial_bytes(pl.grid), 256);
+        // Padded batch with many pairs per SM: sequence lengths live on the device and usually differ, so equal
+        // slices of the virtual (pair x tile) space would leave the CTAs that drew short sequences idle
+        // (efficiency ~ mean/max length).  Dealing whole pairs round-robin gives every CTA pairs of every
+        // sequence; no pair is split, at the price of a last partial round (<= 1/8 of the work here).
+        if (p->pad_bias != nullptr && p->B > 1 && pl.total_pairs >= 8ll * sms && !use_v2_kernel()) {
+            pl.sched_mode = 2;
+            pl.part_bytes = 0;
+        }
     }
     return pl;
 }
@@ -409,12 +427,7 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
-    // RF_FA_V2=0|1 selects the pipeline variant at run time (kernel tuning; both are full implementations)
-    static const bool use_v2 = [] {
-        const char* env = std::getenv("RF_FA_V2");
-        return env != nullptr ? env[0] == '1' : RF_FA_DEFAULT_V2 != 0;
-    }();
-    cudaError_t e = use_v2 ? rf::launch_fa_fwd_sm100_v2(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream)
+    cudaError_t e = use_v2_kernel() ? rf::launch_fa_fwd_sm100_v2(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream)
                            : rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100 launch");
     return RF_OK;

@@ -169,6 +169,13 @@ __device__ __forceinline__ bool next_item(const FaParams& p, Sched& s, Item& it)
         k1 = static_cast<int>(min(static_cast<long long>(K), k0 + (s.t_end - s.t)));
         s.t += k1 - k0;
         it.kind = k0 > 0 ? kItemHeadPart : (k1 < K ? kItemTailPart : kItemFull);
+    } else if (p.sched_mode == 2) {
+        // whole pairs dealt round-robin: pair blockIdx.x, blockIdx.x + gridDim.x, ...  (s.t counts items)
+        const long long lin = blockIdx.x + s.t * gridDim.x;
+        if (lin >= p.total_pairs) return false;
+        ++s.t;
+        pair_lin = static_cast<int>(lin);
+        it.kind = kItemFull;
     } else {
         if (s.done) return false;
         s.done = true;

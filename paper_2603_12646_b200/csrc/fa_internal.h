@@ -44,7 +44,8 @@ struct FaParams {
     float* l_partial;
     float* debug_scores;
     // work distribution (see fa_fwd_sm100.cu): 0 = one query-tile pair per CTA, 1 = persistent,
-    // statically balanced slices of the flat (pair x key tile) space with in-kernel merge
+    // statically balanced slices of the flat (pair x key tile) space with in-kernel merge, 2 = persistent,
+    // whole pairs dealt round-robin (padded batches: every CTA gets pairs of every sequence)
     int sched_mode;
     int total_pairs;     // B * H * pairs_per_head
     int pairs_per_head;  // ceil(S / 256)

@@ -292,6 +292,20 @@ CASES = {
     "graph_32k_local": lambda: case_time_graph("graph_32k_local", 1, 12, 32768, 63, 64),
     "graph_16k_b4_local": lambda: case_time_graph("graph_16k_b4_local", 4, 12, 16384, 63, 64),
     "graph_8k_global": lambda: case_time_graph("graph_8k_global", 1, 12, 8192, -1, -1),
+    "graph_16k_b4_pad_global": lambda: case_time_graph("graph_16k_b4_pad_global", 4, 12, 16384, -1, -1,
+                                                       lens=[16384, 9000, 12000, 8200], iters=5),
+    "graph_8k_b8_pad_global": lambda: case_time_graph("graph_8k_b8_pad_global", 8, 12, 8192, -1, -1,
+                                                      lens=[8192, 4100, 6000, 5000, 7777, 4500, 8000, 0], iters=5),
+    "graph_8k_b8_allfull": lambda: case_time_graph("graph_8k_b8_allfull", 8, 12, 8192, -1, -1, lens=[8192] * 8, iters=5),
+    "graph_8k_b8_allhalf": lambda: case_time_graph("graph_8k_b8_allhalf", 8, 12, 8192, -1, -1, lens=[4096] * 8, iters=5),
+    "graph_8k_b2_skew": lambda: case_time_graph("graph_8k_b2_skew", 2, 12, 8192, -1, -1, lens=[8192, 4096], iters=5),
+    "cross_4k_b4_pad": lambda: case_cross("cross_4k_b4_pad", 4, 12, 4096, -1, -1, [4096, 2100, 3000, 0]),
+    "graph_8k_b8_skew_nozero": lambda: case_time_graph("graph_8k_b8_skew_nozero", 8, 12, 8192, -1, -1,
+                                                       lens=[8192, 4100, 6000, 5000, 7777, 4500, 8000, 8192], iters=5),
+    "graph_8k_b8_onezero": lambda: case_time_graph("graph_8k_b8_onezero", 8, 12, 8192, -1, -1, lens=[8192] * 7 + [0], iters=5),
+    "graph_8k_b8_skew_aligned": lambda: case_time_graph("graph_8k_b8_skew_aligned", 8, 12, 8192, -1, -1,
+                                                        lens=[8192, 4096, 6016, 4992, 7808, 4480, 8064, 8192], iters=5),
+    "graph_8k_pad_global": lambda: case_time_graph("graph_8k_pad_global", 1, 12, 8192, -1, -1, lens=[7168], iters=10),
     "clf_8k": lambda: case_clf("clf_8k", 8192),
     "clf_8k_pad": lambda: case_clf("clf_8k_pad", 8192, padded=True),
     "clf_16k_b4": lambda: case_clf("clf_16k_b4", 16384, B=4, iters=3),
