@@ -657,3 +657,30 @@ def test_cpp_model_backed_classifier_set(torch_mod):
     res = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(res.stdout[-2000:], res.stderr[-2000:])
     assert res.returncode == 0 and "all checks passed" in res.stdout
+
+
+def test_padded_batch_round_robin_schedule(torch_mod, P, oracle):
+    """Padded batch with >= 8 query-tile pairs per SM takes the round-robin whole-pair schedule (mode 2).
+    B=8, H=12, S=4096 with sequence lengths from 0 to S: checked against the generic SIMT kernel everywhere
+    and against the oracle on single (batch, head) slices."""
+    torch = torch_mod
+    B, H, S, d = 8, 12, 4096, 64
+    lens = [4096, 2100, 0, 3000, 4095, 129, 3584, 1]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v = [(torch.rand((B, H, S, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+    pb = torch.from_numpy(tail_pad(B, S, lens)).cuda()
+    spec = P.AttentionSpec(0.0, -1, -1, pb)
+    st = P.FlashStats()
+    a = P.flash_attention(q, k, v, spec, stats=st)
+    assert st.kernel == "tcgen05" and st.grid_ctas <= 148
+    b = P.flash_attention(q, k, v, spec, kernel="simt")
+    torch.cuda.synchronize()
+    assert not torch.isnan(a).any()
+    assert (a.float() - b.float()).abs().max().item() <= 5e-3
+    assert not a[2].any()  # batch 2 is fully padded: every row has no live key and must be exactly 0
+    a2 = P.flash_attention(q, k, v, spec)
+    assert torch.equal(a, a2)  # bitwise run-to-run
+    for (bb, hh) in ((1, 0), (5, 11), (7, 3)):
+        qs, ks, vs = [t[bb:bb + 1, hh:hh + 1].float().cpu().numpy() for t in (q, k, v)]
+        want = oracle.flash_attention(qs, ks, vs, 0.0, -1, -1, tail_pad(1, S, [lens[bb]]), threads=8)
+        assert np.abs(a[bb:bb + 1, hh:hh + 1].float().cpu().numpy() - want).max() <= TOL
