@@ -209,6 +209,41 @@ def case_time_graph(name, B, H, S, wl, wr, lens=None, iters=20):
          "gbs": 4 * B * H * S * 64 * 2 / ms / 1e6})
 
 
+def case_time_strided(name, S, wl, wr, iters=10):
+    """Same op on [B,H,S,d] tensors and on strided views of a packed [B,S,3,H,d] buffer (the classifier's layout)."""
+    import torch
+    import paper_2603_12646_b200 as P
+    B, H, d = 1, 12, 64
+    g = torch.Generator(device="cuda").manual_seed(3)
+    qkv = (torch.rand((B, S, 3, H, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    views = [qkv[:, :, j].permute(0, 2, 1, 3) for j in range(3)]
+    cont = [v.contiguous() for v in views]
+    out_s = torch.empty((B, S, H, d), device="cuda", dtype=torch.bfloat16).permute(0, 2, 1, 3)
+    out_c = torch.empty((B, H, S, d), device="cuda", dtype=torch.bfloat16)
+    spec = P.AttentionSpec(0.0, wl, wr)
+    res = {}
+    for label, (a, o) in (("contiguous", (cont, out_c)), ("packed_qkv_views", (views, out_s))):
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                P.flash_attention(*a, spec, out=o)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            for _ in range(iters):
+                P.flash_attention(*a, spec, out=o)
+        gr.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            gr.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        res[label + "_us"] = e0.elapsed_time(e1) / (5 * iters) * 1000
+    log({"case": name, "S": S, "wl": wl, **res})
+
+
 def case_clf(name, S, B=1, iters=5, padded=False):
     import torch
     from paper_2603_12646_b200.classifier import Classifier, ClassifierConfig, init_weights
@@ -292,6 +327,9 @@ CASES = {
     "graph_32k_local": lambda: case_time_graph("graph_32k_local", 1, 12, 32768, 63, 64),
     "graph_16k_b4_local": lambda: case_time_graph("graph_16k_b4_local", 4, 12, 16384, 63, 64),
     "graph_8k_global": lambda: case_time_graph("graph_8k_global", 1, 12, 8192, -1, -1),
+    "strided_8k_global": lambda: case_time_strided("strided_8k_global", 8192, -1, -1),
+    "strided_8k_local": lambda: case_time_strided("strided_8k_local", 8192, 63, 64, iters=20),
+    "strided_32k_global": lambda: case_time_strided("strided_32k_global", 32768, -1, -1, iters=3),
     "graph_16k_b4_pad_global": lambda: case_time_graph("graph_16k_b4_pad_global", 4, 12, 16384, -1, -1,
                                                        lens=[16384, 9000, 12000, 8200], iters=5),
     "graph_8k_b8_pad_global": lambda: case_time_graph("graph_8k_b8_pad_global", 8, 12, 8192, -1, -1,
