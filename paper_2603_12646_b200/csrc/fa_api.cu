@@ -235,11 +235,21 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         pl.sched_mode = 1;
         pl.grid = sms;
         pl.part_bytes = align_up(rf::fa_fwd_sm100_partial_bytes(pl.grid), 256);
-        // Padded batch with many pairs per SM: sequence lengths live on the device and usually differ, so equal
-        // slices of the virtual (pair x tile) space would leave the CTAs that drew short sequences idle
-        // (efficiency ~ mean/max length).  Dealing whole pairs round-robin gives every CTA pairs of every
-        // sequence; no pair is split, at the price of a last partial round (<= 1/8 of the work here).
-        if (p->pad_bias != nullptr && p->B > 1 && pl.total_pairs >= 8ll * sms && !use_v2_kernel()) {
+        // Batches with many pairs per SM are dealt round-robin as whole pairs instead (mode 2), for two reasons.
+        // (i) CTAs that run at the same time work on neighbouring pairs, i.e. on a handful of heads whose K/V
+        // stay in L2; contiguous slices put the 148 CTAs on as many different heads at once, and with B*H*S*256 B
+        // of K/V beyond the L2 that costs 5-15 % (B=4, S=16K: 785 -> 899 TFLOP/s).  (ii) With padding, sequence
+        // lengths live on the device and usually differ: equal slices of the virtual (pair x tile) space leave
+        // the CTAs that drew short sequences idle (efficiency ~ mean/max length), round-robin gives every CTA
+        // pairs of every sequence.  No pair is split; the price is a last partial round (<= 1/8 of the work).
+        // A single sequence keeps mode 1 (B=1, S=16K: 921 vs 799 TFLOP/s).
+        // RF_FA_SCHED_MODE=1|2 forces a schedule (developer aid for A/B measurements)
+        static const int forced = [] {
+            const char* env = std::getenv("RF_FA_SCHED_MODE");
+            return env != nullptr ? std::atoi(env) : 0;
+        }();
+        const bool want2 = p->B > 1 && pl.total_pairs >= 8ll * sms;
+        if ((forced == 2 || (forced == 0 && want2)) && !use_v2_kernel()) {
             pl.sched_mode = 2;
             pl.part_bytes = 0;
         }

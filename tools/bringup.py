@@ -327,6 +327,11 @@ CASES = {
     "graph_32k_local": lambda: case_time_graph("graph_32k_local", 1, 12, 32768, 63, 64),
     "graph_16k_b4_local": lambda: case_time_graph("graph_16k_b4_local", 4, 12, 16384, 63, 64),
     "graph_8k_global": lambda: case_time_graph("graph_8k_global", 1, 12, 8192, -1, -1),
+    "graph_16k_global": lambda: case_time_graph("graph_16k_global", 1, 12, 16384, -1, -1, iters=5),
+    "graph_32k_global": lambda: case_time_graph("graph_32k_global", 1, 12, 32768, -1, -1, iters=3),
+    "graph_8k_b8_global": lambda: case_time_graph("graph_8k_b8_global", 8, 12, 8192, -1, -1, iters=3),
+    "graph_16k_b4_global": lambda: case_time_graph("graph_16k_b4_global", 4, 12, 16384, -1, -1, iters=3),
+    "graph_4k_b16_global": lambda: case_time_graph("graph_4k_b16_global", 16, 12, 4096, -1, -1, iters=5),
     "strided_8k_global": lambda: case_time_strided("strided_8k_global", 8192, -1, -1),
     "strided_8k_local": lambda: case_time_strided("strided_8k_local", 8192, 63, 64, iters=20),
     "strided_32k_global": lambda: case_time_strided("strided_32k_global", 32768, -1, -1, iters=3),
