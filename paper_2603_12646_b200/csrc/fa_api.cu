@@ -185,7 +185,8 @@ struct Plan {
     int grid;         // CTAs
     int64_t total_pairs, pairs_per_head, tiles_per_pair;
     size_t bias_bytes, flag_bytes_bias, part_bytes;
-    size_t workspace_bytes() const { return bias_bytes + flag_bytes_bias + part_bytes; }
+    size_t qnorm_bytes, kmax_bytes;  // row-max skip test inputs (dense kernel, S >= 512)
+    size_t workspace_bytes() const { return bias_bytes + flag_bytes_bias + part_bytes + qnorm_bytes + kmax_bytes; }
 };
 
 Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
@@ -229,6 +230,16 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
             tiles = std::min<int64_t>(tiles, (span + rf::kBlockN - 1) / rf::kBlockN + 1);
         }
         pl.tiles_per_pair = std::max<int64_t>(tiles, 1);
+    }
+    // Row-max skip test (fa_fwd_sm100.cu): |q_i| per row and max |k_j| per key tile, O(S) floats.
+    // RF_FA_SKIP_MAX=0 turns it off (A/B measurements).
+    static const bool skip_max_enabled = [] {
+        const char* env = std::getenv("RF_FA_SKIP_MAX");
+        return env == nullptr || env[0] != '0';
+    }();
+    if (skip_max_enabled && p->S >= 512 && !use_v2_kernel()) {
+        pl.qnorm_bytes = align_up(static_cast<size_t>(p->B) * p->H * p->S * sizeof(float), 256);
+        pl.kmax_bytes = align_up(static_cast<size_t>(p->B) * p->H * n_kv_tiles(p->S) * sizeof(float), 256);
     }
     const int sms = sm_count_or_default();
     if (!r.partial && pl.total_pairs > sms) {
@@ -432,6 +443,16 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
         rf::fa_fwd_sm100_partial_carve(ws + pl.bias_bytes + pl.flag_bytes_bias, pl.grid, &f, &flag_ptr, &flag_bytes);
         cudaError_t e = cudaMemsetAsync(flag_ptr, 0, flag_bytes, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(partial flags)");
+    }
+    if (pl.qnorm_bytes > 0) {
+        uint8_t* nb = ws + pl.bias_bytes + pl.flag_bytes_bias + pl.part_bytes;
+        float* qnorm = reinterpret_cast<float*>(nb);
+        float* kmax = reinterpret_cast<float*>(nb + pl.qnorm_bytes);
+        const long long qs[3] = {r.qs[0], r.qs[1], r.qs[2]}, ks[3] = {r.ks[0], r.ks[1], r.ks[2]};
+        cudaError_t e = rf::launch_qk_norms(p->q, p->k, qs, ks, p->dtype, f.B, f.H, f.S, f.n_kv_tiles, qnorm, kmax, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "qk_norms launch");
+        f.qnorm = qnorm;
+        f.kmax = kmax;
     }
     CUtensorMap tmq, tmk, tmv;
     if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;

@@ -35,6 +35,50 @@ __global__ void __launch_bounds__(128) bias_prepare_kernel(const float* __restri
         tile_flags[b * n_kv_tiles + n] = !any_live ? kTileSkip : (all_plain ? kTileFull : kTileMixed);
 }
 
+
+// One CTA per (128-row tile, head, batch), one thread per row: |q_row| and |k_row| from 64 16-bit elements
+// (eight 16-byte loads each); the tile's largest key norm by a block reduction.  Rows >= S count as 0.
+template <bool kBf16>
+__device__ __forceinline__ float row_sumsq64(const void* row) {
+    float acc = 0.f;
+    const uint4* p4 = static_cast<const uint4*>(row);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint4 v = __ldg(p4 + i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 f = kBf16 ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]))
+                                   : __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+            acc = fmaf(f.x, f.x, acc);
+            acc = fmaf(f.y, f.y, acc);
+        }
+    }
+    return acc;
+}
+
+template <bool kBf16>
+__global__ void __launch_bounds__(128) qk_norms_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
+                                                       long long q_sb, long long q_sh, long long q_ss, long long k_sb,
+                                                       long long k_sh, long long k_ss, int H, int S, int n_kv_tiles,
+                                                       float* __restrict__ qnorm, float* __restrict__ kmax) {
+    __shared__ float red[4];
+    const int n = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int row = n * kBlockN + threadIdx.x;
+    float kn = 0.f;
+    if (row < S) {
+        const float qs = row_sumsq64<kBf16>(q + b * q_sb + h * q_sh + row * q_ss);
+        qnorm[(static_cast<size_t>(b) * H + h) * S + row] = sqrtf(qs);
+        kn = sqrtf(row_sumsq64<kBf16>(k + b * k_sb + h * k_sh + row * k_ss));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kn = fmaxf(kn, __shfl_xor_sync(0xffffffffu, kn, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = kn;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        kmax[(static_cast<size_t>(b) * H + h) * n_kv_tiles + n] = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+}
+
 constexpr int kMaxParts = 16;
 struct MergePtrs {
     const float* o[kMaxParts];
@@ -173,6 +217,20 @@ cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias
                                 int n_kv_tiles, cudaStream_t stream) {
     dim3 grid(n_kv_tiles, B);
     bias_prepare_kernel<<<grid, kBlockN, 0, stream>>>(pad_bias, S, bias2, tile_flags, n_kv_tiles);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_qk_norms(const void* q, const void* k, const long long qs[3], const long long ks[3], int dtype, int B,
+                            int H, int S, int n_kv_tiles, float* qnorm, float* kmax, cudaStream_t stream) {
+    dim3 grid(n_kv_tiles, H, B);
+    const uint16_t* q16 = static_cast<const uint16_t*>(q);
+    const uint16_t* k16 = static_cast<const uint16_t*>(k);
+    if (dtype == 0)
+        qk_norms_kernel<true><<<grid, kBlockN, 0, stream>>>(q16, k16, qs[0], qs[1], qs[2], ks[0], ks[1], ks[2], H, S,
+                                                                      n_kv_tiles, qnorm, kmax);
+    else
+        qk_norms_kernel<false><<<grid, kBlockN, 0, stream>>>(q16, k16, qs[0], qs[1], qs[2], ks[0], ks[1], ks[2], H, S,
+                                                               n_kv_tiles, qnorm, kmax);
     return cudaGetLastError();
 }
 

@@ -12,7 +12,7 @@
 //               accumulators in TMEM: three rotating S buffers, cols [0,384) (tile g = 2*t + X of
 //               the A,B,A,B,... sequence uses buffer g % 3, so the next S of a warpgroup is computed
 //               while it is still busy with the current one), O_A [384,448), O_B [448,512);
-//               P (bf16) aliases the first 64 columns of its S buffer.
+//               P (bf16) aliases its S buffer: keys [0,64) in columns [0,32), keys [64,128) in [64,96).
 //   warps 0-7   softmax for tile A, warps 8-15 for tile B.  Two threads share one query row
 //               (key columns [0,64) and [64,128) of the tile; tcgen05.ld 32x32b), so four softmax
 //               warps per SM sub-partition hide each other's MUFU/ALU latencies.  The two halves
@@ -410,13 +410,14 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             };
             // O_X += P * V : B operand V is [key][d] with d contiguous = MN-major, 128B swizzle;
             // 8-key groups 1024 B apart (SBO); a K=16 step advances 16 keys = 2048 B.
-            // A = P from TMEM: 16 bf16 per row per step = 8 packed 32-bit columns.
+            // A = P from TMEM: 16 bf16 per row per step = 8 packed 32-bit columns; keys [0,64) sit in S columns
+            // [0,32), keys [64,128) in S columns [64,96) (each softmax half writes P over its own scores only).
             auto issue_pv = [&](uint32_t x, uint32_t vlo, uint32_t ta, uint32_t acc0) {
                 const uint32_t td = tmem_base + kColO + x * kHeadDim;
                 if (leader) {
 #pragma unroll
                     for (int kk = 0; kk < kBlockN / 16; ++kk)
-                        mma_ts(td, ta + kk * 8, desc(vlo + kk * 128), idesc_pv, kk > 0 ? 1u : acc0);
+                        mma_ts(td, ta + kk * 8 + (kk >= 4 ? 32 : 0), desc(vlo + kk * 128), idesc_pv, kk > 0 ? 1u : acc0);
                 }
                 __syncwarp();
             };
@@ -557,6 +558,15 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 
             float m_ref = -CUDART_INF_F;
             float l_run = 0.f;  // this thread's share of the row sum (its 64 columns of every tile)
+            // scale * log2e * |q_row| (with a rounding margin): times a key tile's largest |k| it bounds every
+            // score of this row in that tile (Cauchy-Schwarz)
+            float qn_c = CUDART_INF_F;
+            const float* kmax_row = nullptr;
+            if (p.kmax != nullptr && active && num_live > 0) {
+                const size_t bh = static_cast<size_t>(b) * p.H + h;
+                qn_c = (row < p.S ? __ldg(p.qnorm + bh * p.S + row) : 0.f) * c * 1.001f;
+                kmax_row = p.kmax + bh * p.n_kv_tiles;
+            }
 
             if (active && num_live > 0) {
                 // key tiles [nf0, nf1) need no window / range predicate for any row of this query tile
@@ -579,6 +589,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     }
                     const int kv0 = n * kBlockN;
                     const uint32_t t_s = t_sbase + sb * kBlockN;
+                    const float kmax_n = kmax_row != nullptr ? __ldg(kmax_row + n) : CUDART_INF_F;  // back before S is
                     // The UMMA warp issues PV_A(i) right after P_A(i) and QK_A(i+2) right after P_B(i)
                     // without looking at the TMA barriers itself: this warp checks that V(i) / K(i+2)
                     // have landed (both were requested tiles ago) while it would otherwise idle waiting
@@ -612,9 +623,18 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     // tile class (warp-uniform): "full" tiles need no per-element predicate
                     const bool full = (n >= nf0) && (n < nf1) && (flag == kTileFull);
 
-                    float my_max;
+                    // Row-max skip (warp-uniform): if no score of this tile can exceed the reference max by more
+                    // than the lazy-rescale threshold -- bound = c |q_row| max_j |k_j| -- the reference stays,
+                    // alpha is 1, and neither the max pass nor the exchange with the other half is needed.
+                    // (m_ref == -inf on an item's first tile, and any NaN, fail the test.)  Both halves of a row
+                    // hold the same m_ref and bound, so their warps decide alike.
+                    const bool skip_max =
+                        full && !__any_sync(0xffffffffu, !(qn_c * kmax_n <= m_ref + kRescaleThreshold));
+                    float my_max = 0.f;
                     float mul;
-                    if (full) {
+                    if (skip_max) {
+                        mul = c;
+                    } else if (full) {
                         float mx[4];
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4) mx[q4] = __uint_as_float(su[q4]);
@@ -658,19 +678,21 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         mul = 1.0f;
                     }
 
-                    // row max over both halves: exchange through smem (double-buffered by tile parity).
-                    // The barrier also orders every S read of this tile before any P write below
-                    // (P aliases the first 64 columns of the S buffer, which belong to half 0).
-                    float* xrow = xrow_base + xpar * (4 * kBlockM);
-                    xrow[hf * kBlockM] = my_max;
-                    RF_STAMP(3);
-                    named_bar_sync(bar_id, kPairThreads);
-                    const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
-                    RF_STAMP(4);
-
-                    // lazy running max: move the reference only when it would grow by > 2^8
-                    const float m_new = (tile_max > m_ref + kRescaleThreshold) ? tile_max : m_ref;
-                    const float alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
+                    // row max over both halves: exchange through smem (double-buffered).  (No S/P hazard is
+                    // tied to this barrier: each half writes P over its own S columns only.)
+                    float m_new = m_ref, alpha = 1.0f;
+                    if (!skip_max) {
+                        float* xrow = xrow_base + xpar * (4 * kBlockM);
+                        xrow[hf * kBlockM] = my_max;
+                        RF_STAMP(3);
+                        named_bar_sync(bar_id, kPairThreads);
+                        const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
+                        RF_STAMP(4);
+                        xpar ^= 1u;
+                        // lazy running max: move the reference only when it would grow by > 2^8
+                        m_new = (tile_max > m_ref + kRescaleThreshold) ? tile_max : m_ref;
+                        alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
+                    }
                     const float neg_m = (m_new == -CUDART_INF_F) ? 0.f : -m_new;
 
                     // P = 2^(s*mul - m).  On full tiles every kEmuEvery-th element pair takes the FMA-pipe
@@ -699,7 +721,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                                 sum2 = fadd2v(sum2, pk2(p0, p1));
                                 pk[u] = pack2<kBf16>(p0, p1);
                             }
-                            tmem_st16(t_s + hf * (kHalfN / 2) + cb * 16, pk);
+                            tmem_st16(t_s + hf * kHalfN + cb * 16, pk);  // each half keeps P inside its own S columns
                         }
                     };
                     if (kPingPong) mbar_wait(turn_mine, tn & 1u);
@@ -719,7 +741,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 
                     // O_X *= alpha for rows whose reference max moved (rare after the first tiles thanks
                     // to the lazy threshold): kept out of line so the hot loop stays compact.
-                    if (it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+                    if (!skip_max && it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
                         const uint32_t vprev = vc + static_cast<uint32_t>(it) - 1u;
                         rescale_o_rows(t_o, alpha, bars_r + 8u * (kBarVEmpty + vprev % kStagesV),
                                        (vprev / kStagesV) & 1u);
@@ -734,7 +756,6 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     ++trace_n;
 #endif
                     ++it;
-                    xpar ^= 1u;
                     // this tile index used buffer sb for this warpgroup and, if the other tile is
                     // active, its neighbour (A = B - 1, B = A + 1 mod 3) for the other warpgroup
                     {

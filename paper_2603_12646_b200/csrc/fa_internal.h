@@ -53,6 +53,11 @@ struct FaParams {
     float* part_o;       // mode 1 workspace: partials of pairs cut between two CTAs
     float* part_ml;
     int* part_flag;
+    // Cauchy-Schwarz bound on the scores of a (query row, key tile): |q_i| * max_j |k_j|.  When it cannot
+    // exceed the running reference max by more than the lazy-rescale threshold, the softmax warps skip the
+    // row-max pass of that tile.  qnorm [B,H,S], kmax [B,H,n_kv_tiles] (qk_norms_kernel); nullptr = off.
+    const float* qnorm;
+    const float* kmax;
 };
 
 struct SimtParams {
@@ -86,6 +91,10 @@ cudaError_t launch_fa_fwd_simt(const SimtParams& p, cudaStream_t stream, int* gr
 
 cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias2, uint8_t* tile_flags,
                                 int n_kv_tiles, cudaStream_t stream);
+// |q_i| per query row and max_j |k_j| per 128-key tile (inputs of the row-max skip test)
+cudaError_t launch_qk_norms(const void* q, const void* k, const long long q_strides[3], const long long k_strides[3],
+                            int dtype, int B, int H, int S, int n_kv_tiles, float* qnorm, float* kmax,
+                            cudaStream_t stream);
 cudaError_t launch_merge(const float* const* o_parts, const float* const* m_parts, const float* const* l_parts,
                          int G, long long rows, int d, void* out, int out_dtype, cudaStream_t stream);
 cudaError_t launch_rescale_partial(float* o_part, float* l_part, const float* m_part, const float* m_star,

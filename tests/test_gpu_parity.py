@@ -684,3 +684,32 @@ def test_padded_batch_round_robin_schedule(torch_mod, P, oracle):
         qs, ks, vs = [t[bb:bb + 1, hh:hh + 1].float().cpu().numpy() for t in (q, k, v)]
         want = oracle.flash_attention(qs, ks, vs, 0.0, -1, -1, tail_pad(1, S, [lens[bb]]), threads=8)
         assert np.abs(a[bb:bb + 1, hh:hh + 1].float().cpu().numpy() - want).max() <= TOL
+
+
+@pytest.mark.parametrize("case", ["growing_keys", "late_outlier", "mixed_query_norms", "orthogonal_big_norms"])
+def test_row_max_skip_is_safe(torch_mod, P, oracle, case):
+    """The dense kernel skips a tile's row-max pass when c*|q_i|*max_j|k_j| cannot exceed the running reference
+    by more than the lazy-rescale threshold.  Inputs built to sit on both sides of that test inside one
+    sequence: key norms that grow along the sequence, a late key that dominates, query rows of very
+    different norms, and large-norm but orthogonal q/k (bound >> actual scores: the slow path must be taken)."""
+    rng = np.random.default_rng(hash(case) % 1000)
+    B, H, S, d = 1, 2, 1024, 64
+    q = rng.uniform(-1, 1, (B, H, S, d)).astype(np.float32)
+    k = rng.uniform(-1, 1, (B, H, S, d)).astype(np.float32)
+    v = rng.uniform(-1, 1, (B, H, S, d)).astype(np.float32)
+    if case == "growing_keys":
+        k *= np.linspace(0.2, 6.0, S, dtype=np.float32)[None, None, :, None]
+    elif case == "late_outlier":
+        k *= 0.3
+        k[:, :, 900] = 8.0 * q[:, :, 17] / np.linalg.norm(q[:, :, 17], axis=-1, keepdims=True)  # aligned with query 17
+    elif case == "mixed_query_norms":
+        q *= np.where(np.arange(S) % 3 == 0, 0.01, np.where(np.arange(S) % 3 == 1, 1.0, 12.0)).astype(np.float32)[None, None, :, None]
+    elif case == "orthogonal_big_norms":
+        q[..., 32:] = 0.0
+        k[..., :32] = 0.0   # every score is exactly 0 although |q||k| is large
+        q *= 20.0
+        k *= 20.0
+    q, k, v = [oracle.round_bf16(t) for t in (q, k, v)]
+    for pb in (None, tail_pad(B, S, [777])):
+        err, got, want = run_case(torch_mod, P, oracle, q, k, v, 0.0, -1, -1, pb, expect_kernel="tcgen05")
+        assert err <= TOL, (case, pb is not None, err)
