@@ -185,7 +185,7 @@ struct Plan {
     int grid;         // CTAs
     int64_t total_pairs, pairs_per_head, tiles_per_pair;
     size_t bias_bytes, flag_bytes_bias, part_bytes;
-    size_t qnorm_bytes, kmax_bytes;  // row-max skip test inputs (dense kernel, S >= 512)
+    size_t qnorm_bytes, kmax_bytes;  // row-max skip test inputs (dense kernel, S >= 1024)
     size_t workspace_bytes() const { return bias_bytes + flag_bytes_bias + part_bytes + qnorm_bytes + kmax_bytes; }
 };
 
@@ -237,7 +237,7 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         const char* env = std::getenv("RF_FA_SKIP_MAX");
         return env == nullptr || env[0] != '0';
     }();
-    if (skip_max_enabled && p->S >= 512 && !use_v2_kernel()) {
+    if (skip_max_enabled && p->S >= 1024 && !use_v2_kernel()) {
         pl.qnorm_bytes = align_up(static_cast<size_t>(p->B) * p->H * p->S * sizeof(float), 256);
         pl.kmax_bytes = align_up(static_cast<size_t>(p->B) * p->H * n_kv_tiles(p->S) * sizeof(float), 256);
     }
