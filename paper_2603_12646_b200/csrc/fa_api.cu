@@ -437,19 +437,27 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     f.total_pairs = static_cast<int>(pl.total_pairs);
     f.pairs_per_head = static_cast<int>(pl.pairs_per_head);
     f.tiles_per_pair = static_cast<int>(pl.tiles_per_pair);
+    int* zero_ptr = nullptr;  // split-pair flag block: zeroed by the norms pre-pass when that runs, else by a memset
+    int zero_words = 0;
     if (pl.sched_mode == 1) {
         void* flag_ptr = nullptr;
         size_t flag_bytes = 0;
         rf::fa_fwd_sm100_partial_carve(ws + pl.bias_bytes + pl.flag_bytes_bias, pl.grid, &f, &flag_ptr, &flag_bytes);
-        cudaError_t e = cudaMemsetAsync(flag_ptr, 0, flag_bytes, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(partial flags)");
+        if (pl.qnorm_bytes > 0) {
+            zero_ptr = static_cast<int*>(flag_ptr);
+            zero_words = static_cast<int>(flag_bytes / sizeof(int));
+        } else {
+            cudaError_t e = cudaMemsetAsync(flag_ptr, 0, flag_bytes, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(partial flags)");
+        }
     }
     if (pl.qnorm_bytes > 0) {
         uint8_t* nb = ws + pl.bias_bytes + pl.flag_bytes_bias + pl.part_bytes;
         float* qnorm = reinterpret_cast<float*>(nb);
         float* kmax = reinterpret_cast<float*>(nb + pl.qnorm_bytes);
         const long long qs[3] = {r.qs[0], r.qs[1], r.qs[2]}, ks[3] = {r.ks[0], r.ks[1], r.ks[2]};
-        cudaError_t e = rf::launch_qk_norms(p->q, p->k, qs, ks, p->dtype, f.B, f.H, f.S, f.n_kv_tiles, qnorm, kmax, stream);
+        cudaError_t e = rf::launch_qk_norms(p->q, p->k, qs, ks, p->dtype, f.B, f.H, f.S, f.n_kv_tiles, qnorm, kmax, zero_ptr,
+                                            zero_words, stream);
         if (e != cudaSuccess) return cuda_fail(e, "qk_norms launch");
         f.qnorm = qnorm;
         f.kmax = kmax;
@@ -459,7 +467,8 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
     cudaError_t e = use_v2_kernel() ? rf::launch_fa_fwd_sm100_v2(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream)
-                           : rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream);
+                           : rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream,
+                                                     /*pdl=*/pl.qnorm_bytes > 0);
     if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100 launch");
     return RF_OK;
 }

@@ -61,9 +61,18 @@ template <bool kBf16>
 __global__ void __launch_bounds__(128) qk_norms_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
                                                        long long q_sb, long long q_sh, long long q_ss, long long k_sb,
                                                        long long k_sh, long long k_ss, int H, int S, int n_kv_tiles,
-                                                       float* __restrict__ qnorm, float* __restrict__ kmax) {
+                                                       float* __restrict__ qnorm, float* __restrict__ kmax,
+                                                       int* __restrict__ zero_ptr, int zero_words) {
     __shared__ float red[4];
+    // let the attention kernel (launched with programmatic stream serialization) start its prologue now; it
+    // waits for this grid to complete before it reads anything written here
+    asm volatile("griddepcontrol.launch_dependents;");
     const int n = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    // this launch also zeroes the split-pair flag block of the persistent schedule (saves a memset node)
+    {
+        const int gtid = ((b * gridDim.y + h) * gridDim.x + n) * kBlockN + threadIdx.x;
+        for (int i = gtid; i < zero_words; i += gridDim.x * gridDim.y * gridDim.z * kBlockN) zero_ptr[i] = 0;
+    }
     const int row = n * kBlockN + threadIdx.x;
     float kn = 0.f;
     if (row < S) {
@@ -221,16 +230,17 @@ cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias
 }
 
 cudaError_t launch_qk_norms(const void* q, const void* k, const long long qs[3], const long long ks[3], int dtype, int B,
-                            int H, int S, int n_kv_tiles, float* qnorm, float* kmax, cudaStream_t stream) {
+                            int H, int S, int n_kv_tiles, float* qnorm, float* kmax, int* zero_ptr, int zero_words,
+                            cudaStream_t stream) {
     dim3 grid(n_kv_tiles, H, B);
     const uint16_t* q16 = static_cast<const uint16_t*>(q);
     const uint16_t* k16 = static_cast<const uint16_t*>(k);
     if (dtype == 0)
         qk_norms_kernel<true><<<grid, kBlockN, 0, stream>>>(q16, k16, qs[0], qs[1], qs[2], ks[0], ks[1], ks[2], H, S,
-                                                                      n_kv_tiles, qnorm, kmax);
+                                                                      n_kv_tiles, qnorm, kmax, zero_ptr, zero_words);
     else
         qk_norms_kernel<false><<<grid, kBlockN, 0, stream>>>(q16, k16, qs[0], qs[1], qs[2], ks[0], ks[1], ks[2], H, S,
-                                                               n_kv_tiles, qnorm, kmax);
+                                                               n_kv_tiles, qnorm, kmax, zero_ptr, zero_words);
     return cudaGetLastError();
 }
 

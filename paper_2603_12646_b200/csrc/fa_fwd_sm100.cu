@@ -281,6 +281,10 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Programmatic dependent launch: everything above overlapped the tail of the previous kernel in the stream
+    // (the norms pre-pass); its results -- and the zeroed flag block -- are visible after this.  A no-op when
+    // the kernel was launched normally.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     Sched sched;
     sched_init(p, sched);
@@ -922,7 +926,7 @@ void fa_fwd_sm100_partial_carve(void* base, int grid, FaParams* p, void** flags,
 }
 
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
-                                const FaParams& p, bool bf16, int grid, cudaStream_t stream) {
+                                const FaParams& p, bool bf16, int grid, cudaStream_t stream, bool pdl) {
     const bool has_bias = p.tile_flags != nullptr;
     void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const FaParams) =
         bf16 ? (has_bias ? fa_fwd_sm100_kernel<true, true> : fa_fwd_sm100_kernel<true, false>)
@@ -930,8 +934,21 @@ cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, 
     const size_t smem = fa_fwd_sm100_smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    kern<<<grid, kThreads, smem, stream>>>(tmq, tmk, tmv, p);
-    return cudaGetLastError();
+    if (!pdl) {
+        kern<<<grid, kThreads, smem, stream>>>(tmq, tmk, tmv, p);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tmq, tmk, tmv, p);
 }
 
 }  // namespace rf

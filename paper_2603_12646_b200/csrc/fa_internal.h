@@ -71,8 +71,10 @@ struct SimtParams {
 };
 
 // launchers (return cudaError_t of the launch)
+// pdl: launch with programmatic stream serialization (the previous kernel in the stream calls
+// griddepcontrol.launch_dependents; this one waits for it after its prologue)
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
-                                const FaParams& p, bool bf16, int grid, cudaStream_t stream);
+                                const FaParams& p, bool bf16, int grid, cudaStream_t stream, bool pdl = false);
 // decoupled-pipeline variant (fa_fwd_sm100_v2.cu): same contract, same workspace layout
 cudaError_t launch_fa_fwd_sm100_v2(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
                                    const FaParams& p, bool bf16, int grid, cudaStream_t stream);
@@ -92,9 +94,11 @@ cudaError_t launch_fa_fwd_simt(const SimtParams& p, cudaStream_t stream, int* gr
 cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias2, uint8_t* tile_flags,
                                 int n_kv_tiles, cudaStream_t stream);
 // |q_i| per query row and max_j |k_j| per 128-key tile (inputs of the row-max skip test)
+// (also zeroes zero_words ints at zero_ptr -- the persistent schedule's flag block -- and triggers
+// programmatic launch of the next kernel in the stream)
 cudaError_t launch_qk_norms(const void* q, const void* k, const long long q_strides[3], const long long k_strides[3],
-                            int dtype, int B, int H, int S, int n_kv_tiles, float* qnorm, float* kmax,
-                            cudaStream_t stream);
+                            int dtype, int B, int H, int S, int n_kv_tiles, float* qnorm, float* kmax, int* zero_ptr,
+                            int zero_words, cudaStream_t stream);
 cudaError_t launch_merge(const float* const* o_parts, const float* const* m_parts, const float* const* l_parts,
                          int G, long long rows, int d, void* out, int out_dtype, cudaStream_t stream);
 cudaError_t launch_rescale_partial(float* o_part, float* l_part, const float* m_part, const float* m_star,
