@@ -98,6 +98,15 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int mode, int rounds, long
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) mma_ss(tmem + (kk & 1) * 128, dsc(a + (kk & 3) * 2), dsc(b + (kk & 3) * 2), i_qk, 1);
                 n += 8;
+            } else if (mode >= 11) {  // 11: SS M64 N128   12: SS M64 N256   13: SS M64 N64   14: SS M64 N128, A MN-major (transposed PV)
+                const uint32_t idesc = mode == 11 ? make_idesc_f16(1, 0, 0, 64, 128)
+                                     : mode == 12 ? make_idesc_f16(1, 0, 0, 64, 256)
+                                     : mode == 13 ? make_idesc_f16(1, 0, 0, 64, 64)
+                                                  : make_idesc_f16(1, 1, 0, 64, 128);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_ss(tmem + (kk & 1) * 256, dsc((mode == 14 ? v : a) + (kk & 3) * (mode == 14 ? 128 : 2)), dsc(b + (kk & 3) * 2), idesc, 1);
+                n += 8;
             } else {  // mode 10: PV only, A and B interleaved MMA by MMA (two P sources, two accumulators)
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
@@ -128,10 +137,10 @@ int main() {
     const int smem = 160 * 1024 + 64 + 1024;
     cudaFuncSetAttribute(rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const char* names[] = {"SS M128 N128 K16 (QK)", "TS M128 N64 K16 (PV)", "SS M128 N256 K16", "SS M128 N64 K16",
-                           "kernel mix 8PV+4QK+8PV+4QK", "TS M128 N128 K16", "TS N64 2 accumulators alternating", "TS N64 4 accumulators", "kernel mix interleaved PV/QK/PV", "SS N128 alternating D", "TS N64 PV_A/PV_B interleaved"};
-    const double macs[] = {128. * 128 * 16, 128. * 64 * 16, 128. * 256 * 16, 128. * 64 * 16, 0, 128. * 128 * 16, 128. * 64 * 16, 128. * 64 * 16, 0, 128. * 128 * 16, 128. * 64 * 16};
+                           "kernel mix 8PV+4QK+8PV+4QK", "TS M128 N128 K16", "TS N64 2 accumulators alternating", "TS N64 4 accumulators", "kernel mix interleaved PV/QK/PV", "SS N128 alternating D", "TS N64 PV_A/PV_B interleaved", "SS M64 N128 K16", "SS M64 N256 K16", "SS M64 N64 K16", "SS M64 N128 K16, A MN-major (transposed PV)"};
+    const double macs[] = {128. * 128 * 16, 128. * 64 * 16, 128. * 256 * 16, 128. * 64 * 16, 0, 128. * 128 * 16, 128. * 64 * 16, 128. * 64 * 16, 0, 128. * 128 * 16, 128. * 64 * 16, 64. * 128 * 16, 64. * 256 * 16, 64. * 64 * 16, 64. * 128 * 16};
     for (int grid : {148})
-        for (int mode = 0; mode < 11; ++mode) {
+        for (int mode = 0; mode < 15; ++mode) {
             for (int rep = 0; rep < 2; ++rep) {
                 rate_kernel<<<grid, 128, smem>>>(mode, 512, d);
                 cudaError_t e = cudaDeviceSynchronize();
