@@ -713,3 +713,28 @@ def test_row_max_skip_is_safe(torch_mod, P, oracle, case):
     for pb in (None, tail_pad(B, S, [777])):
         err, got, want = run_case(torch_mod, P, oracle, q, k, v, 0.0, -1, -1, pb, expect_kernel="tcgen05")
         assert err <= TOL, (case, pb is not None, err)
+
+
+def test_row_max_skip_f16_and_packed_views(torch_mod, P, oracle):
+    """The norms pre-pass honours dtype and strides: f16 inputs, and Q/K/V read in place from a packed
+    [B,S,3,H,d] buffer (S >= 1024, so the pre-pass and the skip test run)."""
+    torch = torch_mod
+    rng = np.random.default_rng(21)
+    B, H, S, d = 2, 3, 1280, 64
+    q, k, v = [rng.uniform(-1, 1, (B, H, S, d)).astype(np.float32) for _ in range(3)]
+    k *= np.linspace(0.5, 3.0, S, dtype=np.float32)[None, None, :, None]
+    q16, k16, v16 = [t.astype(np.float16).astype(np.float32) for t in (q, k, v)]
+    err, _, _ = run_case(torch, P, oracle, q16, k16, v16, 0.0, -1, -1, None, kernel="tcgen05", dtype=torch.float16)
+    assert err <= TOL
+    qb, kb, vb = [oracle.round_bf16(t) for t in (q, k, v)]
+    tq, tk, tv = dev_tensors(torch, (qb, kb, vb))
+    qkv = torch.stack([t.permute(0, 2, 1, 3) for t in (tq, tk, tv)], dim=2).contiguous()  # [B,S,3,H,d]
+    out = torch.empty(B, S, H, d, device="cuda", dtype=torch.bfloat16)
+    pb = tail_pad(B, S, [1280, 1111])
+    st = P.FlashStats()
+    P.flash_attention(qkv[:, :, 0].permute(0, 2, 1, 3), qkv[:, :, 1].permute(0, 2, 1, 3), qkv[:, :, 2].permute(0, 2, 1, 3),
+                      P.AttentionSpec(0.0, -1, -1, torch.from_numpy(pb).cuda()), out=out.permute(0, 2, 1, 3), stats=st)
+    torch.cuda.synchronize()
+    assert st.kernel == "tcgen05"
+    want = oracle.flash_attention(qb, kb, vb, 0.0, -1, -1, pb, threads=8)
+    assert np.abs(out.permute(0, 2, 1, 3).float().cpu().numpy() - want).max() <= TOL
