@@ -686,7 +686,8 @@ def test_padded_batch_round_robin_schedule(torch_mod, P, oracle):
         assert np.abs(a[bb:bb + 1, hh:hh + 1].float().cpu().numpy() - want).max() <= TOL
 
 
-@pytest.mark.parametrize("case", ["growing_keys", "late_outlier", "mixed_query_norms", "orthogonal_big_norms"])
+@pytest.mark.parametrize("case", ["growing_keys", "late_outlier", "mixed_query_norms", "orthogonal_big_norms",
+                                  "late_jump_around_lazy_threshold"])
 def test_row_max_skip_is_safe(torch_mod, P, oracle, case):
     """The dense kernel skips a tile's row-max pass when c*|q_i|*max_j|k_j| cannot exceed the running reference
     by more than the lazy-rescale threshold.  Inputs built to sit on both sides of that test inside one
@@ -709,8 +710,17 @@ def test_row_max_skip_is_safe(torch_mod, P, oracle, case):
         k[..., :32] = 0.0   # every score is exactly 0 although |q||k| is large
         q *= 20.0
         k *= 20.0
+    elif case == "late_jump_around_lazy_threshold":
+        # scores are ~0 for the first 900 keys, then jump by 14..28 log2 units depending on the row: some rows
+        # stay under the lazy-rescale slack (P grows to ~2^19 without a rescale), others cross it
+        u = np.zeros(d, np.float32)
+        u[:4] = 0.5
+        a = np.linspace(1.0, 2.0, S, dtype=np.float32)
+        q = a[None, None, :, None] * u[None, None, None, :] * 8.0 + 0.01 * q
+        k = 0.01 * k
+        k[:, :, 900:] += u[None, None, None, :] * 9.75
     q, k, v = [oracle.round_bf16(t) for t in (q, k, v)]
-    for pb in (None, tail_pad(B, S, [777])):
+    for pb in (None, tail_pad(B, S, [1000 if case == "late_jump_around_lazy_threshold" else 777])):
         err, got, want = run_case(torch_mod, P, oracle, q, k, v, 0.0, -1, -1, pb, expect_kernel="tcgen05")
         assert err <= TOL, (case, pb is not None, err)
 
