@@ -589,10 +589,15 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const uint8_t* flags_row = kHasBias ? p.tile_flags + b * p.n_kv_tiles : nullptr;
                 int sb = g % kSBufs;  // S/P buffer of the current tile
                 int it = 0;
+                // the class byte of a key tile is fetched one tile ahead: with ~10 KB of L1 left beside the
+                // shared-memory carve-out the load is an L2 round trip, which would otherwise sit at the top of
+                // every tile of a padded call
+                uint8_t flag_next = (kHasBias && item.n0 < item.n1) ? flags_row[item.n0] : static_cast<uint8_t>(kTileFull);
                 for (int n = item.n0; n < item.n1; ++n) {
                     uint8_t flag = kTileFull;
                     if (kHasBias) {
-                        flag = flags_row[n];
+                        flag = flag_next;
+                        if (n + 1 < item.n1) flag_next = flags_row[n + 1];
                         if (flag == kTileSkip) continue;
                     }
                     const int kv0 = n * kBlockN;
