@@ -237,7 +237,7 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         const char* env = std::getenv("RF_FA_SKIP_MAX");
         return env == nullptr || env[0] != '0';
     }();
-    if (skip_max_enabled && p->S >= 1024 && !use_v2_kernel()) {
+    if (skip_max_enabled && p->S >= 1024) {
         pl.qnorm_bytes = align_up(static_cast<size_t>(p->B) * p->H * p->S * sizeof(float), 256);
         pl.kmax_bytes = align_up(static_cast<size_t>(p->B) * p->H * n_kv_tiles(p->S) * sizeof(float), 256);
     }
@@ -260,7 +260,7 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
             return env != nullptr ? std::atoi(env) : 0;
         }();
         const bool want2 = p->B > 1 && pl.total_pairs >= 8ll * sms;
-        if ((forced == 2 || (forced == 0 && want2)) && !use_v2_kernel()) {
+        if (forced == 2 || (forced == 0 && want2)) {
             pl.sched_mode = 2;
             pl.part_bytes = 0;
         }
@@ -466,7 +466,8 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
-    cudaError_t e = use_v2_kernel() ? rf::launch_fa_fwd_sm100_v2(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream)
+    cudaError_t e = use_v2_kernel() ? rf::launch_fa_fwd_sm100_v2(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream,
+                                                                 /*pdl=*/pl.qnorm_bytes > 0)
                            : rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream,
                                                      /*pdl=*/pl.qnorm_bytes > 0);
     if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100 launch");

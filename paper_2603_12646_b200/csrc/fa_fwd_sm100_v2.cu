@@ -53,7 +53,8 @@ constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;    // + 128 * X
 constexpr uint32_t kColP = 256;  // + 64 * X
 constexpr uint32_t kColO = 384;  // + 64 * X
-constexpr float kRescaleThreshold = 8.0f;  // log2 units: P <= 2^8 before a rescale is forced
+constexpr float kRescaleThresholdBf16 = 20.0f;  // log2 units: P may reach 2^threshold before a rescale is forced
+constexpr float kRescaleThresholdF16 = 8.0f;    // (see fa_fwd_sm100.cu)
 // The two query tiles have no barrier in common, and left alone their softmax warps drift into
 // phase: all four warps of an SM sub-partition then queue on the MUFU pipe together and idle it
 // together (exp phase 2100 clk instead of 1300, profiles/).  With RF_FA_V2_TURNS the two warps of
@@ -62,6 +63,10 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units: P <= 2^8 before a resc
 #define RF_FA_V2_TURNS 1
 #endif
 constexpr bool kTurns = RF_FA_V2_TURNS != 0;
+#ifndef RF_FA_V2_SKEW
+#define RF_FA_V2_SKEW 0
+#endif
+constexpr long long kSkewClk = RF_FA_V2_SKEW;
 // Developer build only (-DRF_FA_TRACE=1): softmax warps of CTA 0 stamp the SM clock at their phase
 // boundaries into the debug_scores buffer, [16 warps][64 tiles][8 stamps] u32 (tools/trace_phases.py).
 #ifndef RF_FA_TRACE
@@ -153,6 +158,13 @@ __device__ __forceinline__ bool next_item(const FaParams& p, Sched& s, Item& it)
         k1 = static_cast<int>(min(static_cast<long long>(K), k0 + (s.t_end - s.t)));
         s.t += k1 - k0;
         it.kind = k0 > 0 ? kItemHeadPart : (k1 < K ? kItemTailPart : kItemFull);
+    } else if (p.sched_mode == 2) {
+        // whole pairs dealt round-robin: pair blockIdx.x, blockIdx.x + gridDim.x, ...  (s.t counts items)
+        const long long lin = blockIdx.x + s.t * gridDim.x;
+        if (lin >= p.total_pairs) return false;
+        ++s.t;
+        pair_lin = static_cast<int>(lin);
+        it.kind = kItemFull;
     } else {
         if (s.done) return false;
         s.done = true;
@@ -257,6 +269,7 @@ fa_fwd_sm100_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // norms pre-pass (programmatic dependent launch), see fa_fwd_sm100.cu
 
     Sched sched;
     sched_init(p, sched);
@@ -485,6 +498,14 @@ fa_fwd_sm100_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 
             float m_ref = -CUDART_INF_F;
             float l_run = 0.f;  // this thread's share of the row sum (its 64 columns of every tile)
+            // row-max skip test inputs (see fa_fwd_sm100.cu): c * |q_row| and the key tiles' largest |k|
+            float qn_c = CUDART_INF_F;
+            const float* kmax_row = nullptr;
+            if (p.kmax != nullptr && active && num_live > 0) {
+                const size_t bh = static_cast<size_t>(b) * p.H + h;
+                qn_c = (row < p.S ? __ldg(p.qnorm + bh * p.S + row) : 0.f) * c * 1.001f;
+                kmax_row = p.kmax + bh * p.n_kv_tiles;
+            }
 
             if (active && num_live > 0) {
                 // key tiles [nf0, nf1) need no window / range predicate for any row of this query tile
@@ -498,13 +519,25 @@ fa_fwd_sm100_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                 }
                 const uint8_t* flags_row = kHasBias ? p.tile_flags + b * p.n_kv_tiles : nullptr;
                 int it = 0;
+                uint8_t flag_next = (kHasBias && item.n0 < item.n1) ? flags_row[item.n0] : static_cast<uint8_t>(kTileFull);
                 for (int n = item.n0; n < item.n1; ++n) {
                     uint8_t flag = kTileFull;
                     if (kHasBias) {
-                        flag = flags_row[n];
+                        flag = flag_next;  // fetched one tile ahead (an L2 round trip otherwise)
+                        if (n + 1 < item.n1) flag_next = flags_row[n + 1];
                         if (flag == kTileSkip) continue;
                     }
                     const int kv0 = n * kBlockN;
+                    const float kmax_n = kmax_row != nullptr ? __ldg(kmax_row + n) : CUDART_INF_F;
+                    // Phase skew: the two query tiles share no barrier, and started together their four softmax
+                    // warps per sub-partition would queue on the MUFU pipe together and leave it idle together.
+                    // Tile B starts each item about half an exponential pass late; with equal periods the two
+                    // tiles then stay in anti-phase.
+                    if (kSkewClk > 0 && x == 1 && it == 0) {
+                        const long long t_skew = clock64();
+                        while (clock64() - t_skew < kSkewClk) {
+                        }
+                    }
                     RF_STAMP(0);
                     mbar_wait(b_sfull, nt & 1u);
                     tc_fence_after();
@@ -531,9 +564,13 @@ fa_fwd_sm100_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                     // tile class (warp-uniform): "full" tiles need no per-element predicate
                     const bool full = (n >= nf0) && (n < nf1) && (flag == kTileFull);
 
-                    float my_max;
+                    constexpr float kThr = kBf16 ? kRescaleThresholdBf16 : kRescaleThresholdF16;
+                    const bool skip_max = full && !__any_sync(0xffffffffu, !(qn_c * kmax_n <= m_ref + kThr));
+                    float my_max = 0.f;
                     float mul;
-                    if (full) {
+                    if (skip_max) {
+                        mul = c;
+                    } else if (full) {
                         float mx[4];
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4) mx[q4] = __uint_as_float(su[q4]);
@@ -577,22 +614,20 @@ fa_fwd_sm100_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                         mul = 1.0f;
                     }
 
-                    // row max over both halves: exchange through smem (double-buffered by tile parity).
-                    // The barrier also orders every S read of this tile before any P write below
-                    // (P aliases the first 64 columns of the S buffer, which belong to half 0).
-                    float* xrow = xrow_base + xpar * (4 * kBlockM);
-                    xrow[hf * kBlockM] = my_max;
-                    RF_STAMP(3);
-                    named_bar_sync(bar_id, kPairThreads);
-                    const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
-                    // P_X may be overwritten once PV of the previous tile has consumed it: test now, the
-                    // answer is back before the first store needs it
-                    uint32_t p_free = mbar_try_wait(b_pfree, (nt & 1u) ^ 1u);
+                    // row max over both halves: exchange through smem (double-buffered)
+                    float m_new = m_ref, alpha = 1.0f;
+                    if (!skip_max) {
+                        float* xrow = xrow_base + xpar * (4 * kBlockM);
+                        xrow[hf * kBlockM] = my_max;
+                        RF_STAMP(3);
+                        named_bar_sync(bar_id, kPairThreads);
+                        const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
+                        xpar ^= 1u;
+                        // lazy running max: move the reference only when it would grow past the threshold
+                        m_new = (tile_max > m_ref + kThr) ? tile_max : m_ref;
+                        alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
+                    }
                     RF_STAMP(4);
-
-                    // lazy running max: move the reference only when it would grow by > 2^8
-                    const float m_new = (tile_max > m_ref + kRescaleThreshold) ? tile_max : m_ref;
-                    const float alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
                     const float neg_m = (m_new == -CUDART_INF_F) ? 0.f : -m_new;
 
                     // P = 2^(s*mul - m).  On full tiles every kEmuEvery-th element pair takes the FMA-pipe
@@ -600,41 +635,41 @@ fa_fwd_sm100_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                     // edge tiles keep MUFU only, because a masked score (-inf) must give exactly 0.
                     uint64_t sum2 = 0;  // packed (0.f, 0.f)
                     const uint64_t mul2 = bc2(mul), negm2 = bc2(neg_m);
-                    auto exp_store = [&](auto emu_tag) {
+                    // All 32 packed P words of the tile are produced first and stored at the end: P_X is needed
+                    // (P V of the previous tile must have consumed it) only after the exponentials, ~1300 clk
+                    // into the tile, so that wait is never on the critical path.
+                    uint32_t p_free = mbar_try_wait(b_pfree, (nt & 1u) ^ 1u);  // test now, consume after the exps
+                    uint32_t pk[kHalfN / 2];
+                    auto exp_all = [&](auto emu_tag) {
                         constexpr bool kEmu = decltype(emu_tag)::value;
 #pragma unroll
-                        for (int cb = 0; cb < kHalfN / 32; ++cb) {
-                            uint32_t pk[16];
-#pragma unroll
-                            for (int u = 0; u < 16; ++u) {
-                                float p0, p1;
-                                unpk2(ffma2v(pk2(__uint_as_float(su[cb * 32 + 2 * u]),
-                                                 __uint_as_float(su[cb * 32 + 2 * u + 1])),
-                                             mul2, negm2),
-                                      p0, p1);
-                                if (kEmu && (u % (kEmuEvery > 0 ? kEmuEvery : 1)) == (kEmuEvery > 0 ? kEmuEvery - 1 : 0)) {
-                                    exp2_poly2(p0, p1);
-                                } else {
-                                    p0 = ex2(p0);
-                                    p1 = ex2(p1);
-                                }
-                                sum2 = fadd2v(sum2, pk2(p0, p1));
-                                pk[u] = pack2<kBf16>(p0, p1);
+                        for (int u = 0; u < kHalfN / 2; ++u) {
+                            float p0, p1;
+                            unpk2(ffma2v(pk2(__uint_as_float(su[2 * u]), __uint_as_float(su[2 * u + 1])), mul2, negm2), p0, p1);
+                            if (kEmu && ((u % 16) % (kEmuEvery > 0 ? kEmuEvery : 1)) == (kEmuEvery > 0 ? kEmuEvery - 1 : 0)) {
+                                exp2_poly2(p0, p1);
+                            } else {
+                                p0 = ex2(p0);
+                                p1 = ex2(p1);
                             }
-                            tmem_st16(t_p + cb * 16, pk);
+                            sum2 = fadd2v(sum2, pk2(p0, p1));
+                            pk[u] = pack2<kBf16>(p0, p1);
                         }
                     };
-                    if (!p_free) mbar_wait(b_pfree, (nt & 1u) ^ 1u);
-                    tc_fence_after();
                     if (kTurns) mbar_wait(turn_mine, tn & 1u);
                     if (kEmuEvery > 0 && full)
-                        exp_store(std::true_type{});
+                        exp_all(std::true_type{});
                     else
-                        exp_store(std::false_type{});
+                        exp_all(std::false_type{});
                     if (kTurns) {
                         mbar_arrive(turn_other);
                         ++tn;
                     }
+                    if (!p_free) mbar_wait(b_pfree, (nt & 1u) ^ 1u);
+                    tc_fence_after();
+#pragma unroll
+                    for (int cb = 0; cb < kHalfN / 32; ++cb)
+                        tmem_st16(t_p + cb * 16, reinterpret_cast<const uint32_t(&)[16]>(pk[cb * 16]));
                     RF_STAMP(5);
                     float sum0, sum1;
                     unpk2(sum2, sum0, sum1);
@@ -643,7 +678,7 @@ fa_fwd_sm100_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 
                     // O_X *= alpha for rows whose reference max moved (rare after the first tiles thanks
                     // to the lazy threshold): kept out of line so the hot loop stays compact.
-                    if (it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o_rows(t_o, alpha);
+                    if (!skip_max && it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o_rows(t_o, alpha);
                     tc_wait_st();
 #else   // tensor-pipe floor: pass the accumulators straight back
                     tc_fence_before();
@@ -659,7 +694,6 @@ fa_fwd_sm100_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 #endif
                     ++it;
                     ++nt;
-                    xpar ^= 1u;
                 }
             } else if (kTurns) {
                 // tile B sits this item out: pass every turn straight back
@@ -794,7 +828,7 @@ size_t fa_fwd_sm100_v2_smem_bytes() {
 }
 
 cudaError_t launch_fa_fwd_sm100_v2(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
-                                const FaParams& p, bool bf16, int grid, cudaStream_t stream) {
+                                const FaParams& p, bool bf16, int grid, cudaStream_t stream, bool pdl) {
     const bool has_bias = p.tile_flags != nullptr;
     void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const FaParams) =
         bf16 ? (has_bias ? fa_fwd_sm100_v2_kernel<true, true> : fa_fwd_sm100_v2_kernel<true, false>)
@@ -802,8 +836,21 @@ cudaError_t launch_fa_fwd_sm100_v2(const CUtensorMap& tmq, const CUtensorMap& tm
     const size_t smem = fa_fwd_sm100_v2_smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    kern<<<grid, kThreads, smem, stream>>>(tmq, tmk, tmv, p);
-    return cudaGetLastError();
+    if (!pdl) {
+        kern<<<grid, kThreads, smem, stream>>>(tmq, tmk, tmv, p);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tmq, tmk, tmv, p);
 }
 
 }  // namespace rf

@@ -77,7 +77,7 @@ cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, 
                                 const FaParams& p, bool bf16, int grid, cudaStream_t stream, bool pdl = false);
 // decoupled-pipeline variant (fa_fwd_sm100_v2.cu): same contract, same workspace layout
 cudaError_t launch_fa_fwd_sm100_v2(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
-                                   const FaParams& p, bool bf16, int grid, cudaStream_t stream);
+                                   const FaParams& p, bool bf16, int grid, cudaStream_t stream, bool pdl = false);
 // narrow-window kernel (fa_fwd_sm100_local.cu): wl + wr <= 127, one 256-key strip per query tile;
 // reads the raw pad_bias [B,S] (nullable), needs no workspace
 bool fa_fwd_sm100_local_covers(int wl, int wr);
