@@ -57,10 +57,11 @@ constexpr float kRescaleThresholdBf16 = 20.0f;  // log2 units: P may reach 2^thr
 constexpr float kRescaleThresholdF16 = 8.0f;    // (see fa_fwd_sm100.cu)
 // The two query tiles have no barrier in common, and left alone their softmax warps drift into
 // phase: all four warps of an SM sub-partition then queue on the MUFU pipe together and idle it
-// together (exp phase 2100 clk instead of 1300, profiles/).  With RF_FA_V2_TURNS the two warps of
-// tile A and the two of tile B of each sub-partition take strict turns on the exponential phase.
+// together (exp phase 1700-2100 clk instead of 1300, profiles/).  With RF_FA_V2_TURNS=1 the two warps of
+// tile A and the two of tile B of each sub-partition take strict turns on the exponential phase; the
+// hand-over barriers cost more than the collisions (798 vs 871 TFLOP/s at 8K), so the default is off.
 #ifndef RF_FA_V2_TURNS
-#define RF_FA_V2_TURNS 1
+#define RF_FA_V2_TURNS 0
 #endif
 constexpr bool kTurns = RF_FA_V2_TURNS != 0;
 #ifndef RF_FA_V2_SKEW
