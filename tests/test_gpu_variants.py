@@ -1,0 +1,56 @@
+"""GPU tests of the run-time kernel selectors (developer variants that ship in librf_fa.so): each runs in a
+subprocess because the selectors are read once per process.  The checker is the generic SIMT kernel on the
+same inputs plus the oracle on one (batch, head) slice."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SNIPPET = r"""
+import os, sys
+import numpy as np
+import torch
+sys.path.insert(0, os.getcwd())
+import paper_2603_12646_b200 as P
+import oracle as O
+g = torch.Generator(device="cuda").manual_seed(5)
+worst = 0.0
+for (B, H, S, wl, wr, lens) in ((1, 12, 8192, -1, -1, None), (2, 3, 1000, -1, -1, [1000, 640]), (1, 2, 700, 63, 64, [650]),
+                                (8, 12, 4096, -1, -1, [4096, 2100, 0, 3000, 4095, 129, 3584, 1]), (1, 2, 900, 300, 10, None)):
+    q, k, v = [(torch.rand((B, H, S, 64), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+    pb = None
+    if lens is not None:
+        pbn = np.zeros((B, 1, 1, S), np.float32)
+        for b, n in enumerate(lens):
+            pbn[b, 0, 0, n:] = -65504.0
+        pb = torch.from_numpy(pbn).cuda()
+    spec = P.AttentionSpec(0.0, wl, wr, pb)
+    st = P.FlashStats()
+    a = P.flash_attention(q, k, v, spec, stats=st)
+    b_ = P.flash_attention(q, k, v, spec, kernel="simt")
+    torch.cuda.synchronize()
+    assert st.kernel == "tcgen05"
+    err = (a.float() - b_.float()).abs().max().item()
+    assert err <= 5e-3 and not torch.isnan(a).any(), (S, wl, err)
+    worst = max(worst, err)
+    if S <= 1000:
+        want = O.flash_attention(q[:1, :1].float().cpu().numpy(), k[:1, :1].float().cpu().numpy(), v[:1, :1].float().cpu().numpy(),
+                                 0.0, wl, wr, pb[:1].cpu().numpy() if pb is not None else None)
+        assert np.abs(a[:1, :1].float().cpu().numpy() - want).max() <= 2e-2
+print("variant ok", worst)
+"""
+
+
+@pytest.mark.parametrize("env", [{"RF_FA_V2": "1"}, {"RF_FA_LOCAL": "0"}, {"RF_FA_SKIP_MAX": "0"}, {"RF_FA_SCHED_MODE": "1"},
+                                 {"RF_FA_SCHED_MODE": "2"}])
+def test_kernel_selector_variants(env):
+    e = dict(os.environ)
+    e.update(env)
+    res = subprocess.run([sys.executable, "-c", SNIPPET], cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    print(env, res.stdout[-500:], res.stderr[-1500:])
+    assert res.returncode == 0 and "variant ok" in res.stdout
