@@ -52,6 +52,9 @@ typedef struct rf_clf_config {
     int32_t local_window; /* 128 -> (63, 64) */
     int32_t n_labels;     /* 3 */
     int32_t mlp_chunk_rows; /* rows of the MLP intermediate computed at once (bounds activation memory) */
+    int32_t act_dtype;    /* rf_dtype of weights and activations: RF_DTYPE_F16 (default: 11 significant bits keep the
+                             logits within 1e-2 of the fp32 oracle at full depth) or RF_DTYPE_BF16; the residual
+                             stream is f32 either way */
     float rope_theta_global; /* 160000 */
     float rope_theta_local;  /* 10000 */
     float eps;               /* 1e-5 */
@@ -66,7 +69,7 @@ void rf_clf_config_default(rf_clf_config* cfg);
  *   head_norm [hidden], cls_w [n_labels, hidden], cls_b [n_labels],
  *   then per layer: attn_norm [hidden], wqkv [3*hidden, hidden], wo [hidden, hidden], mlp_norm [hidden],
  *   wi [2*mlp, hidden], wo2 [hidden, mlp].
- * Matrices are stored on the device in bf16, norm weights and cls_b in f32. */
+ * Matrices are stored on the device in act_dtype, norm weights and cls_b in f32. */
 size_t rf_clf_weight_elems(const rf_clf_config* cfg);
 
 /* Creates a session on `device` from host f32 weights.  RF_ERR_CUDA without a device / cuBLAS. */

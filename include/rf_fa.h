@@ -199,11 +199,12 @@ int rf_fused_flash_attention_op(const float* const* inputs, const int64_t* const
  *   rf_add_layernorm x (f32 residual stream [rows,n]) += delta (bf16, or NULL); y = LN(x)*w (bf16,
  *                    no bias; y may be NULL to only accumulate).  n % 4 == 0, n <= 4096.
  *   rf_geglu         act[rows,I] = gelu(wi_out[:, :I]) * wi_out[:, I:]   (erf GELU)            */
+/* dtype: rf_dtype of the 16-bit activations, RF_DTYPE_BF16 or RF_DTYPE_F16 */
 int rf_rope_qkv(void* qkv, const float* cos_table, const float* sin_table, int64_t tokens, int64_t S, int64_t H,
-                int64_t d, void* stream);
+                int64_t d, int32_t dtype, void* stream);
 int rf_add_layernorm(float* x, const void* delta, const float* w, void* y, int64_t rows, int64_t n, float eps,
-                     void* stream);
-int rf_geglu(const void* wi_out, void* act, int64_t rows, int64_t I, void* stream);
+                     int32_t dtype, void* stream);
+int rf_geglu(const void* wi_out, void* act, int64_t rows, int64_t I, int32_t dtype, void* stream);
 
 /* Memory model (attention.cpp:244-252). */
 uint64_t rf_mask_memory_bytes(uint64_t batch, uint64_t heads, uint64_t seq_len, uint64_t bytes_per_element);

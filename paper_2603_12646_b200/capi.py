@@ -36,7 +36,7 @@ class RfClfConfig(C.Structure):
     _fields_ = [
         ("vocab_size", C.c_int32), ("hidden", C.c_int32), ("n_layers", C.c_int32), ("heads", C.c_int32),
         ("head_dim", C.c_int32), ("mlp", C.c_int32), ("global_every", C.c_int32), ("local_window", C.c_int32),
-        ("n_labels", C.c_int32), ("mlp_chunk_rows", C.c_int32), ("rope_theta_global", C.c_float),
+        ("n_labels", C.c_int32), ("mlp_chunk_rows", C.c_int32), ("act_dtype", C.c_int32), ("rope_theta_global", C.c_float),
         ("rope_theta_local", C.c_float), ("eps", C.c_float),
     ]
 
@@ -118,9 +118,9 @@ def load(build_if_missing: bool = True):
                                    C.POINTER(i64), i64, i32, i32, C.POINTER(RfFaStats)]
     lib.rf_fused_flash_attention_op.argtypes = [C.POINTER(f32p), C.POINTER(C.POINTER(i64)), C.POINTER(i32), i32,
                                                 i32, C.c_double, i32, i64, i32, i64, f32p, i32]
-    lib.rf_rope_qkv.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp]
-    lib.rf_add_layernorm.argtypes = [vp, vp, vp, vp, i64, i64, C.c_float, vp]
-    lib.rf_geglu.argtypes = [vp, vp, i64, i64, vp]
+    lib.rf_rope_qkv.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp]
+    lib.rf_add_layernorm.argtypes = [vp, vp, vp, vp, i64, i64, C.c_float, i32, vp]
+    lib.rf_geglu.argtypes = [vp, vp, i64, i64, i32, vp]
     lib.rf_mask_memory_bytes.restype = u64
     lib.rf_mask_memory_bytes.argtypes = [u64] * 4
     lib.rf_fa_memory_bytes.restype = u64

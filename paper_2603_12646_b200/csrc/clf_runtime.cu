@@ -22,6 +22,7 @@
 // cuBLAS is resolved with dlopen/dlsym (five entry points) so that librf_fa.so itself has no link-time
 // dependency on it; a missing library is RF_ERR_CUDA at session creation, never a fallback.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <math.h>
@@ -53,6 +54,7 @@ typedef int (*cublasGemmEx_fn)(cublasHandle_t, int, int, int, int, int, const vo
                                int, int, const void*, void*, int, int, int, int);
 constexpr int kCublasOpN = 0, kCublasOpT = 1;
 constexpr int kCudaR16BF = 14;          // CUDA_R_16BF
+constexpr int kCudaR16F = 2;            // CUDA_R_16F
 constexpr int kCublasCompute32F = 68;   // CUBLAS_COMPUTE_32F
 constexpr int kCublasGemmDefault = -1;  // CUBLAS_GEMM_DEFAULT
 
@@ -87,71 +89,81 @@ struct Cublas {
 
 // ---- kernels of the session that the operator library did not have yet ----
 
+// 16-bit activation / weight element (bf16 or f16) <-> float
+template <bool kBf16>
+__device__ __forceinline__ float2 pair_to_float2(uint32_t w) {
+    if (kBf16) return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+    return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
+template <bool kBf16>
+__device__ __forceinline__ float elem_to_float(uint16_t h) {
+    if (kBf16) return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(&h));
+    return __half2float(*reinterpret_cast<const __half*>(&h));
+}
+template <bool kBf16>
+__device__ __forceinline__ float round_to_16(float v) {
+    if (kBf16) return __bfloat162float(__float2bfloat16_rn(v));
+    return __half2float(__float2half_rn(v));
+}
+
 // x[row, :] = float(tok_emb[ids[row], :]); one warp per row, 16-byte loads.
-__global__ void __launch_bounds__(128) embed_gather_kernel(const __nv_bfloat16* __restrict__ emb,
-                                                           const long long* __restrict__ ids, float* __restrict__ x,
-                                                           long long rows, int hidden, int vocab) {
+template <bool kBf16>
+__global__ void __launch_bounds__(128) embed_gather_kernel(const uint16_t* __restrict__ emb, const long long* __restrict__ ids,
+                                                           float* __restrict__ x, long long rows, int hidden, int vocab) {
     const long long row = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
     if (row >= rows) return;
     const int lane = threadIdx.x & 31;
     long long id = ids[row];
     id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
-    const __nv_bfloat16* src = emb + id * hidden;
+    const uint16_t* src = emb + id * hidden;
     float* dst = x + row * hidden;
     for (int c = lane * 8; c < hidden; c += 256) {
         const uint4 v = *reinterpret_cast<const uint4*>(src + c);
-        const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&v);
-        float4 a, b;
-        float2 t = __bfloat1622float2(v2[0]); a.x = t.x; a.y = t.y;
-        t = __bfloat1622float2(v2[1]); a.z = t.x; a.w = t.y;
-        t = __bfloat1622float2(v2[2]); b.x = t.x; b.y = t.y;
-        t = __bfloat1622float2(v2[3]); b.z = t.x; b.w = t.y;
-        *reinterpret_cast<float4*>(dst + c) = a;
-        *reinterpret_cast<float4*>(dst + c + 4) = b;
+        const float2 t0 = pair_to_float2<kBf16>(v.x), t1 = pair_to_float2<kBf16>(v.y);
+        const float2 t2 = pair_to_float2<kBf16>(v.z), t3 = pair_to_float2<kBf16>(v.w);
+        *reinterpret_cast<float4*>(dst + c) = make_float4(t0.x, t0.y, t1.x, t1.y);
+        *reinterpret_cast<float4*>(dst + c + 4) = make_float4(t2.x, t2.y, t3.x, t3.y);
     }
 }
 
-// x (f32) = float(h (bf16)): the stream restarts from the bf16-rounded LN(embeddings), as classifier.py does
-__global__ void __launch_bounds__(256) bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ h, float* __restrict__ x,
-                                                          long long n8) {
+// x (f32) = float(h (16-bit)): the stream restarts from the rounded LN(embeddings), as classifier.py does
+template <bool kBf16>
+__global__ void __launch_bounds__(256) half_to_f32_kernel(const uint16_t* __restrict__ h, float* __restrict__ x, long long n8) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n8) return;
     const uint4 v = reinterpret_cast<const uint4*>(h)[i];
-    const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&v);
-    float4 a, b;
-    float2 t = __bfloat1622float2(v2[0]); a.x = t.x; a.y = t.y;
-    t = __bfloat1622float2(v2[1]); a.z = t.x; a.w = t.y;
-    t = __bfloat1622float2(v2[2]); b.x = t.x; b.y = t.y;
-    t = __bfloat1622float2(v2[3]); b.z = t.x; b.w = t.y;
-    reinterpret_cast<float4*>(x)[2 * i] = a;
-    reinterpret_cast<float4*>(x)[2 * i + 1] = b;
+    const float2 t0 = pair_to_float2<kBf16>(v.x), t1 = pair_to_float2<kBf16>(v.y);
+    const float2 t2 = pair_to_float2<kBf16>(v.z), t3 = pair_to_float2<kBf16>(v.w);
+    reinterpret_cast<float4*>(x)[2 * i] = make_float4(t0.x, t0.y, t1.x, t1.y);
+    reinterpret_cast<float4*>(x)[2 * i + 1] = make_float4(t2.x, t2.y, t3.x, t3.y);
 }
 
-// Classification head for one sequence per CTA: pooled = hf[b, 0, :] (CLS); t = gelu(bf16(pooled Wd^T));
+// Classification head for one sequence per CTA: pooled = hf[b, 0, :] (CLS); t = gelu(round16(pooled Wd^T));
 // t = LN(t) * head_norm; logits = t Wc^T + b.  hidden <= 1024.
-__global__ void __launch_bounds__(256) clf_head_kernel(const __nv_bfloat16* __restrict__ hf, long long S, int hidden,
-                                                       const __nv_bfloat16* __restrict__ wd, const float* __restrict__ head_norm,
-                                                       const __nv_bfloat16* __restrict__ wc, const float* __restrict__ bc,
+template <bool kBf16>
+__global__ void __launch_bounds__(256) clf_head_kernel(const uint16_t* __restrict__ hf, long long S, int hidden,
+                                                       const uint16_t* __restrict__ wd, const float* __restrict__ head_norm,
+                                                       const uint16_t* __restrict__ wc, const float* __restrict__ bc,
                                                        int n_labels, float eps, float* __restrict__ logits) {
     __shared__ float pooled[1024];
     __shared__ float t[1024];
     __shared__ float red[2][8];
     const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const __nv_bfloat16* row = hf + static_cast<long long>(b) * S * hidden;
-    for (int c = tid; c < hidden; c += blockDim.x) pooled[c] = __bfloat162float(row[c]);
+    const uint16_t* row = hf + static_cast<long long>(b) * S * hidden;
+    for (int c = tid; c < hidden; c += blockDim.x) pooled[c] = elem_to_float<kBf16>(row[c]);
     __syncthreads();
     // dense: one warp per output feature, lanes stride over the input features
     for (int j = warp; j < hidden; j += 8) {
-        const __nv_bfloat16* wr = wd + static_cast<long long>(j) * hidden;
+        const uint16_t* wr = wd + static_cast<long long>(j) * hidden;
         float acc = 0.f;
         for (int c = lane * 2; c < hidden; c += 64) {
-            const float2 w2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(wr + c));
+            const float2 w2 = pair_to_float2<kBf16>(*reinterpret_cast<const uint32_t*>(wr + c));
             acc += pooled[c] * w2.x + pooled[c + 1] * w2.y;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) {
-            const float v = __bfloat162float(__float2bfloat16_rn(acc));  // the GEMM output is bf16
+            const float v = round_to_16<kBf16>(acc);  // the GEMM output is 16-bit
             t[j] = 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
         }
     }
@@ -177,9 +189,9 @@ __global__ void __launch_bounds__(256) clf_head_kernel(const __nv_bfloat16* __re
     for (int c = tid; c < hidden; c += blockDim.x) pooled[c] = (t[c] - mean) * rstd * head_norm[c];
     __syncthreads();
     for (int k = warp; k < n_labels; k += 8) {
-        const __nv_bfloat16* wr = wc + static_cast<long long>(k) * hidden;
+        const uint16_t* wr = wc + static_cast<long long>(k) * hidden;
         float acc = 0.f;
-        for (int c = lane; c < hidden; c += 32) acc += pooled[c] * __bfloat162float(wr[c]);
+        for (int c = lane; c < hidden; c += 32) acc += pooled[c] * elem_to_float<kBf16>(wr[c]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) logits[b * n_labels + k] = acc + bc[k];
@@ -190,11 +202,11 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct LayerW {
     const float* attn_norm;
-    const __nv_bfloat16* wqkv;
-    const __nv_bfloat16* wo;
+    const uint16_t* wqkv;
+    const uint16_t* wo;
     const float* mlp_norm;
-    const __nv_bfloat16* wi;
-    const __nv_bfloat16* wo2;
+    const uint16_t* wi;
+    const uint16_t* wo2;
 };
 
 }  // namespace
@@ -210,7 +222,7 @@ struct rf_clf {
     void* w16 = nullptr;
     void* w32 = nullptr;
     size_t w16_bytes = 0, w32_bytes = 0;
-    const __nv_bfloat16 *tok_emb = nullptr, *head_dense = nullptr, *cls_w = nullptr;
+    const uint16_t *tok_emb = nullptr, *head_dense = nullptr, *cls_w = nullptr;
     const float *emb_norm = nullptr, *final_norm = nullptr, *head_norm = nullptr, *cls_b = nullptr;
     std::vector<LayerW> layers;
     // activation arena
@@ -266,7 +278,8 @@ int check_cfg(const rf_clf_config* c) {
     if (c->hidden != c->heads * c->head_dim) return fail(RF_ERR_SHAPE, "hidden must equal heads * head_dim");
     if (c->head_dim != 64) return fail(RF_ERR_HEAD_DIM, "the classifier session needs head_dim 64");
     if (c->hidden % 8 || c->hidden > 1024 || c->mlp % 8 || c->n_layers < 1 || c->vocab_size < 1 || c->n_labels < 1 ||
-        c->global_every < 1 || c->local_window < 2 || c->mlp_chunk_rows < 1)
+        c->global_every < 1 || c->local_window < 2 || c->mlp_chunk_rows < 1 ||
+        (c->act_dtype != RF_DTYPE_F16 && c->act_dtype != RF_DTYPE_BF16))
         return fail(RF_ERR_ARG, "bad classifier config");
     return RF_OK;
 }
@@ -287,6 +300,7 @@ void rf_clf_config_default(rf_clf_config* c) {
     c->local_window = 128;
     c->n_labels = 3;
     c->mlp_chunk_rows = 8192;
+    c->act_dtype = RF_DTYPE_F16;
     c->rope_theta_global = 160000.0f;
     c->rope_theta_local = 10000.0f;
     c->eps = 1e-5f;
@@ -361,9 +375,9 @@ int rf_clf_create(const rf_clf_config* cfg, const float* weights, size_t n_elems
     size_t o16 = 0, o32 = 0, src = 0;
     for (const Item& it : items) {
         if (it.mat) {
-            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(s->w16) + o16;
+            uint16_t* dst = static_cast<uint16_t*>(s->w16) + o16;
             cudaMemcpyAsync(stage, weights + src, it.n * 4, cudaMemcpyHostToDevice, s->stream);
-            rf::launch_cast_from_f32(stage, dst, static_cast<long long>(it.n), RF_DTYPE_BF16, s->stream);
+            rf::launch_cast_from_f32(stage, dst, static_cast<long long>(it.n), cfg->act_dtype, s->stream);
             ptrs.push_back(dst);
             o16 += align_up(it.n, 128);
         } else {
@@ -378,21 +392,21 @@ int rf_clf_create(const rf_clf_config* cfg, const float* weights, size_t n_elems
     cudaFree(stage);
     if (e != cudaSuccess) return bail(RF_ERR_CUDA, std::string("weight upload: ") + cudaGetErrorString(e));
     size_t k = 0;
-    s->tok_emb = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+    s->tok_emb = static_cast<const uint16_t*>(ptrs[k++]);
     s->emb_norm = static_cast<const float*>(ptrs[k++]);
     s->final_norm = static_cast<const float*>(ptrs[k++]);
-    s->head_dense = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+    s->head_dense = static_cast<const uint16_t*>(ptrs[k++]);
     s->head_norm = static_cast<const float*>(ptrs[k++]);
-    s->cls_w = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+    s->cls_w = static_cast<const uint16_t*>(ptrs[k++]);
     s->cls_b = static_cast<const float*>(ptrs[k++]);
     for (int i = 0; i < cfg->n_layers; ++i) {
         LayerW lw;
         lw.attn_norm = static_cast<const float*>(ptrs[k++]);
-        lw.wqkv = static_cast<const __nv_bfloat16*>(ptrs[k++]);
-        lw.wo = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+        lw.wqkv = static_cast<const uint16_t*>(ptrs[k++]);
+        lw.wo = static_cast<const uint16_t*>(ptrs[k++]);
         lw.mlp_norm = static_cast<const float*>(ptrs[k++]);
-        lw.wi = static_cast<const __nv_bfloat16*>(ptrs[k++]);
-        lw.wo2 = static_cast<const __nv_bfloat16*>(ptrs[k++]);
+        lw.wi = static_cast<const uint16_t*>(ptrs[k++]);
+        lw.wo2 = static_cast<const uint16_t*>(ptrs[k++]);
         s->layers.push_back(lw);
     }
     *out = s;
@@ -412,6 +426,8 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
     // attention call template: q/k/v are strided views of the packed [B,S,3,H,d] GEMM output, O is [B,S,H,d]
     rf_fa_params fp;
     rf_fa_params_init(&fp);
+    fp.dtype = c.act_dtype;
+    fp.out_dtype = c.act_dtype;
     fp.B = B; fp.H = H; fp.S = S; fp.d = d;
     const int64_t tok = 3ll * hid;
     const int64_t qs[3] = {S * tok, d, tok};
@@ -448,8 +464,8 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
     }
     uint8_t* base = static_cast<uint8_t*>(s->arena);
     float* x = reinterpret_cast<float*>(base + L.x);
-    __nv_bfloat16* big = reinterpret_cast<__nv_bfloat16*>(base + L.big);
-    __nv_bfloat16* slot[2] = {reinterpret_cast<__nv_bfloat16*>(base + L.slot[0]), reinterpret_cast<__nv_bfloat16*>(base + L.slot[1])};
+    uint16_t* big = reinterpret_cast<uint16_t*>(base + L.big);
+    uint16_t* slot[2] = {reinterpret_cast<uint16_t*>(base + L.slot[0]), reinterpret_cast<uint16_t*>(base + L.slot[1])};
     long long* ids = reinterpret_cast<long long*>(base + L.ids);
     float* mask = reinterpret_cast<float*>(base + L.mask);
     float* bias = reinterpret_cast<float*>(base + L.bias);
@@ -529,11 +545,12 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
         if (rc != RF_OK) return rc;
     }
 
-    auto gemm = [&](const __nv_bfloat16* a, const __nv_bfloat16* w, __nv_bfloat16* y, int64_t m, int n, int k) {
+    auto gemm = [&](const uint16_t* a, const uint16_t* w, uint16_t* y, int64_t m, int n, int k) {
         // y[m, n] = a[m, k] @ w[n, k]^T, row-major == column-major y^T[n, m] = w^T(k x n)^T * a^T(k x m)
         const float alpha = 1.f, beta = 0.f;
-        const int r = s->blas.gemm_ex(s->handle, kCublasOpT, kCublasOpN, n, static_cast<int>(m), k, &alpha, w, kCudaR16BF, k, a,
-                                      kCudaR16BF, k, &beta, y, kCudaR16BF, n, kCublasCompute32F, kCublasGemmDefault);
+        const int ty = c.act_dtype == RF_DTYPE_BF16 ? kCudaR16BF : kCudaR16F;
+        const int r = s->blas.gemm_ex(s->handle, kCublasOpT, kCublasOpN, n, static_cast<int>(m), k, &alpha, w, ty, k, a, ty, k,
+                                      &beta, y, ty, n, kCublasCompute32F, kCublasGemmDefault);
         return r == 0 ? RF_OK : fail(RF_ERR_CUDA, "cublasGemmEx failed, status " + std::to_string(r));
     };
 #define RF_TRY(expr)               \
@@ -543,20 +560,24 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
     } while (0)
 
     // embeddings -> f32 stream; h = LN(x) * emb_norm; the stream restarts from the bf16-rounded h
-    embed_gather_kernel<<<static_cast<unsigned>((rows + 3) / 4), 128, 0, st>>>(s->tok_emb, ids, x, rows, hid, c.vocab_size);
+    const bool bf = c.act_dtype == RF_DTYPE_BF16;
+    const int dt = c.act_dtype;
+    if (bf) embed_gather_kernel<true><<<static_cast<unsigned>((rows + 3) / 4), 128, 0, st>>>(s->tok_emb, ids, x, rows, hid, c.vocab_size);
+    else embed_gather_kernel<false><<<static_cast<unsigned>((rows + 3) / 4), 128, 0, st>>>(s->tok_emb, ids, x, rows, hid, c.vocab_size);
     int cur = 0;  // slot that holds the current bf16 GEMM operand (h)
-    RF_TRY(rf_add_layernorm(x, nullptr, s->emb_norm, slot[cur], rows, hid, c.eps, st));
-    bf16_to_f32_kernel<<<static_cast<unsigned>((rows * hid / 8 + 255) / 256), 256, 0, st>>>(slot[cur], x, rows * hid / 8);
+    RF_TRY(rf_add_layernorm(x, nullptr, s->emb_norm, slot[cur], rows, hid, c.eps, dt, st));
+    if (bf) half_to_f32_kernel<true><<<static_cast<unsigned>((rows * hid / 8 + 255) / 256), 256, 0, st>>>(slot[cur], x, rows * hid / 8);
+    else half_to_f32_kernel<false><<<static_cast<unsigned>((rows * hid / 8 + 255) / 256), 256, 0, st>>>(slot[cur], x, rows * hid / 8);
 
     const int64_t chunk = std::min<int64_t>(rows, c.mlp_chunk_rows);
     for (int i = 0; i < c.n_layers; ++i) {
         const LayerW& w = s->layers[i];
         // (for i > 0 the LN that produced h also added the previous layer's MLP output into x: see the loop tail)
-        __nv_bfloat16* h = slot[cur];
+        uint16_t* h = slot[cur];
         RF_TRY(gemm(h, w.wqkv, big, rows, 3 * hid, hid));                       // qkv [rows, 3*hid] == [B,S,3,H,d]
         const bool glob = i % c.global_every == 0;
-        RF_TRY(rf_rope_qkv(big, rope[glob ? 0 : 2], rope[glob ? 1 : 3], rows, S, H, d, st));
-        __nv_bfloat16* attn = slot[cur ^ 1];
+        RF_TRY(rf_rope_qkv(big, rope[glob ? 0 : 2], rope[glob ? 1 : 3], rows, S, H, d, dt, st));
+        uint16_t* attn = slot[cur ^ 1];
         fp.q = big;
         fp.k = big + hid;
         fp.v = big + 2 * hid;
@@ -564,26 +585,30 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
         fp.window_left = glob ? -1 : c.local_window / 2 - 1;                    // rewrite.cpp:355-361
         fp.window_right = glob ? -1 : c.local_window / 2;
         RF_TRY(rf_fa_fwd(&fp, base + L.ws, L.ws_bytes, st));
-        __nv_bfloat16* o = slot[cur];                                            // h is dead
+        uint16_t* o = slot[cur];                                            // h is dead
         RF_TRY(gemm(attn, w.wo, o, rows, hid, hid));
-        __nv_bfloat16* h2 = slot[cur ^ 1];                                       // attn is dead
-        RF_TRY(rf_add_layernorm(x, o, w.mlp_norm, h2, rows, hid, c.eps, st));    // x += attn out; h2 = LN(x)
-        __nv_bfloat16* delta = slot[cur];                                        // o is dead
+        uint16_t* h2 = slot[cur ^ 1];                                       // attn is dead
+        RF_TRY(rf_add_layernorm(x, o, w.mlp_norm, h2, rows, hid, c.eps, dt, st));    // x += attn out; h2 = LN(x)
+        uint16_t* delta = slot[cur];                                        // o is dead
         for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
             const int64_t r1 = std::min(rows, r0 + chunk);
-            __nv_bfloat16* wi_out = big;                                         // qkv is dead
-            __nv_bfloat16* act = big + static_cast<size_t>(chunk) * 2 * c.mlp;
+            uint16_t* wi_out = big;                                         // qkv is dead
+            uint16_t* act = big + static_cast<size_t>(chunk) * 2 * c.mlp;
             RF_TRY(gemm(h2 + r0 * hid, w.wi, wi_out, r1 - r0, 2 * c.mlp, hid));
-            RF_TRY(rf_geglu(wi_out, act, r1 - r0, c.mlp, st));
+            RF_TRY(rf_geglu(wi_out, act, r1 - r0, c.mlp, dt, st));
             RF_TRY(gemm(act, w.wo2, delta + r0 * hid, r1 - r0, hid, c.mlp));
         }
         // x += mlp out; h = LN(x) with the next layer's attn_norm (or the final norm)
         const float* next_norm = i + 1 < c.n_layers ? s->layers[i + 1].attn_norm : s->final_norm;
-        RF_TRY(rf_add_layernorm(x, delta, next_norm, slot[cur ^ 1], rows, hid, c.eps, st));  // h2 is dead
+        RF_TRY(rf_add_layernorm(x, delta, next_norm, slot[cur ^ 1], rows, hid, c.eps, dt, st));  // h2 is dead
         cur ^= 1;
     }
-    clf_head_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(slot[cur], S, hid, s->head_dense, s->head_norm, s->cls_w, s->cls_b,
-                                                              c.n_labels, c.eps, dlogits);
+    if (bf)
+        clf_head_kernel<true><<<static_cast<unsigned>(B), 256, 0, st>>>(slot[cur], S, hid, s->head_dense, s->head_norm, s->cls_w,
+                                                                        s->cls_b, c.n_labels, c.eps, dlogits);
+    else
+        clf_head_kernel<false><<<static_cast<unsigned>(B), 256, 0, st>>>(slot[cur], S, hid, s->head_dense, s->head_norm, s->cls_w,
+                                                                         s->cls_b, c.n_labels, c.eps, dlogits);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "classifier kernels");
     if ((e = cudaMemcpyAsync(pin + pin_logits, dlogits, static_cast<size_t>(B) * c.n_labels * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         return cuda_fail(e, "logits download");

@@ -1,5 +1,5 @@
 """CPU fp32 oracle of the classifier (TEST INFRASTRUCTURE).  Same random-init weights (rounded to
-bf16 like the device copy), every attention call goes through the reference operator
+the classifier's 16-bit type like the device copy), every attention call goes through the reference operator
 (oracle.flash_attention -> routefast::flash_attention semantics); the rest of the network is a
 plain torch fp32 restatement of paper_2603_12646_b200/classifier.py and is this build's own
 construction -- the reference has no neural classifier (SURVEY.md 8(c) "parity unpinned by the
@@ -11,9 +11,10 @@ import torch
 
 
 def oracle_forward(cfg, weights, input_ids, attention_mask, O, impl="port", threads=None):
+    wdt = getattr(cfg, "torch_dtype", torch.bfloat16)  # the device copy of the matrices is rounded to this type
     threads = threads or os.cpu_count() or 1
     norm_keys = {k for k in weights if k.endswith("norm") or k == "cls_b"}
-    w = {k: (v.float() if k in norm_keys else v.to(torch.bfloat16).float()) for k, v in weights.items()}
+    w = {k: (v.float() if k in norm_keys else v.to(wdt).float()) for k, v in weights.items()}
     B, S = input_ids.shape
     H, d, hid = cfg.heads, cfg.head_dim, cfg.hidden
     ln = lambda t, wt: torch.nn.functional.layer_norm(t, (hid,), wt, None, cfg.eps)  # noqa: E731

@@ -427,45 +427,51 @@ def _small_cfg():
     return ClassifierConfig(vocab_size=1000, n_layers=6, n_labels=3)
 
 
-def test_encoder_glue_kernels(torch_mod, P):
-    """rf_rope_qkv / rf_add_layernorm / rf_geglu against plain torch fp32 references of the same op."""
+@pytest.mark.parametrize("dt_name", ["bf16", "f16"])
+def test_encoder_glue_kernels(torch_mod, P, dt_name):
+    """rf_rope_qkv / rf_add_layernorm / rf_geglu against plain torch fp32 references of the same op, for both
+    16-bit activation types."""
     torch = torch_mod
     from paper_2603_12646_b200 import capi
     from paper_2603_12646_b200.classifier import rope_tables
     lib = capi.load()
+    dt = torch.bfloat16 if dt_name == "bf16" else torch.float16
+    rdt = capi.RF_DTYPE_BF16 if dt_name == "bf16" else capi.RF_DTYPE_F16
+    tol = 2e-2 if dt_name == "bf16" else 4e-3   # rounding of the 16-bit result
     g = torch.Generator(device="cuda").manual_seed(0)
     B, S, H, d = 2, 77, 12, 64
-    qkv = torch.randn((B * S, 3, H, d), device="cuda", generator=g).to(torch.bfloat16)
+    qkv = torch.randn((B * S, 3, H, d), device="cuda", generator=g).to(dt)
     ref = qkv.float().clone()
     cos, sin = rope_tables(S, d, 10000.0, "cuda")
-    capi.check(lib.rf_rope_qkv(qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), B * S, S, H, d, None))
+    capi.check(lib.rf_rope_qkv(qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), B * S, S, H, d, rdt, None))
     pos = torch.arange(B * S, device="cuda") % S
     c, s_ = cos[pos][:, None, None, :], sin[pos][:, None, None, :]
     qk = ref[:, :2]
     want = torch.cat([qk[..., :32] * c - qk[..., 32:] * s_, qk[..., 32:] * c + qk[..., :32] * s_], -1)
-    assert (qkv[:, :2].float() - want).abs().max().item() <= 2e-2   # bf16 rounding of the result
+    assert (qkv[:, :2].float() - want).abs().max().item() <= tol
     assert torch.equal(qkv[:, 2].float(), ref[:, 2])                # V untouched
     rows, n = 300, 768
     x = torch.randn((rows, n), device="cuda", generator=g)
-    dl = torch.randn((rows, n), device="cuda", generator=g).to(torch.bfloat16)
+    dl = torch.randn((rows, n), device="cuda", generator=g).to(dt)
     w = torch.rand((n,), device="cuda", generator=g) + 0.5
     x0 = x.clone()
-    y = torch.empty((rows, n), device="cuda", dtype=torch.bfloat16)
-    capi.check(lib.rf_add_layernorm(x.data_ptr(), dl.data_ptr(), w.data_ptr(), y.data_ptr(), rows, n, 1e-5, None))
+    y = torch.empty((rows, n), device="cuda", dtype=dt)
+    capi.check(lib.rf_add_layernorm(x.data_ptr(), dl.data_ptr(), w.data_ptr(), y.data_ptr(), rows, n, 1e-5, rdt, None))
     xs = x0 + dl.float()
     assert (x - xs).abs().max().item() <= 1e-6
     wy = torch.nn.functional.layer_norm(xs, (n,), w, None, 1e-5)
-    assert (y.float() - wy).abs().max().item() <= 3e-2
+    assert (y.float() - wy).abs().max().item() <= 1.5 * tol
     I = 1152
-    wi = torch.randn((rows, 2 * I), device="cuda", generator=g).to(torch.bfloat16)
-    act = torch.empty((rows, I), device="cuda", dtype=torch.bfloat16)
-    capi.check(lib.rf_geglu(wi.data_ptr(), act.data_ptr(), rows, I, None))
+    wi = torch.randn((rows, 2 * I), device="cuda", generator=g).to(dt)
+    act = torch.empty((rows, I), device="cuda", dtype=dt)
+    capi.check(lib.rf_geglu(wi.data_ptr(), act.data_ptr(), rows, I, rdt, None))
     wa = torch.nn.functional.gelu(wi[:, :I].float()) * wi[:, I:].float()
-    assert (act.float() - wa).abs().max().item() <= 3e-2
+    assert (act.float() - wa).abs().max().item() <= 1.5 * tol
+    assert lib.rf_geglu(wi.data_ptr(), act.data_ptr(), rows, I, capi.RF_DTYPE_F32, None) == capi.RF_ERR_ARG
 
 
 @pytest.mark.parametrize("S,padded", [(512, False), (1024, True)])
-def test_classifier_logits_match_oracle_model(torch_mod, P, oracle, S, padded):
+def test_classifier_logits_match_oracle_model(torch_mod, P, oracle, S, padded):  # default activations: f16
     """Logits within 1e-2 of the fp32 oracle model (attention = reference operator) with identical
     argmax (BASELINE.json north_star).  6-layer slice of the ModernBERT-base shape: layers 0 and 3
     global, the rest local (63,64); full width (hidden 768, 12 x 64 heads, MLP 1152)."""
@@ -748,3 +754,47 @@ def test_row_max_skip_f16_and_packed_views(torch_mod, P, oracle):
     assert st.kernel == "tcgen05"
     want = oracle.flash_attention(qb, kb, vb, 0.0, -1, -1, pb, threads=8)
     assert np.abs(out.permute(0, 2, 1, 3).float().cpu().numpy() - want).max() <= TOL
+
+
+@pytest.mark.parametrize("seed,S,padded", [(1234, 512, False), (4321, 384, True), (99, 512, False)])
+def test_classifier_full_depth_logits_within_tolerance(torch_mod, P, oracle, seed, S, padded):
+    """All 22 layers (7 global + 15 local), f16 activations: logits within 1e-2 of the fp32 oracle model with
+    identical argmax (BASELINE target), for the torch-hosted classifier and the native session.  (With bf16
+    activations the same forwards are 9e-3 .. 2e-2 off: that is why f16 is the default.)"""
+    torch = torch_mod
+    from oracle_model import oracle_forward
+    from paper_2603_12646_b200.classifier import Classifier, ClassifierConfig, NativeClassifier, init_weights
+    cfg = ClassifierConfig(vocab_size=1000, n_layers=22, n_labels=3)
+    assert cfg.act_dtype == "f16"
+    w = init_weights(cfg, seed=seed)
+    g = torch.Generator().manual_seed(S)
+    ids = torch.randint(0, cfg.vocab_size, (2, S), generator=g)
+    mask = None
+    if padded:
+        mask = torch.ones((2, S))
+        mask[0, S - S // 8:] = 0
+        mask[1, S - 5:] = 0
+    want = oracle_forward(cfg, w, ids, mask, oracle)
+    hosted = Classifier(cfg, w, torch.device("cuda:0")).forward(ids.cuda(), mask.cuda() if mask is not None else None).cpu().numpy()
+    native = NativeClassifier(cfg, w).forward(ids, mask).numpy()
+    print("hosted diff", np.abs(hosted - want).max(), "native diff", np.abs(native - want).max())
+    for got in (hosted, native):
+        assert np.abs(got - want).max() <= 1e-2
+        assert (got.argmax(1) == want.argmax(1)).all()
+
+
+def test_classifier_bf16_activations_still_supported(torch_mod, P, oracle):
+    """act_dtype="bf16" keeps working end to end (6-layer slice): same argmax, logits within 2e-2."""
+    torch = torch_mod
+    from oracle_model import oracle_forward
+    from paper_2603_12646_b200.classifier import Classifier, ClassifierConfig, NativeClassifier, init_weights
+    cfg = ClassifierConfig(vocab_size=1000, n_layers=6, n_labels=3, act_dtype="bf16")
+    w = init_weights(cfg, seed=1234)
+    ids = torch.randint(0, cfg.vocab_size, (2, 512), generator=torch.Generator().manual_seed(512))
+    want = oracle_forward(cfg, w, ids, None, oracle)
+    hosted = Classifier(cfg, w, torch.device("cuda:0")).forward(ids.cuda()).cpu().numpy()
+    native = NativeClassifier(cfg, w).forward(ids).numpy()
+    for got in (hosted, native):
+        assert np.abs(got - want).max() <= 2e-2
+        assert (got.argmax(1) == want.argmax(1)).all()
+    assert np.abs(hosted - native).max() <= 5e-3
