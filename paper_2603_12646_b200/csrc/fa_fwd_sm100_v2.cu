@@ -54,7 +54,7 @@ constexpr uint32_t kColS = 0;    // + 128 * X
 constexpr uint32_t kColP = 256;  // + 64 * X
 constexpr uint32_t kColO = 384;  // + 64 * X
 constexpr float kRescaleThresholdBf16 = 20.0f;  // log2 units: P may reach 2^threshold before a rescale is forced
-constexpr float kRescaleThresholdF16 = 8.0f;    // (see fa_fwd_sm100.cu)
+constexpr float kRescaleThresholdF16 = 14.0f;    // (see fa_fwd_sm100.cu)
 // The two query tiles have no barrier in common, and left alone their softmax warps drift into
 // phase: all four warps of an SM sub-partition then queue on the MUFU pipe together and idle it
 // together (exp phase 1700-2100 clk instead of 1300, profiles/).  With RF_FA_V2_TURNS=1 the two warps of
