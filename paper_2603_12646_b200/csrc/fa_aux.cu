@@ -36,23 +36,20 @@ __global__ void __launch_bounds__(128) bias_prepare_kernel(const float* __restri
 }
 
 
-// One CTA per (128-row tile, head, batch), one thread per row: |q_row| and |k_row| from 64 16-bit elements
-// (eight 16-byte loads each); the tile's largest key norm by a block reduction.  Rows >= S count as 0.
+// One CTA per (128-row tile, head, batch).  Eight threads share a row (16 bytes each, so a warp reads four whole
+// 128-byte rows per load instruction whatever the row stride is), eight passes cover the tile's 128 rows; the
+// row's sum of squares is an 8-lane shuffle reduction, the tile's largest key norm a block reduction.
+// Rows >= S count as 0.
 template <bool kBf16>
-__device__ __forceinline__ float row_sumsq64(const void* row) {
+__device__ __forceinline__ float sumsq8(const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     float acc = 0.f;
-    const uint4* p4 = static_cast<const uint4*>(row);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const uint4 v = __ldg(p4 + i);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 f = kBf16 ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]))
-                                   : __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
-            acc = fmaf(f.x, f.x, acc);
-            acc = fmaf(f.y, f.y, acc);
-        }
+    for (int e = 0; e < 4; ++e) {
+        const float2 f = kBf16 ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]))
+                               : __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+        acc = fmaf(f.x, f.x, acc);
+        acc = fmaf(f.y, f.y, acc);
     }
     return acc;
 }
@@ -73,19 +70,40 @@ __global__ void __launch_bounds__(128) qk_norms_kernel(const uint16_t* __restric
         const int gtid = ((b * gridDim.y + h) * gridDim.x + n) * kBlockN + threadIdx.x;
         for (int i = gtid; i < zero_words; i += gridDim.x * gridDim.y * gridDim.z * kBlockN) zero_ptr[i] = 0;
     }
-    const int row = n * kBlockN + threadIdx.x;
-    float kn = 0.f;
-    if (row < S) {
-        const float qs = row_sumsq64<kBf16>(q + b * q_sb + h * q_sh + row * q_ss);
-        qnorm[(static_cast<size_t>(b) * H + h) * S + row] = sqrtf(qs);
-        kn = sqrtf(row_sumsq64<kBf16>(k + b * k_sb + h * k_sh + row * k_ss));
+    const int sub = threadIdx.x & 7;   // 16-byte chunk of the row
+    const int rgrp = threadIdx.x >> 3; // row inside a pass of 16 rows
+    const uint16_t* qb = q + b * q_sb + h * q_sh + sub * 8;
+    const uint16_t* kb = k + b * k_sb + h * k_sh + sub * 8;
+    float kn_max = 0.f;
+    constexpr int kPasses = kBlockN / 16;
+    uint4 qv[kPasses], kv[kPasses];  // all sixteen loads of the thread are in flight before the first use
+#pragma unroll
+    for (int pass = 0; pass < kPasses; ++pass) {
+        const int row = n * kBlockN + pass * 16 + rgrp;
+        qv[pass] = kv[pass] = make_uint4(0u, 0u, 0u, 0u);
+        if (row < S) {
+            qv[pass] = __ldg(reinterpret_cast<const uint4*>(qb + row * q_ss));
+            kv[pass] = __ldg(reinterpret_cast<const uint4*>(kb + row * k_ss));
+        }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) kn = fmaxf(kn, __shfl_xor_sync(0xffffffffu, kn, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = kn;
+    for (int pass = 0; pass < kPasses; ++pass) {
+        const int row = n * kBlockN + pass * 16 + rgrp;
+        float qs = sumsq8<kBf16>(qv[pass]), ks = sumsq8<kBf16>(kv[pass]);
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            qs += __shfl_xor_sync(0xffffffffu, qs, o);
+            ks += __shfl_xor_sync(0xffffffffu, ks, o);
+        }
+        if (sub == 0 && row < S) qnorm[(static_cast<size_t>(b) * H + h) * S + row] = sqrtf(qs);
+        kn_max = fmaxf(kn_max, ks);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kn_max = fmaxf(kn_max, __shfl_xor_sync(0xffffffffu, kn_max, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = kn_max;
     __syncthreads();
     if (threadIdx.x == 0)
-        kmax[(static_cast<size_t>(b) * H + h) * n_kv_tiles + n] = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+        kmax[(static_cast<size_t>(b) * H + h) * n_kv_tiles + n] = sqrtf(fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3])));
 }
 
 constexpr int kMaxParts = 16;
