@@ -192,11 +192,12 @@ int rf_fused_flash_attention_op(const float* const* inputs, const int64_t* const
                                 int32_t has_window_right, int64_t window_right, float* output,
                                 int32_t device);
 
-/* Encoder-layer glue either side of the op, bf16, in place where possible:
+/* Encoder-layer glue either side of the op, 16-bit activations (`dtype`: bf16 or f16),
+ * in place where possible:
  *   rf_rope_qkv      rotary embedding ("rotate_half" pairing i, i+d/2) on the Q and K thirds of a
  *                    packed QKV GEMM output [tokens,3,H,d]; cos/sin f32 [S,d/2]; position = t % S.
  *                    The attention kernel then reads the three thirds as strided views.
- *   rf_add_layernorm x (f32 residual stream [rows,n]) += delta (bf16, or NULL); y = LN(x)*w (bf16,
+ *   rf_add_layernorm x (f32 residual stream [rows,n]) += delta (16-bit, or NULL); y = LN(x)*w (16-bit,
  *                    no bias; y may be NULL to only accumulate).  n % 4 == 0, n <= 4096.
  *   rf_geglu         act[rows,I] = gelu(wi_out[:, :I]) * wi_out[:, I:]   (erf GELU)            */
 /* dtype: rf_dtype of the 16-bit activations, RF_DTYPE_BF16 or RF_DTYPE_F16 */
