@@ -18,11 +18,14 @@
 //               warps per SM sub-partition hide each other's MUFU/ALU latencies.  The two halves
 //               exchange their row max through shared memory (one 64-thread named barrier per
 //               tile); row sums stay per-thread until the epilogue.  exp2 with the scale folded in,
-//               packed f32x2 math, lazy rescale of O (only when the running max grows by > 2^8).
+//               packed f32x2 math, lazy rescale of O (only when the running max grows by > 2^20 with
+//               bf16 P, 2^14 with f16 P).  Row-max skip: when c |q_row| max_j |k_j| (norms from the
+//               qk_norms pre-pass) cannot exceed the reference max by more than that slack, the tile's
+//               max pass, the exchange and its barrier are skipped (see the softmax loop).
 //               setmaxnreg moves registers from the producer/MMA warpgroup to the softmax ones.
 //
 // Work distribution.  A work item is (query-tile pair, key-tile range).
-//   mode 0: one item per CTA (grid = number of pairs); used with windows, padding bias, split-KV.
+//   mode 0: one item per CTA (grid = number of pairs); used when the pairs fit one wave and for split-KV.
 //   mode 1: persistent, statically balanced: the flat (pair x key-tile) iteration space is cut
 //           into gridDim.x equal contiguous slices.  A pair cut between CTA c (its first key
 //           tiles, processed LAST by c) and CTA c+1 (its remaining key tiles, processed FIRST by
@@ -30,6 +33,10 @@
 //           workspace, c combines it with its own in a fixed order.  This removes the wave
 //           quantisation of the dense global layers (e.g. 384 pairs on 148 SMs) and stays
 //           run-to-run deterministic.
+//   mode 2: persistent, whole pairs dealt round-robin (pair c, c + gridDim.x, ...): batches with at least
+//           8 pairs per SM.  CTAs that run together work on neighbouring pairs (K/V of a few heads stay in
+//           L2), and sequences of different padded lengths spread over all CTAs.
+// Narrow sliding windows (wl + wr <= 127) do not come here: fa_fwd_sm100_local.cu.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
