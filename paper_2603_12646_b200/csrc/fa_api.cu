@@ -252,14 +252,18 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         // of K/V beyond the L2 that costs 5-15 % (B=4, S=16K: 785 -> 899 TFLOP/s).  (ii) With padding, sequence
         // lengths live on the device and usually differ: equal slices of the virtual (pair x tile) space leave
         // the CTAs that drew short sequences idle (efficiency ~ mean/max length), round-robin gives every CTA
-        // pairs of every sequence.  No pair is split; the price is a last partial round (<= 1/8 of the work).
+        // pairs of every sequence.  No pair is split; the price is a last partial round ...
         // A single sequence keeps mode 1 (B=1, S=16K: 921 vs 799 TFLOP/s).
         // RF_FA_SCHED_MODE=1|2 forces a schedule (developer aid for A/B measurements)
         static const int forced = [] {
             const char* env = std::getenv("RF_FA_SCHED_MODE");
             return env != nullptr ? std::atoi(env) : 0;
         }();
-        const bool want2 = p->B > 1 && pl.total_pairs >= 8ll * sms;
+        // ... chosen when that last round wastes little: its idle share is rounds*sms/pairs - 1 (at most 5 % for
+        // dense batches, where the gain is L2 locality, at most 10 % for padded ones, where lengths differ)
+        const int64_t rounds = (pl.total_pairs + sms - 1) / sms;
+        const double waste = static_cast<double>(rounds * sms) / static_cast<double>(pl.total_pairs) - 1.0;
+        const bool want2 = p->B > 1 && pl.total_pairs >= 4ll * sms && waste <= (p->pad_bias != nullptr ? 0.10 : 0.05);
         if (forced == 2 || (forced == 0 && want2)) {
             pl.sched_mode = 2;
             pl.part_bytes = 0;

@@ -33,8 +33,8 @@
 //           workspace, c combines it with its own in a fixed order.  This removes the wave
 //           quantisation of the dense global layers (e.g. 384 pairs on 148 SMs) and stays
 //           run-to-run deterministic.
-//   mode 2: persistent, whole pairs dealt round-robin (pair c, c + gridDim.x, ...): batches with at least
-//           8 pairs per SM.  CTAs that run together work on neighbouring pairs (K/V of a few heads stay in
+//   mode 2: persistent, whole pairs dealt round-robin (pair c, c + gridDim.x, ...): batches whose last
+//           partial round wastes little (fa_api.cu).  CTAs that run together work on neighbouring pairs (K/V of a few heads stay in
 //           L2), and sequences of different padded lengths spread over all CTAs.
 // Narrow sliding windows (wl + wr <= 127) do not come here: fa_fwd_sm100_local.cu.
 #include <cuda.h>

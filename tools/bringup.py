@@ -341,6 +341,9 @@ CASES = {
                                                       lens=[8192, 4100, 6000, 5000, 7777, 4500, 8000, 0], iters=5),
     "graph_8k_b8_allfull": lambda: case_time_graph("graph_8k_b8_allfull", 8, 12, 8192, -1, -1, lens=[8192] * 8, iters=5),
     "graph_8k_b8_allhalf": lambda: case_time_graph("graph_8k_b8_allhalf", 8, 12, 8192, -1, -1, lens=[4096] * 8, iters=5),
+    "graph_8k_b2_full_bias": lambda: case_time_graph("graph_8k_b2_full_bias", 2, 12, 8192, -1, -1, lens=[8192, 8192], iters=5),
+    "graph_8k_b3_mixed": lambda: case_time_graph("graph_8k_b3_mixed", 3, 12, 8192, -1, -1, lens=[8192, 5000, 6500], iters=5),
+    "graph_8k_b2_global": lambda: case_time_graph("graph_8k_b2_global", 2, 12, 8192, -1, -1, iters=5),
     "graph_8k_b2_skew": lambda: case_time_graph("graph_8k_b2_skew", 2, 12, 8192, -1, -1, lens=[8192, 4096], iters=5),
     "cross_4k_b4_pad": lambda: case_cross("cross_4k_b4_pad", 4, 12, 4096, -1, -1, [4096, 2100, 3000, 0]),
     "graph_8k_b8_skew_nozero": lambda: case_time_graph("graph_8k_b8_skew_nozero", 8, 12, 8192, -1, -1,
