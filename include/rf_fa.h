@@ -103,7 +103,8 @@ typedef struct rf_fa_params {
     int32_t out_dtype; /* rf_dtype of O */
     int32_t kernel;    /* rf_kernel */
     int32_t flags;     /* reserved, must be 0 */
-    int64_t kv_begin; /* split-KV key range; both 0 => [0,S) */
+    int64_t kv_begin; /* split-KV key range.  Full call (o_partial == NULL): both 0 => [0,S).  Partial call: taken
+                       * literally; an empty range writes the merge's neutral element (m = -inf, l = 0, O = 0) */
     int64_t kv_end;
     float* o_partial;
     float* m_partial;

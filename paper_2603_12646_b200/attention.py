@@ -155,8 +155,8 @@ def _device_call(q, k, v, spec: AttentionSpec, stats, out, out_dtype, kernel, fl
         p.pad_bias = pb.data_ptr()
     if kv_range is not None:
         p.kv_begin, p.kv_end = int(kv_range[0]), int(kv_range[1])
-        if p.kv_begin == 0 and p.kv_end == 0:
-            p.kv_begin, p.kv_end = 0, 0  # empty range is expressed by the caller skipping the call
+    elif partials is not None:
+        p.kv_begin, p.kv_end = 0, S  # a partial takes its key range literally ([0, 0) is an empty block)
     if debug_scores is not None:
         p.debug_scores = debug_scores.data_ptr()
 

@@ -228,8 +228,10 @@ struct rf_clf {
     // activation arena
     void* arena = nullptr;
     size_t arena_bytes = 0;
-    // RoPE tables are part of the arena layout; recomputed when S changes
-    int64_t rope_S = 0;
+    // RoPE tables (cos, sin) x (global, local), [rope_cap, d/2] f32 each, in their own allocation: they depend on
+    // the position only, so the tables of a longer sequence serve every shorter one, whatever B or the mask
+    float* rope_buf = nullptr;
+    int64_t rope_cap = 0;
     float last_ms = 0.f;
     // library GEMM workspace owned by the session (so that no allocation happens under graph capture)
     void* blas_ws = nullptr;
@@ -244,7 +246,7 @@ struct rf_clf {
 namespace {
 
 struct Layout {
-    size_t x, big, slot[2], ws, rope[4], ids, mask, bias, logits, total;
+    size_t x, big, slot[2], ws, ids, mask, bias, logits, total;
     size_t ws_bytes;
 };
 
@@ -264,7 +266,6 @@ Layout make_layout(const rf_clf_config& c, int64_t B, int64_t S, size_t attn_ws)
     L.slot[1] = take(rows * hid * 2);
     L.ws_bytes = attn_ws;
     L.ws = take(attn_ws);
-    for (int i = 0; i < 4; ++i) L.rope[i] = take(static_cast<size_t>(S) * (c.head_dim / 2) * 4);  // cos/sin x global/local
     L.ids = take(rows * 8);
     L.mask = take(rows * 4);
     L.bias = take(rows * 4);
@@ -458,7 +459,6 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
         if (s->arena != nullptr) cudaFree(s->arena);
         s->arena = nullptr;
         s->arena_bytes = 0;
-        s->rope_S = 0;
         if ((e = cudaMalloc(&s->arena, L.total)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(arena)");
         s->arena_bytes = L.total;
     }
@@ -470,29 +470,34 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
     float* mask = reinterpret_cast<float*>(base + L.mask);
     float* bias = reinterpret_cast<float*>(base + L.bias);
     float* dlogits = reinterpret_cast<float*>(base + L.logits);
-    float* rope[4];
-    for (int i = 0; i < 4; ++i) rope[i] = reinterpret_cast<float*>(base + L.rope[i]);
-
-    // RoPE tables (cos, sin) x (global, local), f64 on the host like classifier.py's rope_tables.  The arena
-    // layout depends on (B, S): recompute whenever the shape differs from the previous forward.
-    if (s->rope_S != B * (1ll << 32) + S) {
+    // RoPE tables, f64 on the host like classifier.py's rope_tables; rebuilt only when S outgrows them
+    if (S > s->rope_cap) {
+        if (s->graph_exec != nullptr) cudaGraphExecDestroy(s->graph_exec);  // it holds the table addresses
+        s->graph_exec = nullptr;
+        s->graph_key = s->last_key = -1;
+        if (s->rope_buf != nullptr) cudaFree(s->rope_buf);
+        s->rope_buf = nullptr;
+        s->rope_cap = 0;
         const int half = d / 2;
-        std::vector<float> tab(static_cast<size_t>(S) * half);
+        const size_t per = static_cast<size_t>(S) * half;
+        if ((e = cudaMalloc(reinterpret_cast<void**>(&s->rope_buf), 4 * per * sizeof(float))) != cudaSuccess)
+            return cuda_fail(e, "cudaMalloc(rope tables)");
+        std::vector<float> tab(4 * per);
         for (int kind = 0; kind < 2; ++kind) {
             const double theta = kind == 0 ? c.rope_theta_global : c.rope_theta_local;
-            for (int f = 0; f < 2; ++f) {
-                for (int64_t p = 0; p < S; ++p)
-                    for (int i = 0; i < half; ++i) {
-                        const double ang = static_cast<double>(p) / pow(theta, (2.0 * i) / d);
-                        tab[static_cast<size_t>(p) * half + i] = static_cast<float>(f == 0 ? cos(ang) : sin(ang));
-                    }
-                if ((e = cudaMemcpyAsync(rope[kind * 2 + f], tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
-                    return cuda_fail(e, "rope upload");
-                cudaStreamSynchronize(st);  // tab is reused
-            }
+            for (int64_t p = 0; p < S; ++p)
+                for (int i = 0; i < half; ++i) {
+                    const double ang = static_cast<double>(p) / pow(theta, (2.0 * i) / d);
+                    tab[(kind * 2 + 0) * per + static_cast<size_t>(p) * half + i] = static_cast<float>(cos(ang));
+                    tab[(kind * 2 + 1) * per + static_cast<size_t>(p) * half + i] = static_cast<float>(sin(ang));
+                }
         }
-        s->rope_S = B * (1ll << 32) + S;
+        if ((e = cudaMemcpy(s->rope_buf, tab.data(), tab.size() * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess)
+            return cuda_fail(e, "rope upload");
+        s->rope_cap = S;
     }
+    const float* rope[4];
+    for (int i = 0; i < 4; ++i) rope[i] = s->rope_buf + static_cast<size_t>(i) * s->rope_cap * (d / 2);
 
     // page-locked staging: [ids | mask | logits]
     const size_t pin_ids = 0, pin_mask = align_up(rows * 8, 256), pin_logits = pin_mask + align_up(rows * 4, 256);
@@ -655,6 +660,7 @@ void rf_clf_destroy(rf_clf* s) {
     if (s->handle != nullptr && s->blas.destroy != nullptr) s->blas.destroy(s->handle);
     if (s->graph_exec != nullptr) cudaGraphExecDestroy(s->graph_exec);
     if (s->arena != nullptr) cudaFree(s->arena);
+    if (s->rope_buf != nullptr) cudaFree(s->rope_buf);
     if (s->blas_ws != nullptr) cudaFree(s->blas_ws);
     if (s->pinned != nullptr) cudaFreeHost(s->pinned);
     if (s->w16 != nullptr) cudaFree(s->w16);

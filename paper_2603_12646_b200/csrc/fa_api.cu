@@ -16,10 +16,6 @@
 #include "../../include/rf_fa.h"
 #include "fa_internal.h"
 
-#ifndef RF_FA_DEFAULT_V2
-#define RF_FA_DEFAULT_V2 0
-#endif
-
 namespace {
 
 thread_local std::string g_last_error;
@@ -53,6 +49,7 @@ struct Resolved {
     int64_t qs[3], ks[3], vs[3], os[3];
     double scale;  // effective
     int64_t kv_begin, kv_end;
+    int64_t wl, wr;  // saturated windows: -1 = unbounded (any negative bound, or one that reaches past the sequence)
     bool partial;
 };
 
@@ -79,8 +76,10 @@ int validate(const rf_fa_params* p, Resolved* r) {
         return fail(RF_ERR_ARG, "dtype must be bf16 or f16");
     if (p->out_dtype < RF_DTYPE_BF16 || p->out_dtype > RF_DTYPE_F32) return fail(RF_ERR_ARG, "bad out_dtype");
     if (p->kernel < RF_KERNEL_AUTO || p->kernel > RF_KERNEL_SIMT) return fail(RF_ERR_ARG, "bad kernel selector");
+    if (p->flags != 0) return fail(RF_ERR_ARG, "flags is reserved and must be 0");
     // any negative window bound means "unbounded", as in attention.cpp:132-136
-    if (p->S > (1ll << 30) || p->B * p->H > (1ll << 30)) return fail(RF_ERR_ARG, "dimension too large");
+    // B and H index grid.y / grid.z of the auxiliary kernels (65535 each)
+    if (p->S > (1ll << 30) || p->B > 65535 || p->H > 65535) return fail(RF_ERR_ARG, "dimension too large");
     r->partial = p->o_partial != nullptr;
     if (r->partial && (p->m_partial == nullptr || p->l_partial == nullptr))
         return fail(RF_ERR_ARG, "split-KV needs o_partial, m_partial and l_partial");
@@ -95,9 +94,15 @@ int validate(const rf_fa_params* p, Resolved* r) {
     resolve_strides(p->o_stride, r->os, p->H, p->S, p->d);
     r->scale = p->scale != 0.0 ? p->scale : 1.0 / std::sqrt(static_cast<double>(p->d));  // attention.cpp:34-36
     if (!std::isfinite(r->scale)) return fail(RF_ERR_ARG, "scale is not finite");
+    // any negative bound means unbounded (attention.cpp:132-136); so does one of S or more, which keeps every
+    // later sum of the two inside int64 whatever the caller passes for "no limit"
+    r->wl = (p->window_left < 0 || p->window_left >= p->S) ? -1 : p->window_left;
+    r->wr = (p->window_right < 0 || p->window_right >= p->S) ? -1 : p->window_right;
     r->kv_begin = p->kv_begin;
     r->kv_end = p->kv_end;
-    if (r->kv_begin == 0 && r->kv_end == 0) r->kv_end = p->S;
+    // "both 0" means the whole sequence only for a full call; a split-KV partial takes its range literally, so
+    // an honestly empty key block [0, 0) yields the neutral element of the merge (m = -inf, l = 0, O = 0)
+    if (!r->partial && r->kv_begin == 0 && r->kv_end == 0) r->kv_end = p->S;
     if (r->kv_begin < 0 || r->kv_end > p->S || r->kv_begin > r->kv_end)
         return fail(RF_ERR_ARG, "kv range must satisfy 0 <= kv_begin <= kv_end <= S");
     return RF_OK;
@@ -168,16 +173,6 @@ int sm_count_or_default() {
     return 148;
 }
 
-// RF_FA_V2=0|1 selects the pipeline variant of the dense kernel at run time (kernel tuning; both are full
-// implementations)
-bool use_v2_kernel() {
-    static const bool use_v2 = [] {
-        const char* env = std::getenv("RF_FA_V2");
-        return env != nullptr ? env[0] == '1' : RF_FA_DEFAULT_V2 != 0;
-    }();
-    return use_v2;
-}
-
 struct Plan {
     int kernel;
     bool local;       // tcgen05 only: the narrow-window kernel takes the call
@@ -205,9 +200,9 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         const char* env = std::getenv("RF_FA_LOCAL");
         return env == nullptr || env[0] != '0';
     }();
-    if (local_enabled && !r.partial && r.kv_begin == 0 && r.kv_end == p->S && p->window_left >= 0 &&
-        p->window_right >= 0 && p->window_left + p->window_right < rf::kBlockN &&
-        rf::fa_fwd_sm100_local_covers(static_cast<int>(p->window_left), static_cast<int>(p->window_right))) {
+    if (local_enabled && !r.partial && r.kv_begin == 0 && r.kv_end == p->S && r.wl >= 0 && r.wr >= 0 &&
+        r.wl < rf::kBlockN && r.wr < rf::kBlockN && r.wl + r.wr < rf::kBlockN &&
+        rf::fa_fwd_sm100_local_covers(static_cast<int>(r.wl), static_cast<int>(r.wr))) {
         pl.local = true;
         const int64_t tiles = static_cast<int64_t>(p->B) * p->H * ((p->S + rf::kBlockM - 1) / rf::kBlockM);
         pl.grid = static_cast<int>(std::min<int64_t>(tiles, sm_count_or_default()));
@@ -225,8 +220,8 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         const int64_t t_begin = r.kv_begin / rf::kBlockN;
         const int64_t t_end = (r.kv_end + rf::kBlockN - 1) / rf::kBlockN;
         int64_t tiles = t_end - t_begin;
-        if (p->window_left >= 0 && p->window_right >= 0) {
-            const int64_t span = rf::kRowsPerCta + p->window_left + p->window_right;  // keys a pair can see
+        if (r.wl >= 0 && r.wr >= 0) {
+            const int64_t span = rf::kRowsPerCta + r.wl + r.wr;  // keys a pair can see
             tiles = std::min<int64_t>(tiles, (span + rf::kBlockN - 1) / rf::kBlockN + 1);
         }
         pl.tiles_per_pair = std::max<int64_t>(tiles, 1);
@@ -297,8 +292,8 @@ void fill_fa_params(const rf_fa_params* p, const Resolved& r, rf::FaParams* f) {
     f->S = static_cast<int>(p->S);
     f->kv_begin = static_cast<int>(r.kv_begin);
     f->kv_end = static_cast<int>(r.kv_end);
-    f->wl = static_cast<int>(p->window_left < 0 ? -1 : (p->window_left > (1 << 30) ? (1 << 30) : p->window_left));
-    f->wr = static_cast<int>(p->window_right < 0 ? -1 : (p->window_right > (1 << 30) ? (1 << 30) : p->window_right));
+    f->wl = static_cast<int>(r.wl);
+    f->wr = static_cast<int>(r.wr);
     f->scale_log2 = static_cast<float>(r.scale * 1.4426950408889634);
     f->n_kv_tiles = static_cast<int>(n_kv_tiles(p->S));
     f->bias_stride = f->n_kv_tiles * rf::kBlockN;
@@ -386,6 +381,12 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     if (rc != RF_OK) return rc;
     if (p->B == 0 || p->H == 0 || p->S == 0) return RF_OK;
     cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+    if (r.partial && r.kv_begin == r.kv_end) {  // empty key block: the neutral element of the merge
+        cudaError_t e = rf::launch_partial_neutral(p->o_partial, p->m_partial, p->l_partial, p->B * p->H * p->S,
+                                                   static_cast<int>(p->d), stream);
+        if (e != cudaSuccess) return cuda_fail(e, "partial_neutral launch");
+        return RF_OK;
+    }
 
     rf::FaParams f;
     fill_fa_params(p, r, &f);
@@ -470,10 +471,8 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
     if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
     if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
-    cudaError_t e = use_v2_kernel() ? rf::launch_fa_fwd_sm100_v2(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream,
-                                                                 /*pdl=*/pl.qnorm_bytes > 0)
-                           : rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream,
-                                                     /*pdl=*/pl.qnorm_bytes > 0);
+    cudaError_t e = rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream,
+                                            /*pdl=*/pl.qnorm_bytes > 0);
     if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100 launch");
     return RF_OK;
 }
@@ -585,6 +584,7 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
         return RF_OK;
     }
     if (q == nullptr || k == nullptr || v == nullptr || out == nullptr) return fail(RF_ERR_ARG, "null host pointer");
+    if (device < 0 || device >= kMaxDevices) return fail(RF_ERR_ARG, "device index out of range");
 
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
@@ -642,7 +642,6 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
     }
     float* d_out_full = nullptr;
 
-    if (device < 0 || device >= kMaxDevices) return fail(RF_ERR_ARG, "device index out of range");
     HostCtx& ctx = g_host_ctx[device];
     cudaStream_t* streams = ctx.streams;
     float* d_f32[kStreams] = {nullptr, nullptr, nullptr, nullptr};    // f32 staging: 3 inputs, then reused for O
@@ -652,6 +651,9 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
     cudaEvent_t& bias_ready = ctx.ready;
     int rc = RF_OK;
     auto cleanup = [&]() {
+        // work queued on any stream may still read the shared buffers: drain all of them before freeing
+        for (int i = 0; i < kStreams; ++i)
+            if (streams[i] != nullptr) cudaStreamSynchronize(streams[i]);
         for (int i = 0; i < kStreams; ++i) {
             if (streams[i] == nullptr) continue;
             if (d_f32[i]) cudaFreeAsync(d_f32[i], streams[i]);

@@ -169,6 +169,16 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergePtrs ptrs, int G,
     store_dyn(out, o + 3, acc.w * inv, out_dtype);
 }
 
+__global__ void __launch_bounds__(256) partial_neutral_kernel(float* __restrict__ o_part, float* __restrict__ m_part,
+                                                              float* __restrict__ l_part, long long rows, int d) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx < rows * d) o_part[idx] = 0.f;
+    if (idx < rows) {
+        m_part[idx] = -CUDART_INF_F;
+        l_part[idx] = 0.f;
+    }
+}
+
 __global__ void __launch_bounds__(256) rescale_partial_kernel(float* o_part, float* l_part,
                                                               const float* __restrict__ m_part,
                                                               const float* __restrict__ m_star, long long rows, int d) {
@@ -274,6 +284,13 @@ cudaError_t launch_merge(const float* const* o_parts, const float* const* m_part
     const long long n = rows * (d >> 2);
     if (n == 0) return cudaSuccess;
     merge_kernel<<<blocks_for(n, 256), 256, 0, stream>>>(ptrs, G, rows, d, out, out_dtype);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_partial_neutral(float* o_part, float* m_part, float* l_part, long long rows, int d, cudaStream_t stream) {
+    const long long n = rows * d;
+    if (n == 0) return cudaSuccess;
+    partial_neutral_kernel<<<blocks_for(n, 256), 256, 0, stream>>>(o_part, m_part, l_part, rows, d);
     return cudaGetLastError();
 }
 

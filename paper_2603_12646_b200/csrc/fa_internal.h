@@ -75,9 +75,6 @@ struct SimtParams {
 // griddepcontrol.launch_dependents; this one waits for it after its prologue)
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
                                 const FaParams& p, bool bf16, int grid, cudaStream_t stream, bool pdl = false);
-// decoupled-pipeline variant (fa_fwd_sm100_v2.cu): same contract, same workspace layout
-cudaError_t launch_fa_fwd_sm100_v2(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
-                                   const FaParams& p, bool bf16, int grid, cudaStream_t stream, bool pdl = false);
 // narrow-window kernel (fa_fwd_sm100_local.cu): wl + wr <= 127, one 256-key strip per query tile;
 // reads the raw pad_bias [B,S] (nullable), needs no workspace
 bool fa_fwd_sm100_local_covers(int wl, int wr);
@@ -101,6 +98,8 @@ cudaError_t launch_qk_norms(const void* q, const void* k, const long long q_stri
                             int zero_words, cudaStream_t stream);
 cudaError_t launch_merge(const float* const* o_parts, const float* const* m_parts, const float* const* l_parts,
                          int G, long long rows, int d, void* out, int out_dtype, cudaStream_t stream);
+// split-KV partial of an empty key block: O = 0, m = -inf, l = 0
+cudaError_t launch_partial_neutral(float* o_part, float* m_part, float* l_part, long long rows, int d, cudaStream_t stream);
 cudaError_t launch_rescale_partial(float* o_part, float* l_part, const float* m_part, const float* m_star,
                                    long long rows, int d, cudaStream_t stream);
 cudaError_t launch_normalize(const float* o_sum, const float* l_sum, long long rows, int d, void* out,

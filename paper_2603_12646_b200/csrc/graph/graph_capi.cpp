@@ -182,14 +182,25 @@ int rf_graph_interpret(const char* json, int32_t n_inputs, const char* const* na
 }
 
 int32_t rf_graph_result_count(const rf_graph_result* r) { return r ? static_cast<int32_t>(r->names.size()) : 0; }
-const char* rf_graph_result_name(const rf_graph_result* r, int32_t i) { return r->names.at(static_cast<size_t>(i)).c_str(); }
-int32_t rf_graph_result_rank(const rf_graph_result* r, int32_t i) {
-    return static_cast<int32_t>(r->tensors.at(static_cast<size_t>(i)).shape.size());
+// accessors never throw through the C boundary: a null result or an index out of range yields NULL / -1
+static bool result_index_ok(const rf_graph_result* r, int32_t i) {
+    return r != nullptr && i >= 0 && static_cast<size_t>(i) < r->tensors.size() && static_cast<size_t>(i) < r->names.size();
 }
-const int64_t* rf_graph_result_dims(const rf_graph_result* r, int32_t i) { return r->tensors.at(static_cast<size_t>(i)).shape.data(); }
-const float* rf_graph_result_data(const rf_graph_result* r, int32_t i) { return r->tensors.at(static_cast<size_t>(i)).data.data(); }
+const char* rf_graph_result_name(const rf_graph_result* r, int32_t i) {
+    return result_index_ok(r, i) ? r->names[static_cast<size_t>(i)].c_str() : nullptr;
+}
+int32_t rf_graph_result_rank(const rf_graph_result* r, int32_t i) {
+    return result_index_ok(r, i) ? static_cast<int32_t>(r->tensors[static_cast<size_t>(i)].shape.size()) : -1;
+}
+const int64_t* rf_graph_result_dims(const rf_graph_result* r, int32_t i) {
+    return result_index_ok(r, i) ? r->tensors[static_cast<size_t>(i)].shape.data() : nullptr;
+}
+const float* rf_graph_result_data(const rf_graph_result* r, int32_t i) {
+    return result_index_ok(r, i) ? r->tensors[static_cast<size_t>(i)].data.data() : nullptr;
+}
 int32_t rf_graph_result_is_f16(const rf_graph_result* r, int32_t i) {
-    return r->tensors.at(static_cast<size_t>(i)).dtype == rb::DType::f16 ? 1 : 0;
+    if (!result_index_ok(r, i)) return -1;
+    return r->tensors[static_cast<size_t>(i)].dtype == rb::DType::f16 ? 1 : 0;
 }
 void rf_graph_result_stats(const rf_graph_result* r, rf_graph_stats* stats) {
     if (r == nullptr || stats == nullptr) return;

@@ -463,7 +463,23 @@ DevTensor run_fused_attention(Runner& rt, const Node& node, const DevTensor& q, 
     p.window_right = node.attr_int("window_right", -1);
     p.dtype = RF_DTYPE_BF16;
     p.out_dtype = RF_DTYPE_F32;
-    uint16_t* qkv16 = static_cast<uint16_t*>(rt.scratch(3 * n * 2));
+    // scratch buffers are released on every exit path, including a throwing RF_CUDA / rt.scratch
+    struct Scratch {
+        Runner& rt;
+        void* ptr = nullptr;
+        std::size_t bytes = 0;
+        explicit Scratch(Runner& r) : rt(r) {}
+        void* get(std::size_t n_bytes) {
+            ptr = rt.scratch(n_bytes);
+            bytes = n_bytes;
+            return ptr;
+        }
+        ~Scratch() {
+            if (ptr != nullptr) rt.scratch_free(ptr, bytes);
+        }
+    };
+    Scratch qkv_buf(rt), ws_buf(rt);
+    uint16_t* qkv16 = static_cast<uint16_t*>(qkv_buf.get(3 * n * 2));
     const float* src[3] = {q.ptr, k.ptr, v.ptr};
     for (int t = 0; t < 3; ++t) {
         RF_CUDA(rf::launch_cast_from_f32(src[t], qkv16 + static_cast<std::size_t>(t) * n, static_cast<long long>(n),
@@ -479,10 +495,8 @@ DevTensor run_fused_attention(Runner& rt, const Node& node, const DevTensor& q, 
     std::size_t ws_bytes = 0;
     int rc = rf_fa_fwd_workspace_bytes(&p, &ws_bytes);
     void* ws = nullptr;
-    if (rc == RF_OK && ws_bytes > 0) ws = rt.scratch(ws_bytes);
+    if (rc == RF_OK && ws_bytes > 0) ws = ws_buf.get(ws_bytes);
     if (rc == RF_OK) rc = rf_fa_fwd(&p, ws, ws_bytes, rt.stream());
-    if (ws != nullptr) rt.scratch_free(ws, ws_bytes);
-    rt.scratch_free(qkv16, 3 * n * 2);
     if (rc == RF_ERR_SHAPE) throw ShapeMismatch(rf_last_error());
     if (rc == RF_ERR_HEAD_DIM) throw UnsupportedHeadDim(rf_last_error());
     if (rc != RF_OK) throw std::runtime_error(std::string("rf_fa: ") + rf_last_error());

@@ -8,7 +8,7 @@ gather of the [n_req, n_labels] logits.  Assignment is LPT (longest processing t
 cost model of the attention work, which is what dominates at 8K-32K tokens.
 
 The scheduler is pure host logic; the per-unit work is a callable, so the N > 1 path is covered
-by world_size-2 gloo tests on CPU (tests/test_scheduler_gloo.py).
+by world_size-2 gloo tests on CPU (tests/test_multi_gpu_host_logic.py).
 """
 from __future__ import annotations
 

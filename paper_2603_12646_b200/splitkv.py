@@ -44,12 +44,8 @@ class CudaSplitKVOps:
         o = torch.empty((B, H, S, d), device=q.device, dtype=torch.float32)
         m = torch.empty((B, H, S), device=q.device, dtype=torch.float32)
         l = torch.empty((B, H, S), device=q.device, dtype=torch.float32)
-        if kv_range[1] <= kv_range[0]:  # empty block: the neutral element of the merge
-            o.zero_()
-            m.fill_(float("-inf"))
-            l.zero_()
-        else:
-            flash_attention(q, k, v, spec, kv_range=kv_range, partials=(o, m, l))
+        # an empty block yields the neutral element of the merge (m = -inf, l = 0, O = 0) inside the library
+        flash_attention(q, k, v, spec, kv_range=kv_range, partials=(o, m, l))
         return o, m, l
 
     def rescale(self, o, l, m, m_star):

@@ -46,7 +46,7 @@ print("variant ok", worst)
 """
 
 
-@pytest.mark.parametrize("env", [{"RF_FA_V2": "1"}, {"RF_FA_LOCAL": "0"}, {"RF_FA_SKIP_MAX": "0"}, {"RF_FA_SCHED_MODE": "1"},
+@pytest.mark.parametrize("env", [{"RF_FA_LOCAL": "0"}, {"RF_FA_SKIP_MAX": "0"}, {"RF_FA_SCHED_MODE": "1"},
                                  {"RF_FA_SCHED_MODE": "2"}])
 def test_kernel_selector_variants(env):
     e = dict(os.environ)

@@ -44,11 +44,6 @@ dm = np.diff(tm, axis=1) % (1 << 32)
 out["mma_warp"] = {n: float(np.median(dm[:, i])) for i, n in enumerate(
     ["wait_V", "wait_PA", "issue_PVA_QKB", "wait_PB", "issue_PVB", "wait_K", "issue_QKA"])}
 out["mma_warp"]["period"] = float(np.median((tm[1:, 0] - tm[:-1, 0]) % (1 << 32)))
-tm2 = t[18, 8:56]  # second issuer (decoupled variant only)
-dm2 = np.diff(tm2, axis=1) % (1 << 32)
-out["mma_warp_b"] = {n: float(np.median(dm2[:, i])) for i, n in enumerate(
-    ["wait_V", "wait_PA", "issue_PVA_QKB", "wait_PB", "issue_PVB", "wait_K", "issue_QKA"])}
-out["v2_stamp_names"] = "issuer: 0 top, 1 S free+K full, 2 QK issued, 3 P full+V full, 4 PV issued"
 # absolute alignment for one steady-state tile (i = 20): all stamps relative to warp 0's stamp 0 of tile 20
 i0 = 20
 ref = t[0, i0, 0]
