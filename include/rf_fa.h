@@ -53,14 +53,16 @@ typedef enum rf_status {
     RF_ERR_SCHEMA = 7,         /* reference: SchemaError (graph.hpp:17-20) */
     RF_ERR_VALIDATION = 8,     /* reference: ValidationError (graph.hpp:23-26) */
     RF_ERR_NO_MASK_INPUT = 9,  /* reference: NoAttentionMaskInput (rewrite.hpp:19-22) */
-    RF_ERR_UNSUPPORTED_OP = 10 /* reference: UnsupportedOp (interpreter.hpp:14-17) */
+    RF_ERR_UNSUPPORTED_OP = 10, /* reference: UnsupportedOp (interpreter.hpp:14-17) */
+    RF_ERR_DEVICE_TIMEOUT = 11  /* a bounded wait inside a kernel ran out (rf_fa_launch_status); the context stays usable */
 } rf_status;
 
 typedef enum rf_dtype { RF_DTYPE_BF16 = 0, RF_DTYPE_F16 = 1, RF_DTYPE_F32 = 2 } rf_dtype;
 
-/* Which kernel family runs.  AUTO picks tcgen05 whenever the shape allows (head_dim 64);
- * SIMT is the generic sm_100a kernel (any head_dim in {32,64,128}), also used as an
- * on-device cross-check in tests.  Neither is a CPU path. */
+/* Which kernel family runs.  AUTO picks tcgen05 whenever the layout allows (every head_dim of the reference
+ * contract, rewrite.cpp:266-269: 64 on the tuned kernels, 32 through the same kernels zero-padded to 64, 128 on
+ * its own kernel); SIMT is the generic CUDA-core sm_100a kernel (unaligned layouts, negative scale), also used as
+ * an on-device cross-check in tests.  Neither is a CPU path. */
 typedef enum rf_kernel { RF_KERNEL_AUTO = 0, RF_KERNEL_TCGEN05 = 1, RF_KERNEL_SIMT = 2 } rf_kernel;
 
 /*
@@ -114,7 +116,7 @@ typedef struct rf_fa_params {
 
 /* Scratch sizes of one call, the analogue of FlashStats (attention.hpp:36-40): all O(S). */
 typedef struct rf_fa_stats {
-    uint64_t workspace_bytes;     /* device workspace the caller must pass (bias + tile flags) */
+    uint64_t workspace_bytes;     /* device workspace the caller must pass (status word, bias + tile flags, schedule state) */
     uint64_t tile_scratch_bytes;  /* on-chip per-CTA scratch (smem + TMEM), independent of S */
     uint64_t row_state_bytes;     /* running max + sum kept in registers: 2*4 bytes per query row */
     uint64_t output_bytes;        /* B*H*S*d*sizeof(out) */
@@ -139,6 +141,25 @@ int rf_fa_stats_query(const rf_fa_params* p, rf_fa_stats* stats);
 /* Launch on `stream` (cudaStream_t as void*).  workspace may be NULL when
  * rf_fa_fwd_workspace_bytes reports 0. */
 int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, void* stream);
+
+/* The launcher's resolved form of one call (the "launcher and workspace allocator" of the operator: the
+ * reference has no counterpart because routefast::flash_attention, attention.cpp:106-213, has nothing to
+ * prepare).  rf_fa_plan_create does what rf_fa_fwd does before its launches -- validation, kernel and schedule
+ * selection, workspace carve-up, the three TMA tensor maps -- once; rf_fa_plan_launch only enqueues the kernels
+ * (asynchronous, any stream, any number of times; thread-safe for concurrent launches as long as concurrent
+ * launches do not share one workspace).  The plan refers to the tensors and the workspace of `p` by address:
+ * they must stay allocated, their contents may change between launches. */
+typedef struct rf_fa_plan rf_fa_plan;
+int rf_fa_plan_create(const rf_fa_params* p, void* workspace, size_t workspace_bytes, rf_fa_plan** plan);
+int rf_fa_plan_launch(const rf_fa_plan* plan, void* stream);
+void rf_fa_plan_destroy(rf_fa_plan* plan);
+
+/* Every wait inside the tcgen05 kernels is bounded.  A wait that runs out (a protocol bug, or a peer CTA that
+ * never got scheduled) does not hang or trap: the kernel raises a status word at the head of the workspace, drains
+ * and exits normally; its output is then invalid.  This call synchronises `stream`, reads the word, and returns
+ * RF_OK or RF_ERR_DEVICE_TIMEOUT (clearing the word).  The CUDA context stays usable either way.  The host entry
+ * points (rf_fa_fwd_host, rf_clf_forward) call it themselves. */
+int rf_fa_launch_status(void* workspace, void* stream);
 
 /* Split-KV softmax merge (the one exchange step of SURVEY 8(e)):
  *   m* = max_g m_g;  O = sum_g O_g 2^(m_g-m*) / sum_g l_g 2^(m_g-m*), 0 where the sum is 0.

@@ -3,12 +3,12 @@
 Public surface mirrors the reference operator interface (see attention.py).  The compute
 path is librf_fa.so (hand-written sm_100a CUDA behind the C ABI in include/rf_fa.h).
 """
-from .attention import (AttentionSpec, FlashStats, RewriteOptions, ShapeMismatch, UnsupportedHeadDim,  # noqa: F401
+from .attention import (AttentionSpec, FaPlan, FlashStats, RewriteOptions, ShapeMismatch, UnsupportedHeadDim,  # noqa: F401
                         WorkspaceAllocator, fa_memory_bytes, flash_attention, fused_flash_attention,
                         kMaskThreshold, kMaskValue, local_window_attrs, mask_memory_bytes, pad_bias_from_mask)
 
 __all__ = [
-    "AttentionSpec", "FlashStats", "RewriteOptions", "ShapeMismatch", "UnsupportedHeadDim", "WorkspaceAllocator",
+    "AttentionSpec", "FaPlan", "FlashStats", "RewriteOptions", "ShapeMismatch", "UnsupportedHeadDim", "WorkspaceAllocator",
     "fa_memory_bytes", "flash_attention", "fused_flash_attention", "kMaskThreshold", "kMaskValue",
     "local_window_attrs", "mask_memory_bytes", "pad_bias_from_mask",
 ]

@@ -12,7 +12,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librf_fa.so")
-SOURCES = ["fa_fwd_sm100.cu", "fa_fwd_sm100_local.cu", "fa_fwd_simt.cu", "fa_aux.cu", "fa_api.cu", "encoder_ops.cu", "clf_runtime.cu",
+SOURCES = ["fa_fwd_sm100.cu", "fa_fwd_sm100_d128.cu", "fa_fwd_sm100_local.cu", "fa_fwd_simt.cu", "fa_aux.cu", "fa_api.cu", "encoder_ops.cu", "clf_runtime.cu",
            # graph layer around the operator: IR, SDPA -> FusedFlashAttention rewriter, GPU executor, C ABI
            os.path.join("graph", "graph_ir.cpp"), os.path.join("graph", "sdpa_rewriter.cpp"),
            os.path.join("graph", "graph_executor.cu"), os.path.join("graph", "graph_capi.cpp")]

@@ -111,9 +111,8 @@ def _check_qkv_shapes(q, k, v) -> None:
         raise ShapeMismatch(capi.RF_ERR_SHAPE, "Q, K, V must have identical shapes")
 
 
-def _device_call(q, k, v, spec: AttentionSpec, stats, out, out_dtype, kernel, flags, kv_range, partials,
-                 debug_scores):
-    lib = capi.load()
+def _device_params(q, k, v, spec: AttentionSpec, out, out_dtype, kernel, flags, kv_range, partials, debug_scores):
+    """rf_fa_params for one call on device tensors; returns (params, out, keep-alive list)."""
     B, H, S, d = q.shape
     if q.dtype not in (torch.bfloat16, torch.float16) or k.dtype != q.dtype or v.dtype != q.dtype:
         raise capi.RfError(capi.RF_ERR_ARG, "device q/k/v must share dtype bfloat16 or float16")
@@ -159,7 +158,22 @@ def _device_call(q, k, v, spec: AttentionSpec, stats, out, out_dtype, kernel, fl
         p.kv_begin, p.kv_end = 0, S  # a partial takes its key range literally ([0, 0) is an empty block)
     if debug_scores is not None:
         p.debug_scores = debug_scores.data_ptr()
+    return p, out, [q, k, v, pb, out, partials, debug_scores]
 
+
+def _fill_stats(stats, st) -> None:
+    stats.workspace_bytes = int(st.workspace_bytes)
+    stats.tile_scratch_bytes = int(st.tile_scratch_bytes)
+    stats.score_matrix_bytes = int(st.score_matrix_bytes)
+    stats.kernel = {1: "tcgen05", 2: "simt"}.get(int(st.kernel), "?")
+    stats.grid_ctas = int(st.grid_ctas)
+
+
+def _device_call(q, k, v, spec: AttentionSpec, stats, out, out_dtype, kernel, flags, kv_range, partials,
+                 debug_scores):
+    lib = capi.load()
+    dev = q.device
+    p, out, _keep = _device_params(q, k, v, spec, out, out_dtype, kernel, flags, kv_range, partials, debug_scores)
     st = capi.RfFaStats()
     capi.check(lib.rf_fa_stats_query(C.byref(p), C.byref(st)))
     stream = torch.cuda.current_stream(dev)
@@ -168,12 +182,55 @@ def _device_call(q, k, v, spec: AttentionSpec, stats, out, out_dtype, kernel, fl
         capi.check(lib.rf_fa_fwd(C.byref(p), ws.data_ptr() if ws is not None else None,
                                  ws.numel() if ws is not None else 0, stream.cuda_stream))
     if stats is not None:
-        stats.workspace_bytes = int(st.workspace_bytes)
-        stats.tile_scratch_bytes = int(st.tile_scratch_bytes)
-        stats.score_matrix_bytes = int(st.score_matrix_bytes)
-        stats.kernel = {1: "tcgen05", 2: "simt"}.get(int(st.kernel), "?")
-        stats.grid_ctas = int(st.grid_ctas)
+        _fill_stats(stats, st)
     return out
+
+
+class FaPlan:
+    """rf_fa_plan (include/rf_fa.h): one call resolved once -- validation, kernel and schedule choice, workspace
+    carve-up, TMA tensor maps -- and launched any number of times on the current stream with no host work
+    beyond the kernel launches.  The plan owns its workspace and keeps the tensors alive; their contents may
+    change between launches, their addresses may not."""
+
+    def __init__(self, q, k, v, spec: Optional[AttentionSpec] = None, *, out: Optional[torch.Tensor] = None,
+                 out_dtype: Optional[torch.dtype] = None, kernel: str = "auto", kv_range=None, partials=None):
+        _check_qkv_shapes(q, k, v)
+        self.lib = capi.load()
+        self.device = q.device
+        spec = spec or AttentionSpec()
+        p, self.out, self._keep = _device_params(q, k, v, spec, out, out_dtype, kernel, 0, kv_range, partials, None)
+        st = capi.RfFaStats()
+        capi.check(self.lib.rf_fa_stats_query(C.byref(p), C.byref(st)))
+        self.stats = FlashStats()
+        _fill_stats(self.stats, st)
+        nbytes = int(st.workspace_bytes)
+        self._ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=self.device)
+        self._h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            capi.check(self.lib.rf_fa_plan_create(C.byref(p), self._ws.data_ptr() if nbytes else None, nbytes,
+                                                  C.byref(self._h)))
+
+    def launch(self) -> torch.Tensor:
+        capi.check(self.lib.rf_fa_plan_launch(self._h, torch.cuda.current_stream(self.device).cuda_stream))
+        return self.out
+
+    def status(self) -> int:
+        """Synchronises the current stream and returns RF_OK or RF_ERR_DEVICE_TIMEOUT (rf_fa_launch_status)."""
+        if self.stats.workspace_bytes == 0:
+            return capi.RF_OK
+        with torch.cuda.device(self.device):
+            return int(self.lib.rf_fa_launch_status(self._ws.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
+
+    def close(self) -> None:
+        if self._h:
+            self.lib.rf_fa_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 def _host_call(q, k, v, spec: AttentionSpec, tile, stats, device_index, compute_dtype):

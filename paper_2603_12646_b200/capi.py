@@ -11,13 +11,15 @@ import os
 from . import _build
 
 RF_OK, RF_ERR_SHAPE, RF_ERR_HEAD_DIM, RF_ERR_ARG, RF_ERR_CUDA, RF_ERR_WORKSPACE, RF_ERR_UNSUPPORTED = range(7)
+RF_ERR_DEVICE_TIMEOUT = 11
 RF_DTYPE_BF16, RF_DTYPE_F16, RF_DTYPE_F32 = 0, 1, 2
 RF_KERNEL_AUTO, RF_KERNEL_TCGEN05, RF_KERNEL_SIMT = 0, 1, 2
 
 # every symbol include/rf_fa.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
     "rf_last_error", "rf_abi_version", "rf_fa_params_init", "rf_fa_validate", "rf_fa_fwd_workspace_bytes",
-    "rf_fa_stats_query", "rf_fa_fwd", "rf_fa_merge", "rf_fa_rescale_partial", "rf_fa_normalize",
+    "rf_fa_stats_query", "rf_fa_fwd", "rf_fa_plan_create", "rf_fa_plan_launch", "rf_fa_plan_destroy",
+    "rf_fa_launch_status", "rf_fa_merge", "rf_fa_rescale_partial", "rf_fa_normalize",
     "rf_pad_bias_from_mask", "rf_cast_f32_to", "rf_cast_to_f32", "rf_fa_fwd_host", "rf_fa_host_release",
     "rf_fused_flash_attention_op", "rf_mask_memory_bytes", "rf_fa_memory_bytes", "rf_device_check",
     "rf_rope_qkv", "rf_add_layernorm", "rf_geglu",
@@ -108,6 +110,14 @@ def load(build_if_missing: bool = True):
     lib.rf_fa_fwd_workspace_bytes.argtypes = [PP, C.POINTER(C.c_size_t)]
     lib.rf_fa_stats_query.argtypes = [PP, C.POINTER(RfFaStats)]
     lib.rf_fa_fwd.argtypes = [PP, vp, C.c_size_t, vp]
+    lib.rf_fa_plan_create.argtypes = [PP, vp, C.c_size_t, C.POINTER(vp)]
+    lib.rf_fa_plan_create.restype = C.c_int
+    lib.rf_fa_plan_launch.argtypes = [vp, vp]
+    lib.rf_fa_plan_launch.restype = C.c_int
+    lib.rf_fa_plan_destroy.argtypes = [vp]
+    lib.rf_fa_plan_destroy.restype = None
+    lib.rf_fa_launch_status.argtypes = [vp, vp]
+    lib.rf_fa_launch_status.restype = C.c_int
     lib.rf_fa_merge.argtypes = [C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), i32, i64, i64, vp, i32, vp]
     lib.rf_fa_rescale_partial.argtypes = [vp, vp, vp, vp, i64, i64, vp]
     lib.rf_fa_normalize.argtypes = [vp, vp, i64, i64, vp, i32, vp]

@@ -522,6 +522,10 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
     auto finish = [&]() -> int {
         cudaEventRecord(s->ev1, st);
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "classifier forward");
+        if (L.ws_bytes > 0) {  // a bounded wait inside an attention kernel ran out: the logits are invalid
+            const int rc_st = rf_fa_launch_status(base + L.ws, st);
+            if (rc_st != RF_OK) return rc_st;
+        }
         cudaEventElapsedTime(&s->last_ms, s->ev0, s->ev1);
         std::memcpy(logits, pin + pin_logits, static_cast<size_t>(B) * c.n_labels * 4);
         return RF_OK;

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <new>
 #include <chrono>
 #include <cstdlib>
 #include <string>
@@ -123,10 +124,12 @@ thread_local HostCtx g_host_ctx[kMaxDevices];
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
 bool strides_ok_tma(const int64_t s[3]) { return s[0] > 0 && s[1] > 0 && s[2] > 0 && s[0] % 8 == 0 && s[1] % 8 == 0 && s[2] % 8 == 0; }
 
-// Can the tcgen05 kernel take this call?  (head_dim 64, scale > 0, TMA-compatible layout.)
+// Can a tcgen05 kernel take this call?  (scale > 0, TMA-compatible layout.)  head_dim 64 has the tuned kernels,
+// 32 runs through the same kernels zero-padded to 64 (the TMA box is 64 wide, the 32 columns outside the tensor
+// arrive as zeros: the call is exponential-bound either way), 128 has its own kernel (fa_fwd_sm100_d128.cu).
 bool tcgen05_eligible(const rf_fa_params* p, const Resolved& r, std::string* why) {
-    if (p->d != 64) {
-        *why = "tcgen05 kernel covers head_dim 64";
+    if (p->d == 128 && !rf::fa_fwd_sm100_d128_available()) {
+        *why = "head_dim 128 tcgen05 kernel is not built in";
         return false;
     }
     if (!(r.scale > 0.0)) {
@@ -173,15 +176,21 @@ int sm_count_or_default() {
     return 148;
 }
 
+constexpr size_t kStatusBlockBytes = 256;  // head of every tcgen05 workspace: the launch status word (ptx.cuh)
+
 struct Plan {
     int kernel;
     bool local;       // tcgen05 only: the narrow-window kernel takes the call
+    bool d128;        // tcgen05 only: head_dim 128 kernel
     int sched_mode;   // tcgen05 only
     int grid;         // CTAs
     int64_t total_pairs, pairs_per_head, tiles_per_pair;
+    size_t status_bytes;
     size_t bias_bytes, flag_bytes_bias, part_bytes;
     size_t qnorm_bytes, kmax_bytes;  // row-max skip test inputs (dense kernel, S >= 1024)
-    size_t workspace_bytes() const { return bias_bytes + flag_bytes_bias + part_bytes + qnorm_bytes + kmax_bytes; }
+    size_t workspace_bytes() const {
+        return status_bytes + bias_bytes + flag_bytes_bias + part_bytes + qnorm_bytes + kmax_bytes;
+    }
 };
 
 Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
@@ -192,15 +201,20 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         pl.grid = static_cast<int>(((p->S + 31) / 32) * p->H * p->B);
         return pl;
     }
+    pl.status_bytes = kStatusBlockBytes;
     pl.pairs_per_head = (p->S + rf::kRowsPerCta - 1) / rf::kRowsPerCta;
     pl.total_pairs = pl.pairs_per_head * p->H * p->B;
+    if (r.partial && r.kv_begin == r.kv_end) {  // empty key block: one fill kernel, no workspace
+        pl.status_bytes = 0;
+        return pl;
+    }
     // narrow sliding window (the reference's local layers): one 256-key strip per query tile, no
     // workspace.  RF_FA_LOCAL=0 routes these calls to the general kernel (A/B measurements).
     static const bool local_enabled = [] {
         const char* env = std::getenv("RF_FA_LOCAL");
         return env == nullptr || env[0] != '0';
     }();
-    if (local_enabled && !r.partial && r.kv_begin == 0 && r.kv_end == p->S && r.wl >= 0 && r.wr >= 0 &&
+    if (p->d != 128 && local_enabled && !r.partial && r.kv_begin == 0 && r.kv_end == p->S && r.wl >= 0 && r.wr >= 0 &&
         r.wl < rf::kBlockN && r.wr < rf::kBlockN && r.wl + r.wr < rf::kBlockN &&
         rf::fa_fwd_sm100_local_covers(static_cast<int>(r.wl), static_cast<int>(r.wr))) {
         pl.local = true;
@@ -232,11 +246,21 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         const char* env = std::getenv("RF_FA_SKIP_MAX");
         return env == nullptr || env[0] != '0';
     }();
+    const int sms = sm_count_or_default();
+    if (p->d == 128) {
+        // head_dim 128: whole pairs only -- one per CTA while they fit a wave (and for split-KV partials),
+        // else dealt round-robin over a persistent grid
+        pl.d128 = true;
+        if (!r.partial && pl.total_pairs > sms) {
+            pl.sched_mode = 2;
+            pl.grid = sms;
+        }
+        return pl;
+    }
     if (skip_max_enabled && p->S >= 1024) {
         pl.qnorm_bytes = align_up(static_cast<size_t>(p->B) * p->H * p->S * sizeof(float), 256);
         pl.kmax_bytes = align_up(static_cast<size_t>(p->B) * p->H * n_kv_tiles(p->S) * sizeof(float), 256);
     }
-    const int sms = sm_count_or_default();
     if (!r.partial && pl.total_pairs > sms) {
         pl.sched_mode = 1;
         pl.grid = sms;
@@ -275,6 +299,8 @@ int make_tmap(CUtensorMap* tm, const void* base, int dtype, int64_t d, int64_t S
                                 static_cast<cuuint64_t>(B)};
     const cuuint64_t strides[3] = {static_cast<cuuint64_t>(st[2]) * 2, static_cast<cuuint64_t>(st[1]) * 2,
                                    static_cast<cuuint64_t>(st[0]) * 2};
+    // box: 64 head-dim columns x 128 rows.  d = 32: the upper 32 columns are out of bounds and arrive as zeros;
+    // d = 128: a tile is two boxes (columns [0,64) and [64,128))
     const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(rf::kBlockN), 1, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUresult res =
@@ -290,6 +316,7 @@ void fill_fa_params(const rf_fa_params* p, const Resolved& r, rf::FaParams* f) {
     f->B = static_cast<int>(p->B);
     f->H = static_cast<int>(p->H);
     f->S = static_cast<int>(p->S);
+    f->d = static_cast<int>(p->d);
     f->kv_begin = static_cast<int>(r.kv_begin);
     f->kv_end = static_cast<int>(r.kv_end);
     f->wl = static_cast<int>(r.wl);
@@ -308,7 +335,182 @@ void fill_fa_params(const rf_fa_params* p, const Resolved& r, rf::FaParams* f) {
     f->debug_scores = p->debug_scores;
 }
 
+// Everything one call needs, resolved once: kernel choice, schedule, workspace carve-up, tensor maps and the
+// pre-pass arguments.  rf_fa_fwd builds one on the stack per call; an rf_fa_plan keeps it, so that steady-state
+// launches do no validation, no planning and no cuTensorMapEncodeTiled (three driver calls) at all.
+struct Launch {
+    int kernel = RF_KERNEL_SIMT;
+    bool empty = false;    // B, H or S is 0: nothing to launch
+    bool neutral = false;  // split-KV partial over an empty key block
+    bool bf16 = true;
+    Plan pl{};
+    rf::FaParams f{};
+    rf::SimtParams sp{};
+    CUtensorMap tmq{}, tmk{}, tmv{};
+    const float* pad_bias = nullptr;  // raw [B,S]
+    // pre-pass
+    float* bias2 = nullptr;
+    uint8_t* tile_flags = nullptr;
+    bool norms = false;
+    const void* q = nullptr;
+    const void* k = nullptr;
+    long long qs[3] = {0, 0, 0}, ks[3] = {0, 0, 0};
+    int dtype = 0;
+    float* qnorm = nullptr;
+    float* kmax = nullptr;
+    int* zero_ptr = nullptr;
+    int zero_words = 0;
+    void* memset_ptr = nullptr;
+    size_t memset_bytes = 0;
+    // neutral partial
+    float* o_partial = nullptr;
+    float* m_partial = nullptr;
+    float* l_partial = nullptr;
+    long long rows = 0;
+    int d = 0;
+};
+
+int build_launch(const rf_fa_params* p, void* workspace, size_t workspace_bytes, Launch* L) {
+    Resolved r;
+    int rc = validate(p, &r);
+    if (rc != RF_OK) return rc;
+    int kernel;
+    rc = select_kernel(p, r, &kernel);
+    if (rc != RF_OK) return rc;
+    L->kernel = kernel;
+    if (p->B == 0 || p->H == 0 || p->S == 0) {
+        L->empty = true;
+        return RF_OK;
+    }
+    L->bf16 = p->dtype == RF_DTYPE_BF16;
+    L->d = static_cast<int>(p->d);
+    if (r.partial && r.kv_begin == r.kv_end) {  // empty key block: the neutral element of the merge
+        L->neutral = true;
+        L->o_partial = p->o_partial;
+        L->m_partial = p->m_partial;
+        L->l_partial = p->l_partial;
+        L->rows = static_cast<long long>(p->B) * p->H * p->S;
+        return RF_OK;
+    }
+    rf::FaParams& f = L->f;
+    fill_fa_params(p, r, &f);
+    L->pad_bias = p->pad_bias;
+
+    if (kernel == RF_KERNEL_SIMT) {
+        rf::SimtParams& sp = L->sp;
+        std::memset(&sp, 0, sizeof(sp));
+        sp.q = p->q;
+        sp.k = p->k;
+        sp.v = p->v;
+        sp.q_sb = r.qs[0]; sp.q_sh = r.qs[1]; sp.q_ss = r.qs[2];
+        sp.k_sb = r.ks[0]; sp.k_sh = r.ks[1]; sp.k_ss = r.ks[2];
+        sp.v_sb = r.vs[0]; sp.v_sh = r.vs[1]; sp.v_ss = r.vs[2];
+        sp.in_dtype = p->dtype;
+        sp.d = static_cast<int>(p->d);
+        sp.f = f;
+        sp.f.bias2 = p->pad_bias;  // raw [B,S] bias; see launch_fa_fwd_simt
+        return RF_OK;
+    }
+
+    // ---- tcgen05 path ----
+    const Plan pl = make_plan(p, r, kernel);
+    L->pl = pl;
+    const size_t need = pl.workspace_bytes();
+    if (need > 0) {
+        if (workspace == nullptr || workspace_bytes < need)
+            return fail(RF_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+        if (!aligned16(workspace)) return fail(RF_ERR_WORKSPACE, "workspace must be 16-byte aligned");
+    }
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    f.status = reinterpret_cast<int*>(ws);
+    ws += pl.status_bytes;
+    if ((rc = make_tmap(&L->tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
+    if ((rc = make_tmap(&L->tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
+    if ((rc = make_tmap(&L->tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
+    if (pl.local) return RF_OK;
+    if (pl.bias_bytes > 0) {
+        L->bias2 = reinterpret_cast<float*>(ws);
+        L->tile_flags = ws + pl.bias_bytes;
+        f.bias2 = L->bias2;
+        f.tile_flags = L->tile_flags;
+    }
+    f.sched_mode = pl.sched_mode;
+    f.total_pairs = static_cast<int>(pl.total_pairs);
+    f.pairs_per_head = static_cast<int>(pl.pairs_per_head);
+    f.tiles_per_pair = static_cast<int>(pl.tiles_per_pair);
+    if (pl.sched_mode == 1) {
+        // split-pair flag block: zeroed by the norms pre-pass when that runs, else by a memset node
+        void* flag_ptr = nullptr;
+        size_t flag_bytes = 0;
+        rf::fa_fwd_sm100_partial_carve(ws + pl.bias_bytes + pl.flag_bytes_bias, pl.grid, &f, &flag_ptr, &flag_bytes);
+        if (pl.qnorm_bytes > 0) {
+            L->zero_ptr = static_cast<int*>(flag_ptr);
+            L->zero_words = static_cast<int>(flag_bytes / sizeof(int));
+        } else {
+            L->memset_ptr = flag_ptr;
+            L->memset_bytes = flag_bytes;
+        }
+    }
+    if (pl.qnorm_bytes > 0) {
+        uint8_t* nb = ws + pl.bias_bytes + pl.flag_bytes_bias + pl.part_bytes;
+        L->norms = true;
+        L->q = p->q;
+        L->k = p->k;
+        for (int i = 0; i < 3; ++i) {
+            L->qs[i] = r.qs[i];
+            L->ks[i] = r.ks[i];
+        }
+        L->dtype = p->dtype;
+        L->qnorm = reinterpret_cast<float*>(nb);
+        L->kmax = reinterpret_cast<float*>(nb + pl.qnorm_bytes);
+        f.qnorm = L->qnorm;
+        f.kmax = L->kmax;
+    }
+    return RF_OK;
+}
+
+int run_launch(const Launch& L, cudaStream_t stream) {
+    if (L.empty) return RF_OK;
+    cudaError_t e;
+    if (L.neutral) {
+        e = rf::launch_partial_neutral(L.o_partial, L.m_partial, L.l_partial, L.rows, L.d, stream);
+        return e == cudaSuccess ? RF_OK : cuda_fail(e, "partial_neutral launch");
+    }
+    if (L.kernel == RF_KERNEL_SIMT) {
+        int grid = 0;
+        e = rf::launch_fa_fwd_simt(L.sp, stream, &grid);
+        return e == cudaSuccess ? RF_OK : cuda_fail(e, "fa_fwd_simt launch");
+    }
+    const rf::FaParams& f = L.f;
+    if (L.pl.local) {
+        e = rf::launch_fa_fwd_sm100_local(L.tmq, L.tmk, L.tmv, f, L.pad_bias, L.bf16, L.pl.grid, stream);
+        return e == cudaSuccess ? RF_OK : cuda_fail(e, "fa_fwd_sm100_local launch");
+    }
+    if (L.bias2 != nullptr) {
+        e = rf::launch_bias_prepare(L.pad_bias, f.B, f.S, L.bias2, L.tile_flags, f.n_kv_tiles, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "bias_prepare launch");
+    }
+    if (L.memset_bytes > 0) {
+        e = cudaMemsetAsync(L.memset_ptr, 0, L.memset_bytes, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(partial flags)");
+    }
+    if (L.norms) {
+        e = rf::launch_qk_norms(L.q, L.k, L.qs, L.ks, L.dtype, f.B, f.H, f.S, f.d, f.n_kv_tiles, L.qnorm, L.kmax, L.zero_ptr,
+                                L.zero_words, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "qk_norms launch");
+    }
+    if (L.pl.d128)
+        e = rf::launch_fa_fwd_sm100_d128(L.tmq, L.tmk, L.tmv, f, L.bf16, L.pl.grid, stream);
+    else
+        e = rf::launch_fa_fwd_sm100(L.tmq, L.tmk, L.tmv, f, L.bf16, L.pl.grid, stream, /*pdl=*/L.norms);
+    return e == cudaSuccess ? RF_OK : cuda_fail(e, "fa_fwd_sm100 launch");
+}
+
 }  // namespace
+
+struct rf_fa_plan {
+    Launch launch;
+};
 
 namespace rf {
 int set_last_error(int code, const std::string& message) { return fail(code, message); }
@@ -373,108 +575,47 @@ int rf_fa_stats_query(const rf_fa_params* p, rf_fa_stats* st) {
 }
 
 int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, void* stream_v) {
-    Resolved r;
-    int rc = validate(p, &r);
+    Launch L;
+    const int rc = build_launch(p, workspace, workspace_bytes, &L);
     if (rc != RF_OK) return rc;
-    int kernel;
-    rc = select_kernel(p, r, &kernel);
-    if (rc != RF_OK) return rc;
-    if (p->B == 0 || p->H == 0 || p->S == 0) return RF_OK;
-    cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
-    if (r.partial && r.kv_begin == r.kv_end) {  // empty key block: the neutral element of the merge
-        cudaError_t e = rf::launch_partial_neutral(p->o_partial, p->m_partial, p->l_partial, p->B * p->H * p->S,
-                                                   static_cast<int>(p->d), stream);
-        if (e != cudaSuccess) return cuda_fail(e, "partial_neutral launch");
-        return RF_OK;
-    }
+    return run_launch(L, static_cast<cudaStream_t>(stream_v));
+}
 
-    rf::FaParams f;
-    fill_fa_params(p, r, &f);
-    int grid = 0;
-    (void)grid;
-
-    if (kernel == RF_KERNEL_SIMT) {
-        rf::SimtParams sp;
-        std::memset(&sp, 0, sizeof(sp));
-        sp.q = p->q;
-        sp.k = p->k;
-        sp.v = p->v;
-        sp.q_sb = r.qs[0]; sp.q_sh = r.qs[1]; sp.q_ss = r.qs[2];
-        sp.k_sb = r.ks[0]; sp.k_sh = r.ks[1]; sp.k_ss = r.ks[2];
-        sp.v_sb = r.vs[0]; sp.v_sh = r.vs[1]; sp.v_ss = r.vs[2];
-        sp.in_dtype = p->dtype;
-        sp.d = static_cast<int>(p->d);
-        sp.f = f;
-        sp.f.bias2 = p->pad_bias;  // raw [B,S] bias; see launch_fa_fwd_simt
-        cudaError_t e = rf::launch_fa_fwd_simt(sp, stream, &grid);
-        if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_simt launch");
-        return RF_OK;
+int rf_fa_plan_create(const rf_fa_params* p, void* workspace, size_t workspace_bytes, rf_fa_plan** plan) {
+    if (plan == nullptr) return fail(RF_ERR_ARG, "plan is null");
+    *plan = nullptr;
+    rf_fa_plan* pl = new (std::nothrow) rf_fa_plan();
+    if (pl == nullptr) return fail(RF_ERR_ARG, "out of host memory");
+    const int rc = build_launch(p, workspace, workspace_bytes, &pl->launch);
+    if (rc != RF_OK) {
+        delete pl;
+        return rc;
     }
-
-    // ---- tcgen05 path ----
-    const Plan pl = make_plan(p, r, kernel);
-    if (pl.local) {
-        CUtensorMap tmq, tmk, tmv;
-        if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
-        if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
-        if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
-        cudaError_t e = rf::launch_fa_fwd_sm100_local(tmq, tmk, tmv, f, p->pad_bias, p->dtype == RF_DTYPE_BF16, pl.grid,
-                                                      stream);
-        if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100_local launch");
-        return RF_OK;
-    }
-    const size_t need = pl.workspace_bytes();
-    if (need > 0) {
-        if (workspace == nullptr || workspace_bytes < need)
-            return fail(RF_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
-        if (!aligned16(workspace)) return fail(RF_ERR_WORKSPACE, "workspace must be 16-byte aligned");
-    }
-    uint8_t* ws = static_cast<uint8_t*>(workspace);
-    if (pl.bias_bytes > 0) {
-        float* bias2 = reinterpret_cast<float*>(ws);
-        uint8_t* flags = ws + pl.bias_bytes;
-        cudaError_t e = rf::launch_bias_prepare(p->pad_bias, f.B, f.S, bias2, flags, f.n_kv_tiles, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "bias_prepare launch");
-        f.bias2 = bias2;
-        f.tile_flags = flags;
-    }
-    f.sched_mode = pl.sched_mode;
-    f.total_pairs = static_cast<int>(pl.total_pairs);
-    f.pairs_per_head = static_cast<int>(pl.pairs_per_head);
-    f.tiles_per_pair = static_cast<int>(pl.tiles_per_pair);
-    int* zero_ptr = nullptr;  // split-pair flag block: zeroed by the norms pre-pass when that runs, else by a memset
-    int zero_words = 0;
-    if (pl.sched_mode == 1) {
-        void* flag_ptr = nullptr;
-        size_t flag_bytes = 0;
-        rf::fa_fwd_sm100_partial_carve(ws + pl.bias_bytes + pl.flag_bytes_bias, pl.grid, &f, &flag_ptr, &flag_bytes);
-        if (pl.qnorm_bytes > 0) {
-            zero_ptr = static_cast<int*>(flag_ptr);
-            zero_words = static_cast<int>(flag_bytes / sizeof(int));
-        } else {
-            cudaError_t e = cudaMemsetAsync(flag_ptr, 0, flag_bytes, stream);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(partial flags)");
-        }
-    }
-    if (pl.qnorm_bytes > 0) {
-        uint8_t* nb = ws + pl.bias_bytes + pl.flag_bytes_bias + pl.part_bytes;
-        float* qnorm = reinterpret_cast<float*>(nb);
-        float* kmax = reinterpret_cast<float*>(nb + pl.qnorm_bytes);
-        const long long qs[3] = {r.qs[0], r.qs[1], r.qs[2]}, ks[3] = {r.ks[0], r.ks[1], r.ks[2]};
-        cudaError_t e = rf::launch_qk_norms(p->q, p->k, qs, ks, p->dtype, f.B, f.H, f.S, f.n_kv_tiles, qnorm, kmax, zero_ptr,
-                                            zero_words, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "qk_norms launch");
-        f.qnorm = qnorm;
-        f.kmax = kmax;
-    }
-    CUtensorMap tmq, tmk, tmv;
-    if ((rc = make_tmap(&tmq, p->q, p->dtype, p->d, p->S, p->H, p->B, r.qs)) != RF_OK) return rc;
-    if ((rc = make_tmap(&tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
-    if ((rc = make_tmap(&tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
-    cudaError_t e = rf::launch_fa_fwd_sm100(tmq, tmk, tmv, f, p->dtype == RF_DTYPE_BF16, pl.grid, stream,
-                                            /*pdl=*/pl.qnorm_bytes > 0);
-    if (e != cudaSuccess) return cuda_fail(e, "fa_fwd_sm100 launch");
+    *plan = pl;
     return RF_OK;
+}
+
+int rf_fa_plan_launch(const rf_fa_plan* plan, void* stream) {
+    if (plan == nullptr) return fail(RF_ERR_ARG, "plan is null");
+    return run_launch(plan->launch, static_cast<cudaStream_t>(stream));
+}
+
+void rf_fa_plan_destroy(rf_fa_plan* plan) { delete plan; }
+
+int rf_fa_launch_status(void* workspace, void* stream_v) {
+    if (workspace == nullptr) return RF_OK;  // kernels without a workspace have no cross-warp waits to time out
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+    uint32_t word = 0;
+    cudaError_t e = cudaMemcpyAsync(&word, workspace, sizeof(word), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return cuda_fail(e, "launch status read");
+    if ((word & 0xffff0000u) != rf::kLaunchStatusMagic) return RF_OK;
+    cudaMemsetAsync(workspace, 0, sizeof(word), stream);  // reported once
+    const unsigned code = (word >> 12) & 0xfu, cta = word & 0xfffu;
+    return fail(RF_ERR_DEVICE_TIMEOUT,
+                std::string(code == 2 ? "a CTA timed out waiting for the partial of its predecessor"
+                                      : "a barrier wait inside a CTA timed out") +
+                    " (CTA " + std::to_string(cta) + "); the output of that launch is invalid");
 }
 
 int rf_fa_merge(const float* const* o_parts, const float* const* m_parts, const float* const* l_parts, int32_t G,
@@ -753,6 +894,8 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
     }
     lap("enqueued");
     for (int i = 0; i < n_streams; ++i) RF_TRY_CUDA(cudaStreamSynchronize(streams[i]), "stream sync");
+    for (int i = 0; i < n_streams; ++i)
+        if (d_ws[i] != nullptr) RF_TRY_RC(rf_fa_launch_status(d_ws[i], streams[i]));
     lap("synced");
     if (d_out_full != nullptr) RF_TRY_CUDA(cudaMemcpy(out, d_out_full, nb32, cudaMemcpyDeviceToHost), "D2H copy");
 #undef RF_TRY_CUDA

@@ -57,7 +57,7 @@ __device__ __forceinline__ float sumsq8(const uint4& v) {
 template <bool kBf16>
 __global__ void __launch_bounds__(128) qk_norms_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
                                                        long long q_sb, long long q_sh, long long q_ss, long long k_sb,
-                                                       long long k_sh, long long k_ss, int H, int S, int n_kv_tiles,
+                                                       long long k_sh, long long k_ss, int H, int S, int d, int n_kv_tiles,
                                                        float* __restrict__ qnorm, float* __restrict__ kmax,
                                                        int* __restrict__ zero_ptr, int zero_words) {
     __shared__ float red[4];
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(128) qk_norms_kernel(const uint16_t* __restric
     for (int pass = 0; pass < kPasses; ++pass) {
         const int row = n * kBlockN + pass * 16 + rgrp;
         qv[pass] = kv[pass] = make_uint4(0u, 0u, 0u, 0u);
-        if (row < S) {
+        if (row < S && sub * 8 < d) {  // head_dim 32: rows are four 16-byte chunks
             qv[pass] = __ldg(reinterpret_cast<const uint4*>(qb + row * q_ss));
             kv[pass] = __ldg(reinterpret_cast<const uint4*>(kb + row * k_ss));
         }
@@ -258,16 +258,16 @@ cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias
 }
 
 cudaError_t launch_qk_norms(const void* q, const void* k, const long long qs[3], const long long ks[3], int dtype, int B,
-                            int H, int S, int n_kv_tiles, float* qnorm, float* kmax, int* zero_ptr, int zero_words,
+                            int H, int S, int d, int n_kv_tiles, float* qnorm, float* kmax, int* zero_ptr, int zero_words,
                             cudaStream_t stream) {
     dim3 grid(n_kv_tiles, H, B);
     const uint16_t* q16 = static_cast<const uint16_t*>(q);
     const uint16_t* k16 = static_cast<const uint16_t*>(k);
     if (dtype == 0)
-        qk_norms_kernel<true><<<grid, kBlockN, 0, stream>>>(q16, k16, qs[0], qs[1], qs[2], ks[0], ks[1], ks[2], H, S,
+        qk_norms_kernel<true><<<grid, kBlockN, 0, stream>>>(q16, k16, qs[0], qs[1], qs[2], ks[0], ks[1], ks[2], H, S, d,
                                                                       n_kv_tiles, qnorm, kmax, zero_ptr, zero_words);
     else
-        qk_norms_kernel<false><<<grid, kBlockN, 0, stream>>>(q16, k16, qs[0], qs[1], qs[2], ks[0], ks[1], ks[2], H, S,
+        qk_norms_kernel<false><<<grid, kBlockN, 0, stream>>>(q16, k16, qs[0], qs[1], qs[2], ks[0], ks[1], ks[2], H, S, d,
                                                                n_kv_tiles, qnorm, kmax, zero_ptr, zero_words);
     return cudaGetLastError();
 }

@@ -1,5 +1,6 @@
 // fa_fwd_sm100.cu -- FusedFlashAttention forward for sm_100a (B200), head_dim 64.
 //
+// (head_dim 32 runs through the same kernel zero-padded to 64: see FaParams::d.)
 // Semantics: reference routefast::flash_attention (proj/core/src/attention.cpp:106-213):
 // non-causal, additive padding bias (masked at <= -30000), optional two-sided sliding window,
 // online softmax, rows without a live key -> 0.  No S x S tensor is ever materialised.
@@ -27,12 +28,14 @@
 // Work distribution.  A work item is (query-tile pair, key-tile range).
 //   mode 0: one item per CTA (grid = number of pairs); used when the pairs fit one wave and for split-KV.
 //   mode 1: persistent, statically balanced: the flat (pair x key-tile) iteration space is cut
-//           into gridDim.x equal contiguous slices.  A pair cut between CTA c (its first key
-//           tiles, processed LAST by c) and CTA c+1 (its remaining key tiles, processed FIRST by
-//           c+1) is merged in-kernel: c+1 publishes an un-normalised partial (O, m, l) to the
-//           workspace, c combines it with its own in a fixed order.  This removes the wave
-//           quantisation of the dense global layers (e.g. 384 pairs on 148 SMs) and stays
-//           run-to-run deterministic.
+//           into gridDim.x equal contiguous slices, each walked from its LAST pair to its first.
+//           A pair cut between CTA c (its leading key tiles: c's first item) and CTA c+1 (its
+//           trailing key tiles: c+1's last item) is merged in-kernel: c publishes an un-normalised
+//           partial (O, m, l) to the workspace right away, c+1 combines it with its own in a fixed
+//           order at the very end.  A CTA therefore only ever waits for a LOWER-indexed CTA (dispatched
+//           no later than itself), so the chain cannot starve when other work shares the GPU.  This
+//           removes the wave quantisation of the dense global layers (e.g. 384 pairs on 148 SMs) and
+//           stays run-to-run deterministic.
 //   mode 2: persistent, whole pairs dealt round-robin (pair c, c + gridDim.x, ...): batches whose last
 //           partial round wastes little (fa_api.cu).  CTAs that run together work on neighbouring pairs (K/V of a few heads stay in
 //           L2), and sequences of different padded lengths spread over all CTAs.
@@ -135,9 +138,14 @@ enum : uint32_t {
     kBarTurn = kBarOFull + 2,            // [2 tiles][4 quadrants] exp-phase turn of (tile, SM sub-partition)
     kNumBars = kBarTurn + 8,
 };
-static_assert(kNumBars * 8 + 8 <= Smem::bar_bytes, "barrier block too small");
+constexpr uint32_t kTmemSlotOff = kNumBars * 8;                     // u32: TMEM base address
+constexpr uint32_t kWaitBlockOff = (kTmemSlotOff + 8 + 15) & ~15u;  // 16 bytes: abort word + status pointer (ptx.cuh)
+static_assert(kWaitBlockOff + 16 <= Smem::bar_bytes, "barrier block too small");
 
-enum : int { kItemFull = 0, kItemHeadPart = 1, kItemTailPart = 2 };
+// kItemPublish: the CTA owns the LEADING key tiles of a pair cut at the end of its slice: processed first, partial
+// published for the next CTA.  kItemMerge: it owns the TRAILING key tiles of the pair its slice starts in:
+// processed last, merged with the partial of the previous CTA.
+enum : int { kItemFull = 0, kItemPublish = 1, kItemMerge = 2 };
 
 // One unit of work of a CTA: a query-tile pair and a range of key tiles.
 struct Item {
@@ -149,7 +157,7 @@ struct Item {
 };
 
 struct Sched {
-    long long t, t_end;  // mode 1: flat (pair, key tile) cursor
+    long long t, t_end;  // mode 1: the unprocessed part [t, t_end) of the CTA's slice, consumed from the END
     bool done;           // mode 0
 };
 
@@ -173,13 +181,17 @@ template <bool kHasBias>
 __device__ __forceinline__ bool next_item(const FaParams& p, Sched& s, Item& it) {
     int pair_lin, k0 = 0, k1 = 0x7fffffff;
     if (p.sched_mode == 1) {
+        // The slice is walked from its last pair to its first, so that the piece shared with the NEXT CTA is
+        // published before anything else and the piece shared with the PREVIOUS CTA is merged last: a CTA only
+        // ever waits for a lower-indexed -- i.e. earlier-dispatched -- CTA, and that one published long ago.
         if (s.t >= s.t_end) return false;
         const int K = p.tiles_per_pair;  // virtual key tiles per pair (upper bound of any pair's range)
-        pair_lin = static_cast<int>(s.t / K);
-        k0 = static_cast<int>(s.t - static_cast<long long>(pair_lin) * K);
-        k1 = static_cast<int>(min(static_cast<long long>(K), k0 + (s.t_end - s.t)));
-        s.t += k1 - k0;
-        it.kind = k0 > 0 ? kItemHeadPart : (k1 < K ? kItemTailPart : kItemFull);
+        pair_lin = static_cast<int>((s.t_end - 1) / K);
+        const long long pair_start = static_cast<long long>(pair_lin) * K;
+        k0 = static_cast<int>(max(s.t, pair_start) - pair_start);
+        k1 = static_cast<int>(s.t_end - pair_start);
+        s.t_end = pair_start + k0;
+        it.kind = k0 > 0 ? kItemMerge : (k1 < K ? kItemPublish : kItemFull);
     } else if (p.sched_mode == 2) {
         // whole pairs dealt round-robin: pair blockIdx.x, blockIdx.x + gridDim.x, ...  (s.t counts items)
         const long long lin = blockIdx.x + s.t * gridDim.x;
@@ -228,8 +240,9 @@ __device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
 // so "S ready" does not imply that PV of the previous tile has finished.  The V-empty barrier of
 // that tile is committed after both of its PVs: wait for its phase first (it is at most one phase
 // away, so the parity wait is exact).
-__device__ __noinline__ void rescale_o_rows(uint32_t t_o, float alpha, uint32_t v_empty_bar, uint32_t parity) {
-    mbar_wait(v_empty_bar, parity);
+__device__ __noinline__ void rescale_o_rows(uint32_t t_o, float alpha, uint32_t v_empty_bar, uint32_t parity,
+                                            WaitCtx wctx) {
+    mbar_wait(v_empty_bar, parity, wctx);
     tc_fence_after();
     uint32_t o[32];
     tmem_ld32(t_o, o);
@@ -255,8 +268,8 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     asm volatile("mov.u32 %0, %0;" : "+r"(smem_base));  // keep in a register: do not rematerialise
     const uint32_t bars = smem_base + Smem::bars;
     auto bar = [&](uint32_t i) { return bars + 8u * i; };
-    volatile uint32_t* tmem_slot =
-        reinterpret_cast<volatile uint32_t*>(smem_gen + Smem::bars + 8 * kNumBars);
+    volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_gen + Smem::bars + kTmemSlotOff);
+    const WaitCtx wctx{bars + kWaitBlockOff};
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -282,6 +295,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
         for (int x = 0; x < 2; ++x) mbar_init(bar(kBarOFull + x), 1);
         for (int i = 0; i < 8; ++i) mbar_init(bar(kBarTurn + i), 64);  // both warps of the other tile arrive
+        wait_block_init(wctx.block_smem, p.status);
         fence_barrier_init();
     }
     if (warp == kMmaWarp) {
@@ -314,7 +328,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         while (next_item<kHasBias>(p, sched, item)) {
             if (item.num_live == 0) continue;
             const int b = item.b, h = item.h;
-            mbar_wait(bar(kBarQEmpty), (qi & 1) ^ 1);
+            mbar_wait(bar(kBarQEmpty), (qi & 1) ^ 1, wctx);
             if (leader) {
                 mbar_arrive_expect_tx(bar(kBarQFull), item.has_b ? 2 * kTileBytes : kTileBytes);
                 tma_load_4d(smem_base + Smem::q, &tm_q, bar(kBarQFull), 0, item.q0, h, b);
@@ -326,7 +340,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // K runs two tiles ahead of V: QK^T of tile t+2 is issued while tile t is in softmax
             auto load_k = [&](int n) {
                 const uint32_t st = kc % kStagesK;
-                mbar_wait(bar(kBarKEmpty + st), ((kc / kStagesK) & 1) ^ 1);
+                mbar_wait(bar(kBarKEmpty + st), ((kc / kStagesK) & 1) ^ 1, wctx);
                 if (leader) {
                     mbar_arrive_expect_tx(bar(kBarKFull + st), kTileBytes);
                     tma_load_4d(smem_base + Smem::k + st * kTileBytes, &tm_k, bar(kBarKFull + st), 0, n * kBlockN, h, b);
@@ -336,7 +350,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             };
             auto load_v = [&](int n) {
                 const uint32_t st = vc % kStagesV;
-                mbar_wait(bar(kBarVEmpty + st), ((vc / kStagesV) & 1) ^ 1);
+                mbar_wait(bar(kBarVEmpty + st), ((vc / kStagesV) & 1) ^ 1, wctx);
                 if (leader) {
                     mbar_arrive_expect_tx(bar(kBarVFull + st), kTileBytes);
                     tma_load_4d(smem_base + Smem::v + st * kTileBytes, &tm_v, bar(kBarVFull + st), 0, n * kBlockN, h, b);
@@ -440,7 +454,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // in the steady state the softmax warps check them before they publish P (see there), so
             // that this loop has exactly two waits per key tile.
             auto wait_k = [&](uint32_t i) {
-                mbar_wait(bar(kBarKFull + ((kc + i) & (kStagesK - 1))), ((kc + i) / kStagesK) & 1);
+                mbar_wait(bar(kBarKFull + ((kc + i) & (kStagesK - 1))), ((kc + i) / kStagesK) & 1, wctx);
                 tc_fence_after();
             };
             static_assert((kStagesK & (kStagesK - 1)) == 0, "K ring depth must be a power of two");
@@ -454,7 +468,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             uint32_t buf_a = sa;                        // S buffer of A(i); B(i) uses the next one
             uint32_t ks1 = inc_mod(ks, 1, kStagesK);    // K stage of tile i+1
             uint32_t vsi = vs, vpi = vp;                // V stage of tile i and its phase parity
-            mbar_wait(bar(kBarQFull), qi & 1);
+            mbar_wait(bar(kBarQFull), qi & 1, wctx);
             wait_k(0);
             issue_qk(0, ks, buf_a);
             if (has_b) issue_qk(1, ks, inc_mod(buf_a, 1, kSBufs));
@@ -480,9 +494,9 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 pin(ta);
                 RF_STAMP(1);
                 if (!RF_FA_VK_IN_SOFTMAX)  // V(i) was requested tiles ago: check it in the shadow of the P wait
-                    mbar_wait2(bar(kBarVFull + vsi), vpi, bar(kBarPFull + buf_a), (par_bits >> buf_a) & 1u);
+                    mbar_wait2(bar(kBarVFull + vsi), vpi, bar(kBarPFull + buf_a), (par_bits >> buf_a) & 1u, wctx);
                 else
-                    mbar_wait(bar(kBarPFull + buf_a), (par_bits >> buf_a) & 1u);  // implies V(i) has landed
+                    mbar_wait(bar(kBarPFull + buf_a), (par_bits >> buf_a) & 1u, wctx);  // implies V(i) has landed
                 tc_fence_after();
                 RF_STAMP(2);
                 issue_pv(0, vlo, ta, i > 0 ? 1u : 0u);
@@ -498,9 +512,9 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     pin(ta);
                     if (!RF_FA_VK_IN_SOFTMAX && i + 2 < num_live)  // K(i+2) for the S_A(i+2) issued right after
                         mbar_wait2(bar(kBarKFull + ks2), ((kc + i + 2) / kStagesK) & 1,
-                                   bar(kBarPFull + buf_b), (par_bits >> buf_b) & 1u);
+                                   bar(kBarPFull + buf_b), (par_bits >> buf_b) & 1u, wctx);
                     else
-                        mbar_wait(bar(kBarPFull + buf_b), (par_bits >> buf_b) & 1u);  // implies K(i+2) has landed
+                        mbar_wait(bar(kBarPFull + buf_b), (par_bits >> buf_b) & 1u, wctx);  // implies K(i+2) has landed
                     tc_fence_after();
                     RF_STAMP(4);
                     issue_pv(1, vlo, ta, i > 0 ? 1u : 0u);
@@ -549,6 +563,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         constexpr uint32_t kPairThreads = 64;
         uint32_t bars_r = bars;
         asm volatile("mov.u32 %0, %0;" : "+r"(bars_r));
+        const WaitCtx wctx{bars_r + kWaitBlockOff};  // (shadows the outer one: derived from the pinned register)
 
         uint32_t oi = 0;    // items this warpgroup worked on so far (O-full barrier phase)
         uint32_t vc = 0;    // V tiles consumed by the tensor pipe in earlier items (V ring position)
@@ -616,13 +631,13 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     // for S, long before it publishes P.
                     if (RF_FA_VK_IN_SOFTMAX) {
                         const uint32_t tv = vc + static_cast<uint32_t>(it);
-                        if (x == 0) mbar_wait(bars_r + 8u * (kBarVFull + tv % kStagesV), (tv / kStagesV) & 1u);
+                        if (x == 0) mbar_wait(bars_r + 8u * (kBarVFull + tv % kStagesV), (tv / kStagesV) & 1u, wctx);
                         if ((x == 1 || !item.has_b) && it + 2 < num_live)
                             mbar_wait(bars_r + 8u * (kBarKFull + ((tv + 2u) & (kStagesK - 1))),
-                                      ((tv + 2u) / kStagesK) & 1u);
+                                      ((tv + 2u) / kStagesK) & 1u, wctx);
                     }
                     RF_STAMP(0);
-                    mbar_wait(bars_r + 8u * (kBarSFull + sb), (par_bits >> sb) & 1u);
+                    mbar_wait(bars_r + 8u * (kBarSFull + sb), (par_bits >> sb) & 1u, wctx);
                     tc_fence_after();
                     RF_STAMP(1);
 
@@ -744,7 +759,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             tmem_st16(t_s + hf * kHalfN + cb * 16, pk);  // each half keeps P inside its own S columns
                         }
                     };
-                    if (kPingPong) mbar_wait(turn_mine, tn & 1u);
+                    if (kPingPong) mbar_wait(turn_mine, tn & 1u, wctx);
                     if (kEmuEvery > 0 && full)
                         exp_store(std::true_type{});
                     else
@@ -764,7 +779,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     if (!skip_max && it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
                         const uint32_t vprev = vc + static_cast<uint32_t>(it) - 1u;
                         rescale_o_rows(t_o, alpha, bars_r + 8u * (kBarVEmpty + vprev % kStagesV),
-                                       (vprev / kStagesV) & 1u);
+                                       (vprev / kStagesV) & 1u, wctx);
                     }
                     tc_wait_st();
 #endif  // !RF_FA_MMAONLY
@@ -790,7 +805,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 for (int i = 0; i < num_live; ++i) {
                     par_bits ^= 1u << ((g - 1u + 2u * i) % kSBufs);
                     if (kPingPong) {  // keep the turn protocol going: pass every turn straight back
-                        mbar_wait(turn_mine, tn & 1u);
+                        mbar_wait(turn_mine, tn & 1u, wctx);
                         mbar_arrive(turn_other);
                         ++tn;
                     }
@@ -814,7 +829,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const int col0 = hf * kOutCols;
                 float o[kOutCols];
                 if (num_live > 0) {
-                    mbar_wait(bars_r + 8u * (kBarOFull + x), oi & 1u);
+                    mbar_wait(bars_r + 8u * (kBarOFull + x), oi & 1u, wctx);
                     tc_fence_after();
                     tmem_ld32(t_o, reinterpret_cast<uint32_t(&)[32]>(o));
                     tc_wait_ld();
@@ -823,9 +838,9 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     for (int u = 0; u < kOutCols; ++u) o[u] = 0.f;
                 }
 
-                if (item.kind == kItemHeadPart) {
-                    // this CTA owns only the trailing key tiles of the pair: publish an un-normalised
-                    // partial for CTA blockIdx.x - 1, which holds the leading key tiles
+                if (item.kind == kItemPublish) {
+                    // this CTA owns only the leading key tiles of the pair: publish an un-normalised partial
+                    // for CTA blockIdx.x + 1, which holds the trailing key tiles and merges at the end of its slice
                     const size_t slot = (static_cast<size_t>(blockIdx.x) * 2 + x) * kBlockM + r;
                     float4* dst = reinterpret_cast<float4*>(p.part_o + slot * kHeadDim + col0);
 #pragma unroll
@@ -839,17 +854,18 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     __syncwarp();
                     if (lane == 0) st_release_gpu(p.part_flag + blockIdx.x * kNumSoftmaxWarps + warp, 1);
                 } else {
-                    if (item.kind == kItemTailPart) {
-                        // merge with the partial CTA blockIdx.x + 1 published for the same rows (its
-                        // half-0 warp of the same quadrant wrote m and l, this warp's twin wrote the
-                        // columns); own part first: fixed order, deterministic
-                        const int* flag_o = p.part_flag + (blockIdx.x + 1) * kNumSoftmaxWarps + warp;
-                        const int* flag_ml = p.part_flag + (blockIdx.x + 1) * kNumSoftmaxWarps + (warp & ~4);
+                    if (item.kind == kItemMerge) {
+                        // merge with the partial CTA blockIdx.x - 1 published for the same rows at the START of
+                        // its slice (its half-0 warp of the same quadrant wrote m and l, this warp's twin wrote
+                        // the columns); own part first: fixed order, deterministic.  The wait is on a
+                        // lower-indexed CTA only, so it cannot starve whatever else is resident on the GPU.
+                        const int* flag_o = p.part_flag + (blockIdx.x - 1) * kNumSoftmaxWarps + warp;
+                        const int* flag_ml = p.part_flag + (blockIdx.x - 1) * kNumSoftmaxWarps + (warp & ~4);
                         uint32_t spins = 0;
                         while (ld_acquire_gpu(flag_o) == 0 || ld_acquire_gpu(flag_ml) == 0) {
-                            if (++spins > RF_MBAR_SPIN_LIMIT) __trap();
+                            if (!wait_slow_path(spins, wctx, kStatusPeerTimeout)) break;
                         }
-                        const size_t slot = (static_cast<size_t>(blockIdx.x + 1) * 2 + x) * kBlockM + r;
+                        const size_t slot = (static_cast<size_t>(blockIdx.x - 1) * 2 + x) * kBlockM + r;
                         const float m2 = __ldcg(p.part_ml + slot * 2);
                         const float l2 = __ldcg(p.part_ml + slot * 2 + 1);
                         const float ms = fmaxf(m_ref, m2);
@@ -867,10 +883,10 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         l_tot = l_tot * w1 + l2 * w2;
                         m_ref = ms;
                     }
-                    if (row < p.S) {
+                    if (row < p.S && col0 < p.d) {  // head_dim 32 runs zero-padded to 64: its columns [32, 64) do not exist
                         if (p.o_partial != nullptr) {
                             const size_t ridx = (static_cast<size_t>(b) * p.H + h) * p.S + row;
-                            float4* dst = reinterpret_cast<float4*>(p.o_partial + ridx * kHeadDim + col0);
+                            float4* dst = reinterpret_cast<float4*>(p.o_partial + ridx * p.d + col0);
 #pragma unroll
                             for (int u = 0; u < kOutCols / 4; ++u)
                                 dst[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);

@@ -100,7 +100,9 @@ enum : uint32_t {
     kBarOFull,
     kNumBars,
 };
-static_assert(kNumBars * 8 + 8 <= Smem::bar_bytes, "barrier block too small");
+constexpr uint32_t kTmemSlotOff = kNumBars * 8;                     // u32: TMEM base address
+constexpr uint32_t kWaitBlockOff = (kTmemSlotOff + 8 + 15) & ~15u;  // 16 bytes: abort word + status pointer (ptx.cuh)
+static_assert(kWaitBlockOff + 16 <= Smem::bar_bytes, "barrier block too small");
 
 struct Tile {
     int b, h, r0, kb;  // batch, head, first query row, first key of the strip
@@ -144,7 +146,8 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
     uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
     const uint32_t bars = smem_base + Smem::bars;
     auto bar = [&](uint32_t i) { return bars + 8u * i; };
-    volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_gen + Smem::bars + 8 * kNumBars);
+    volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_gen + Smem::bars + kTmemSlotOff);
+    const WaitCtx wctx{bars + kWaitBlockOff};
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -172,6 +175,7 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         mbar_init(bar(kBarSFree), kSoftmaxWarps);
         mbar_init(bar(kBarPFull), kSoftmaxThreads);
         mbar_init(bar(kBarOFull), 1);
+        wait_block_init(wctx.block_smem, p.status);
         fence_barrier_init();
     }
     if (warp == kMmaWarp) {
@@ -192,12 +196,12 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         uint32_t bc = 0;  // K/V boxes requested so far: ring slot bc % kRing, use (bc / kRing)
         auto load_box = [&](const Tile& t, int key0) {
             const uint32_t slot = bc % kRing, par = ((bc / kRing) & 1) ^ 1;
-            mbar_wait(bar(kBarKEmpty + slot), par);
+            mbar_wait(bar(kBarKEmpty + slot), par, wctx);
             if (lane == 0) {
                 mbar_arrive_expect_tx(bar(kBarKFull + slot), kTileBytes);
                 tma_load_4d(smem_base + Smem::k + slot * kTileBytes, &tm_k, bar(kBarKFull + slot), 0, key0, t.h, t.b);
             }
-            mbar_wait(bar(kBarVEmpty + slot), par);
+            mbar_wait(bar(kBarVEmpty + slot), par, wctx);
             if (lane == 0) {
                 mbar_arrive_expect_tx(bar(kBarVFull + slot), kTileBytes);
                 tma_load_4d(smem_base + Smem::v + slot * kTileBytes, &tm_v, bar(kBarVFull + slot), 0, key0, t.h, t.b);
@@ -208,7 +212,7 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         for (int n = 0; n < my_tiles; ++n) {
             const Tile t = decode_tile(p, g0 + n, q_tiles);
             const uint32_t s = n & 1;
-            mbar_wait(bar(kBarQEmpty + s), ((n >> 1) & 1) ^ 1);
+            mbar_wait(bar(kBarQEmpty + s), ((n >> 1) & 1) ^ 1, wctx);
             if (lane == 0) {
                 mbar_arrive_expect_tx(bar(kBarQFull + s), kTileBytes);
                 tma_load_4d(smem_base + Smem::q + s * kTileBytes, &tm_q, bar(kBarQFull + s), 0, t.r0, t.h, t.b);
@@ -240,8 +244,8 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
             first_qk = fresh ? nb : nb - 1;
             nb = first_qk + 2;
             const uint32_t s0 = first_qk % kRing, s1 = (first_qk + 1) % kRing;
-            mbar_wait(bar(kBarQFull + (n & 1)), (n >> 1) & 1);
-            mbar_wait2(bar(kBarKFull + s0), (first_qk / kRing) & 1, bar(kBarKFull + s1), ((first_qk + 1) / kRing) & 1);
+            mbar_wait(bar(kBarQFull + (n & 1)), (n >> 1) & 1, wctx);
+            mbar_wait2(bar(kBarKFull + s0), (first_qk / kRing) & 1, bar(kBarKFull + s1), ((first_qk + 1) / kRing) & 1, wctx);
             tc_fence_after();
             if (leader) {
                 const uint32_t qbase = smem_base + Smem::q + (n & 1) * kTileBytes;
@@ -266,7 +270,7 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
             RF_STAMP(n, 0);
             if (n + 1 < my_tiles) {
                 // S(n) is in registers: Q K^T of the next tile runs under the softmax of this one
-                mbar_wait(bar(kBarSFree), n & 1);
+                mbar_wait(bar(kBarSFree), n & 1, wctx);
                 RF_STAMP(n, 1);
                 issue_qk(n + 1);
             }
@@ -277,9 +281,9 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
                 nb_pv = first_pv + 2;
             }
             const uint32_t s0 = first_pv % kRing, s1 = (first_pv + 1) % kRing;
-            mbar_wait2(bar(kBarVFull + s0), (first_pv / kRing) & 1, bar(kBarVFull + s1), ((first_pv + 1) / kRing) & 1);
+            mbar_wait2(bar(kBarVFull + s0), (first_pv / kRing) & 1, bar(kBarVFull + s1), ((first_pv + 1) / kRing) & 1, wctx);
             RF_STAMP(n, 3);
-            mbar_wait(bar(kBarPFull), n & 1);
+            mbar_wait(bar(kBarPFull), n & 1, wctx);
             tc_fence_after();
             RF_STAMP(n, 4);
             if (leader) {
@@ -357,7 +361,7 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
                 if (__all_sync(0xffffffffu, lo <= c0 && hi >= c0 + 31)) full |= 1u << cb;
             }
             RF_STAMP(n, 2);
-            mbar_wait(bar(kBarSFull), par);
+            mbar_wait(bar(kBarSFull), par, wctx);
             tc_fence_after();
             RF_STAMP(n, 3);
 #pragma unroll
@@ -419,7 +423,7 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
             tmem_ld16(t_o + par * kHeadDim, reinterpret_cast<uint32_t(&)[16]>(o));
             tc_wait_ld();
             const int row = t.r0 + r;
-            if (row < p.S) {
+            if (row < p.S && part * kOutCols < p.d) {  // head_dim 32 runs zero-padded to 64 (FaParams::d)
                 const size_t off = static_cast<size_t>(t.b) * p.o_sb + static_cast<size_t>(t.h) * p.o_sh +
                                    static_cast<size_t>(row) * p.o_ss + part * kOutCols;
                 if (p.out_dtype == 2) {
@@ -494,7 +498,7 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
                     for (int u = 0; u < 16; ++u) pk[u] = 0u;
                 }
                 if (cb == 0) {
-                    if (!p_free) mbar_wait(bar(kBarOFull), par ^ 1u);
+                    if (!p_free) mbar_wait(bar(kBarOFull), par ^ 1u, wctx);
                     tc_fence_after();
                 }
                 tmem_st16(t_p + cb * 16, pk);
@@ -513,7 +517,7 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         if (my_tiles > 0) {
             const int n = my_tiles - 1;
             named_bar_sync(row_bar, 32 * kParts);  // lsum of the last tile
-            mbar_wait(bar(kBarOFull), n & 1);
+            mbar_wait(bar(kBarOFull), n & 1, wctx);
             tc_fence_after();
             epilogue(n, cur);
         }

@@ -13,6 +13,7 @@ namespace rf {
 int set_last_error(int code, const std::string& message);
 
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr uint32_t kLaunchStatusMagic = 0x52460000u;  // == rfptx::kStatusMagic (ptx.cuh)
 constexpr float kMaskThreshold = -30000.0f;  // reference attention.hpp:16
 
 // Geometry of the tcgen05 kernel.
@@ -26,6 +27,9 @@ enum : uint8_t { kTileSkip = 0, kTileFull = 1, kTileMixed = 2 };
 
 struct FaParams {
     int B, H, S;
+    int d;                 // head_dim of the tensors: 64, or 32 (the tcgen05 kernels then run it zero-padded to 64:
+                           // TMA boxes are 64 wide and the 32 columns outside the tensor arrive as zeros)
+    int* status;           // launch status word (ptx.cuh: written only when a bounded wait times out), may be null
     int kv_begin, kv_end;  // key range [kv_begin, kv_end), 0 <= kv_begin <= kv_end <= S
     int wl, wr;            // window, -1 = unbounded
     float scale_log2;      // effective scale * log2(e)
@@ -83,6 +87,11 @@ size_t fa_fwd_sm100_local_smem_bytes();
 cudaError_t launch_fa_fwd_sm100_local(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
                                       const FaParams& p, const float* pad_bias, bool bf16, int grid,
                                       cudaStream_t stream);
+// head_dim 128 kernel (fa_fwd_sm100_d128.cu): whole query-tile pairs, sched_mode 0 or 2
+cudaError_t launch_fa_fwd_sm100_d128(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
+                                     const FaParams& p, bool bf16, int grid, cudaStream_t stream);
+size_t fa_fwd_sm100_d128_smem_bytes();
+bool fa_fwd_sm100_d128_available();
 size_t fa_fwd_sm100_smem_bytes();
 size_t fa_fwd_sm100_partial_bytes(int grid);
 void fa_fwd_sm100_partial_carve(void* base, int grid, FaParams* p, void** flags, size_t* flag_bytes);
@@ -94,7 +103,7 @@ cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias
 // (also zeroes zero_words ints at zero_ptr -- the persistent schedule's flag block -- and triggers
 // programmatic launch of the next kernel in the stream)
 cudaError_t launch_qk_norms(const void* q, const void* k, const long long q_strides[3], const long long k_strides[3],
-                            int dtype, int B, int H, int S, int n_kv_tiles, float* qnorm, float* kmax, int* zero_ptr,
+                            int dtype, int B, int H, int S, int d, int n_kv_tiles, float* qnorm, float* kmax, int* zero_ptr,
                             int zero_words, cudaStream_t stream);
 cudaError_t launch_merge(const float* const* o_parts, const float* const* m_parts, const float* const* l_parts,
                          int G, long long rows, int d, void* out, int out_dtype, cudaStream_t stream);

@@ -44,27 +44,79 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity)
     return ok;
 }
 
-// Bounded wait: a protocol bug must surface as a CUDA error, never as a hung GPU.
-// try_wait suspends in hardware for a while per call, so the poll budget is generous.
+// Bounded waits.  A wait that exhausts its poll budget (a protocol bug, or a dependency that is never
+// scheduled) must neither hang the GPU nor kill the context: it records a code in a status word in global
+// memory (the host reads it: rf_fa_launch_status) and raises the CTA's abort word in shared memory.  Every
+// wait of the CTA polls that word from its slow path and returns as soon as it is set, so the kernel runs
+// through to its normal teardown (results are garbage, the status word says so).  The fast path -- the
+// barrier is ready on the first polls -- is unchanged.
 #ifndef RF_MBAR_SPIN_LIMIT
 #define RF_MBAR_SPIN_LIMIT (1u << 24)
 #endif
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+// The CTA's 16-byte wait block in shared memory: [0,4) abort word (0 = running), [8,16) the launch's global
+// status word pointer (may be null).  Keeping the pointer there instead of in a WaitCtx member costs the
+// 32-register producer / MMA warps nothing.
+struct WaitCtx {
+    uint32_t block_smem;  // shared-memory address of the wait block
+};
+// Status word values: kStatusMagic | code << 12 | (CTA index & 0xfff).  The workspace is caller-owned and never
+// cleared on the launch path (a memset node would cost the 20 us local-window layer 5-10 %), so the word is only
+// meaningful when it carries the magic tag; the host clears it after reporting.
+enum : int { kStatusBarrierTimeout = 1, kStatusPeerTimeout = 2 };
+constexpr uint32_t kStatusMagic = 0x52460000u;
+
+__device__ __forceinline__ void wait_block_init(uint32_t block_smem, int* status) {
+    asm volatile("st.shared::cta.u32 [%0], %1;" ::"r"(block_smem), "r"(0u) : "memory");
+    asm volatile("st.shared::cta.u64 [%0], %1;" ::"r"(block_smem + 8u), "l"(reinterpret_cast<uint64_t>(status)) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+static __device__ __noinline__ void wait_timed_out(uint32_t block_smem, int code) {
+    asm volatile("st.volatile.shared::cta.u32 [%0], %1;" ::"r"(block_smem), "r"(1u) : "memory");
+    uint64_t ptr;
+    asm volatile("ld.shared::cta.u64 %0, [%1];" : "=l"(ptr) : "r"(block_smem + 8u) : "memory");
+    int* status = reinterpret_cast<int*>(ptr);
+    if (status != nullptr)
+        *reinterpret_cast<volatile uint32_t*>(status) = kStatusMagic | (static_cast<uint32_t>(code) << 12) | (blockIdx.x & 0xfffu);
+}
+// true = keep polling
+__device__ __forceinline__ bool wait_slow_path(uint32_t& spins, const WaitCtx& w, int code) {
+    if ((++spins & 0xffu) != 0) return true;
+    if (ld_shared_u32(w.block_smem) != 0) return false;
+    if (spins > RF_MBAR_SPIN_LIMIT) {
+        wait_timed_out(w.block_smem, code);
+        return false;
+    }
+    return true;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, const WaitCtx& w) {
     uint32_t spins = 0;
     while (!mbar_try_wait(bar, parity)) {
-        if (++spins > RF_MBAR_SPIN_LIMIT) __trap();  // surfaces as cudaErrorLaunchFailure on the host
+        if (!wait_slow_path(spins, w, kStatusBarrierTimeout)) break;
+    }
+}
+
+// Test probes only (tests/gpu_probe, tools/probes): a single-CTA micro-kernel with no status word traps instead.
+__device__ __forceinline__ void mbar_wait_or_trap(uint32_t bar, uint32_t parity) {
+    uint32_t spins = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if (++spins > RF_MBAR_SPIN_LIMIT) __trap();
     }
 }
 
 // Two barriers at once: both try_waits are in flight together, so the (long) latency of a
 // phase check is paid once, not twice.
-__device__ __forceinline__ void mbar_wait2(uint32_t bar_a, uint32_t parity_a, uint32_t bar_b, uint32_t parity_b) {
+__device__ __forceinline__ void mbar_wait2(uint32_t bar_a, uint32_t parity_a, uint32_t bar_b, uint32_t parity_b,
+                                           const WaitCtx& w) {
     uint32_t spins = 0;
     for (;;) {
         const uint32_t oa = mbar_try_wait(bar_a, parity_a);
         const uint32_t ob = mbar_try_wait(bar_b, parity_b);
         if (oa & ob) break;
-        if (++spins > RF_MBAR_SPIN_LIMIT) __trap();
+        if (!wait_slow_path(spins, w, kStatusBarrierTimeout)) break;
     }
 }
 

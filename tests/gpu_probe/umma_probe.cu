@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(128, 1) umma_probe_kernel(int mode, const uint
         }
         tc_commit(bar);
     }
-    mbar_wait(bar, 0);
+    mbar_wait_or_trap(bar, 0);
     tc_fence_after();
     for (int cb = 0; cb < N / 32; ++cb) {
         uint32_t r[32];

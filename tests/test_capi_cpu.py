@@ -61,13 +61,25 @@ def test_validation_mirrors_reference_errors(lib):
     p.kv_begin, p.kv_end = 8, 4
     assert lib.rf_fa_validate(C.byref(p)) == capi.RF_ERR_ARG
     p.kv_begin, p.kv_end = 0, 0
-    # forcing the tensor-core kernel onto a head dim it does not cover is an explicit error
-    p.d, p.kernel = 32, capi.RF_KERNEL_TCGEN05
+    # every head dim of the reference contract runs on the tensor cores (rewrite.cpp:266-269)
+    st = capi.RfFaStats()
+    for d in (32, 64, 128):
+        p.d, p.kernel = d, capi.RF_KERNEL_TCGEN05
+        assert lib.rf_fa_validate(C.byref(p)) == capi.RF_OK
+        p.kernel = capi.RF_KERNEL_AUTO
+        assert lib.rf_fa_stats_query(C.byref(p), C.byref(st)) == capi.RF_OK
+        assert st.kernel == capi.RF_KERNEL_TCGEN05 and st.score_matrix_bytes == 0
+    # forcing the tensor-core kernel onto a call it does not cover is an explicit error; AUTO falls back to the
+    # generic CUDA-core kernel (still on the device)
+    p.d, p.scale, p.kernel = 64, -0.5, capi.RF_KERNEL_TCGEN05
     assert lib.rf_fa_validate(C.byref(p)) == capi.RF_ERR_UNSUPPORTED
     p.kernel = capi.RF_KERNEL_AUTO
-    st = capi.RfFaStats()
     assert lib.rf_fa_stats_query(C.byref(p), C.byref(st)) == capi.RF_OK
     assert st.kernel == capi.RF_KERNEL_SIMT and st.score_matrix_bytes == 0
+    p.scale = 0.0
+    p.flags = 1
+    assert lib.rf_fa_validate(C.byref(p)) == capi.RF_ERR_ARG   # reserved, must be 0
+    p.flags = 0
 
 
 def test_workspace_is_linear_in_S(lib):
@@ -100,8 +112,8 @@ def test_workspace_is_linear_in_S(lib):
         dense.append(n.value)
     assert 0 < dense[0] < dense[1] < 13 * 1024 * 1024
     assert dense[1] - dense[0] <= (32768 - 8192) * (4 * 12 + 4 * 12 / 128.0) + 1024
-    p.S = 512  # 24 pairs fit one wave: one pair per CTA, no workspace at all
-    assert lib.rf_fa_fwd_workspace_bytes(C.byref(p), C.byref(n)) == capi.RF_OK and n.value == 0
+    p.S = 512  # 24 pairs fit one wave: one pair per CTA, nothing but the 256-byte launch-status block
+    assert lib.rf_fa_fwd_workspace_bytes(C.byref(p), C.byref(n)) == capi.RF_OK and n.value == 256
 
 
 def test_host_entry_checks_in_reference_order(lib):

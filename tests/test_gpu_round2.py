@@ -111,3 +111,135 @@ def test_huge_windows_mean_unbounded_and_flags_are_rejected(torch_mod, P, oracle
         assert np.abs(got - want).max() <= TOL, w
     with pytest.raises(capi.RfError):
         P.flash_attention(tq, tk, tv, P.AttentionSpec(), flags=1)
+
+
+# ------------------------------------------------------------------ head_dim 32 / 128 on the tensor cores
+@pytest.mark.parametrize("d", [32, 128])
+def test_head_dims_32_128_run_on_tcgen05(torch_mod, P, oracle, d):
+    """rewrite.cpp:266-269: head dims {32, 64, 128}.  Every one of them takes a tcgen05 kernel (32 zero-padded
+    to 64 inside the TMA box, 128 on its own kernel): parity grid over windows, padding and ragged lengths."""
+    torch = torch_mod
+    rng = np.random.default_rng(100 + d)
+    worst = 0.0
+    for (B, H, S) in ((1, 2, 37), (2, 3, 300), (1, 2, 1000), (1, 1, 1500)):
+        q, k, v = [oracle.round_bf16(rng.uniform(-1, 1, (B, H, S, d)).astype(np.float32)) for _ in range(3)]
+        lens = [max(1, S - 1 - 31 * b) for b in range(B)]
+        for (wl, wr) in ((-1, -1), (63, 64), (1, 2), (-1, 0), (200, 100)):
+            for pb in (None, tail_pad(B, S, lens)):
+                tq, tk, tv = [torch.from_numpy(t).cuda().to(torch.bfloat16) for t in (q, k, v)]
+                st = P.FlashStats()
+                out = P.flash_attention(tq, tk, tv, P.AttentionSpec(0.0, wl, wr, torch.from_numpy(pb).cuda() if pb is not None else None),
+                                        stats=st, kernel="tcgen05")
+                torch.cuda.synchronize()
+                assert st.kernel == "tcgen05"
+                want = oracle.flash_attention(q, k, v, 0.0, wl, wr, pb, threads=8)
+                got = out.float().cpu().numpy()
+                assert not np.isnan(got).any()
+                err = float(np.abs(got - want).max())
+                worst = max(worst, err)
+                assert err <= TOL, (d, B, H, S, wl, wr, pb is not None, err)
+    print("d", d, "worst", worst)
+
+
+@pytest.mark.parametrize("d", [32, 128])
+def test_head_dims_32_128_long_sequence_and_split_kv(torch_mod, P, oracle, d):
+    """S = 4096 (persistent schedules), f16 inputs, strided [B,S,H,d] views and a split-KV merge, one head
+    checked against the oracle and every head against the CUDA-core kernel."""
+    torch = torch_mod
+    from paper_2603_12646_b200.splitkv import kv_block, merge_partials_local
+    B, H, S = 2, 12, 4096
+    g = torch.Generator(device="cuda").manual_seed(d)
+    qkv = (torch.rand((B, S, 3, H, d), device="cuda", generator=g) * 2 - 1).to(torch.float16)
+    q, k, v = (qkv[:, :, j].permute(0, 2, 1, 3) for j in range(3))
+    lens = [4096, 3001]
+    pb = torch.from_numpy(tail_pad(B, S, lens)).cuda()
+    for (wl, wr) in ((-1, -1), (63, 64)):
+        spec = P.AttentionSpec(0.0, wl, wr, pb)
+        st = P.FlashStats()
+        out = P.flash_attention(q, k, v, spec, stats=st, out_dtype=torch.float32)
+        ref = P.flash_attention(q, k, v, spec, kernel="simt", out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert st.kernel == "tcgen05"
+        assert (out - ref).abs().max().item() <= 5e-3
+        b, h = 1, 5
+        want = oracle.flash_attention(q[b:b + 1, h:h + 1].float().cpu().numpy(), k[b:b + 1, h:h + 1].float().cpu().numpy(),
+                                      v[b:b + 1, h:h + 1].float().cpu().numpy(), 0.0, wl, wr, pb[b:b + 1].cpu().numpy())
+        assert np.abs(out[b:b + 1, h:h + 1].cpu().numpy() - want).max() <= TOL
+    spec = P.AttentionSpec(0.0, -1, -1, pb)
+    full = P.flash_attention(q, k, v, spec, out_dtype=torch.float32)
+    parts = []
+    for r in range(3):
+        o = torch.empty((B, H, S, d), device="cuda")
+        m = torch.empty((B, H, S), device="cuda")
+        l = torch.empty((B, H, S), device="cuda")
+        P.flash_attention(q, k, v, spec, kv_range=kv_block(S, r, 3), partials=(o, m, l))
+        parts.append((o, m, l))
+    merged = merge_partials_local(parts)
+    assert (merged - full).abs().max().item() <= 2e-3
+
+
+# ------------------------------------------------------------------ plan object
+def test_plan_launch_equals_direct_call_and_reports_status(torch_mod, P, oracle):
+    """rf_fa_plan_create / rf_fa_plan_launch: same result bit for bit as rf_fa_fwd, relaunchable after the
+    tensors' contents change; rf_fa_launch_status reports RF_OK."""
+    torch = torch_mod
+    from paper_2603_12646_b200 import capi
+    from paper_2603_12646_b200.attention import FaPlan
+    lib = capi.load()
+    B, H, S, d = 1, 12, 2048, 64
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q, k, v = [(torch.rand((B, H, S, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+    for (wl, wr, padded) in ((-1, -1, False), (-1, -1, True), (63, 64, True)):
+        pb = torch.from_numpy(tail_pad(B, S, [1777])).cuda() if padded else None
+        spec = P.AttentionSpec(0.0, wl, wr, pb)
+        direct = P.flash_attention(q, k, v, spec).clone()
+        out = torch.zeros_like(direct)
+        plan = FaPlan(q, k, v, spec, out=out)
+        plan.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(out, direct)
+        q2 = q.clone()
+        q.copy_(-q)                      # same addresses, new contents
+        plan.launch()
+        direct2 = P.flash_attention(q, k, v, spec)
+        torch.cuda.synchronize()
+        assert torch.equal(out, direct2) and not torch.equal(out, direct)
+        q.copy_(q2)
+        assert plan.status() == capi.RF_OK
+        plan.close()
+
+
+# ------------------------------------------------------------------ persistent schedule under contention
+def test_two_persistent_calls_on_two_streams_do_not_starve(torch_mod, P, oracle):
+    """Two balanced-schedule (mode 1) launches run concurrently on two streams, each with its own workspace,
+    while a third stream keeps the SMs busy with other work.  A CTA of the split-pair chain only ever waits for
+    a lower-indexed CTA, so both finish, bit-identical to their isolated runs, with a clean status word."""
+    torch = torch_mod
+    from paper_2603_12646_b200 import capi
+    from paper_2603_12646_b200.attention import FaPlan
+    B, H, S, d = 1, 12, 4096, 64     # 192 pairs > 148 SMs: persistent balanced schedule with split pairs
+    g = torch.Generator(device="cuda").manual_seed(11)
+    mk = lambda: [(torch.rand((B, H, S, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+    (q1, k1, v1), (q2, k2, v2) = mk(), mk()
+    spec = P.AttentionSpec()
+    st = P.FlashStats()
+    ref1 = P.flash_attention(q1, k1, v1, spec, stats=st).clone()
+    ref2 = P.flash_attention(q2, k2, v2, spec).clone()
+    assert st.grid_ctas == torch.cuda.get_device_properties(0).multi_processor_count
+    o1, o2 = torch.empty_like(ref1), torch.empty_like(ref2)
+    p1, p2 = FaPlan(q1, k1, v1, spec, out=o1), FaPlan(q2, k2, v2, spec, out=o2)
+    s1, s2, s3 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    for _ in range(20):
+        with torch.cuda.stream(s3):
+            a @ a
+        with torch.cuda.stream(s1):
+            p1.launch()
+        with torch.cuda.stream(s2):
+            p2.launch()
+    torch.cuda.synchronize()
+    assert p1.status() == capi.RF_OK and p2.status() == capi.RF_OK
+    assert torch.equal(o1, ref1) and torch.equal(o2, ref2)
+    p1.close()
+    p2.close()

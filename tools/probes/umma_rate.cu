@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int mode, int rounds, long
         }
         long long t1 = clock64();
         tc_commit(bar);
-        mbar_wait(bar, 0);
+        mbar_wait_or_trap(bar, 0);
         long long t2 = clock64();
         if (blockIdx.x == 0) {
             out[0] = t1 - t0;
