@@ -243,3 +243,83 @@ def test_two_persistent_calls_on_two_streams_do_not_starve(torch_mod, P, oracle)
     assert torch.equal(o1, ref1) and torch.equal(o2, ref2)
     p1.close()
     p2.close()
+
+
+# ------------------------------------------------------------------ bench.py workloads / N-GPU launcher
+def _run_bench(argv, timeout=900):
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + argv, cwd=root, env=env, capture_output=True,
+                         text=True, timeout=timeout)
+    lines = [json.loads(ln) for ln in res.stdout.splitlines() if ln.startswith("{")]
+    return res, lines
+
+
+def test_bench_workloads_on_one_gpu(torch_mod):
+    """config3 / config4 / config5 run through BatchScheduler / split_kv_attention's N=1 path and print one
+    contract line each."""
+    for wl, metric in (("config4", "attention_fwd_tflops"), ("config3", "classifier_requests_per_s"),
+                       ("config5", "classifier_requests_per_s")):
+        res, lines = _run_bench(["--workload", wl, "--steps", "1", "--warmup", "3"])
+        assert res.returncode == 0, res.stderr[-2000:]
+        assert len(lines) == 1
+        ln = lines[0]
+        assert ln["metric"] == metric and ln["n_gpus"] == 1 and ln["value"] > 0 and wl in ln["config"]["workload"]
+        if wl == "config3":
+            assert ln["config"]["units"] == 12 and ln["config"]["units_per_rank"] == [12]
+
+
+def test_bench_gpus_n_spawns_ranks_or_fails_loudly(torch_mod):
+    """`bench.py --gpus 2` outside torchrun starts 2 NCCL ranks itself; with fewer GPUs visible it exits 2 with an
+    error line instead of silently running one rank."""
+    torch = torch_mod
+    if torch.cuda.device_count() >= 2:
+        for wl in ("op8k", "config4", "config3"):
+            res, lines = _run_bench(["--gpus", "2", "--workload", wl, "--steps", "2", "--warmup", "3", "--quick", "--no-cpu"])
+            assert res.returncode == 0, res.stderr[-2000:]
+            assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
+    else:
+        res, lines = _run_bench(["--gpus", "2", "--steps", "2", "--warmup", "3", "--quick", "--no-cpu"])
+        assert res.returncode == 2 and lines and "error" in lines[0]
+
+
+def test_split_kv_over_nccl_matches_single_pass(torch_mod):
+    """2-rank NCCL split-KV (config 4's exchange) against the single-GPU op; skipped below 2 GPUs."""
+    torch = torch_mod
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r'''
+import os, sys, torch, torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+import paper_2603_12646_b200 as P
+from paper_2603_12646_b200.splitkv import split_kv_attention
+rank = int(os.environ["LOCAL_RANK"]); torch.cuda.set_device(rank)
+dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+g = torch.Generator(device="cuda").manual_seed(4)
+q, k, v = [(torch.rand((1, 12, 4096, 64), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+pb = torch.zeros((1, 1, 1, 4096), device="cuda"); pb[..., 3000:] = -65504.0
+for spec in (P.AttentionSpec(), P.AttentionSpec(0.0, -1, -1, pb), P.AttentionSpec(0.0, 300, 200, pb)):
+    full = split_kv_attention(q, k, v, spec, out_dtype=torch.float32)
+    ref = P.flash_attention(q, k, v, spec, out_dtype=torch.float32)
+    assert (full - ref).abs().max().item() <= 2e-3, (full - ref).abs().max().item()
+dist.barrier(); dist.destroy_process_group()
+print("nccl split-kv ok")
+'''
+    import tempfile
+    with tempfile.NamedTemporaryFile("w", suffix=".py", delete=False) as f:
+        f.write(script)
+        path = f.name
+    try:
+        res = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+                              "127.0.0.1", "--master-port", "29631", path], cwd=root, capture_output=True, text=True, timeout=600)
+    finally:
+        os.unlink(path)
+    assert res.returncode == 0 and "nccl split-kv ok" in res.stdout, res.stderr[-3000:]
