@@ -219,7 +219,7 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         rf::fa_fwd_sm100_local_covers(static_cast<int>(r.wl), static_cast<int>(r.wr))) {
         pl.local = true;
         const int64_t tiles = static_cast<int64_t>(p->B) * p->H * ((p->S + rf::kBlockM - 1) / rf::kBlockM);
-        pl.grid = static_cast<int>(std::min<int64_t>(tiles, sm_count_or_default()));
+        pl.grid = rf::fa_fwd_sm100_local_grid(tiles, sm_count_or_default());  // two CTAs per SM
         return pl;
     }
     pl.grid = static_cast<int>(pl.total_pairs);

@@ -82,7 +82,7 @@ cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, 
 // narrow-window kernel (fa_fwd_sm100_local.cu): wl + wr <= 127, one 256-key strip per query tile;
 // reads the raw pad_bias [B,S] (nullable), needs no workspace
 bool fa_fwd_sm100_local_covers(int wl, int wr);
-int fa_fwd_sm100_local_grid(const FaParams& p, int sms);
+int fa_fwd_sm100_local_grid(long long query_tiles, int sms);  // CTAs: two per SM, at most one per query tile
 size_t fa_fwd_sm100_local_smem_bytes();
 cudaError_t launch_fa_fwd_sm100_local(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
                                       const FaParams& p, const float* pad_bias, bool bf16, int grid,
