@@ -271,7 +271,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_gen + Smem::bars + kTmemSlotOff);
     const WaitCtx wctx{bars + kWaitBlockOff};
 
-    const int warp = threadIdx.x >> 5;
+    const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform by construction: lets roles, buffer indices and TMEM addresses live in uniform registers
     const int lane = threadIdx.x & 31;
 
     // ---------------- prologue ----------------

@@ -79,8 +79,11 @@ constexpr uint32_t kColS = 0, kColP = 0, kColO = 128;
 #ifndef RF_LOCAL_SKEW
 #define RF_LOCAL_SKEW 0
 #endif
+#ifndef RF_LOCAL_SKEW_ODD
+#define RF_LOCAL_SKEW_ODD 0
+#endif
 #ifndef RF_LOCAL_POLY
-#define RF_LOCAL_POLY 0
+#define RF_LOCAL_POLY 2
 #endif
 
 // Developer build only (-DRF_FA_TRACE=1): CTA 0 stamps the SM clock at phase boundaries into the
@@ -223,6 +226,12 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Programmatic dependent launch: everything above overlapped the tail of the previous kernel in the stream; its
+    // results (Q, K, V come out of the layer's RoPE kernel) are visible, and whatever it still read of the output
+    // buffer is done, after the wait.  The next kernel in the stream may then start its own prologue as this
+    // grid's CTAs retire.  Both are no-ops under a plain launch.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
 
     if (warp >= kSoftmaxWarps) setmaxnreg_dec<kRegsOther>();
 
@@ -273,7 +282,7 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
 #if RF_LOCAL_SKEW > 0
         // Two co-resident CTAs that start together stay in lockstep (both in their exponentials, then both waiting
         // for the tensor pipe).  The second CTA of an SM starts its chain half a tile period late instead.
-        if (blockIdx.x >= gridDim.x / 2 && gridDim.x > 148) {
+        if ((RF_LOCAL_SKEW_ODD ? (blockIdx.x & 1) != 0 : blockIdx.x >= gridDim.x / 2) && gridDim.x > 148) {
             const long long t0 = clock64();
             while (clock64() - t0 < RF_LOCAL_SKEW) { }
         }
@@ -334,7 +343,11 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         const int part = warp >> 2;            // which half of the quad's live pieces
         const int quad = warp & 3;
         const int r = quad * 32 + lane;        // row inside the tile == TMEM lane
-        const int tid = threadIdx.x;           // 0..255
+        int tid = threadIdx.x;                 // 0..255
+        int seq_len = p.S;
+        // pinned in registers: re-reading SR_TID.X / the parameter bank at the top of every tile put ~10 % of the
+        // softmax warps' stall samples there (ncu)
+        asm volatile("" : "+r"(tid), "+r"(seq_len));
         const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
         const uint32_t t_s = tmem_base + lane_base + kColS;
         const uint32_t t_p = tmem_base + lane_base + kColP;
@@ -377,17 +390,17 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         auto column_bias = [&](const Tile& t) -> float {
             const int key = t.kb + tid;
             float v = -CUDART_INF_F;
-            if (key >= 0 && key < p.S) {
+            if (key >= 0 && key < seq_len) {
                 v = 0.f;
                 if (kHasBias) {
-                    const float raw = __ldg(pad_bias + static_cast<size_t>(t.b) * p.S + key);
+                    const float raw = __ldg(pad_bias + static_cast<size_t>(t.b) * seq_len + key);
                     v = raw > kMaskThreshold ? raw * kLog2e : -CUDART_INF_F;
                 }
             }
             return v;
         };
         // without a pad bias only the first and last tiles of a head need the column term (keys outside [0, S))
-        auto needs_column_bias = [&](const Tile& t) { return kHasBias || t.kb < 0 || t.kb + kStrip > p.S; };
+        auto needs_column_bias = [&](const Tile& t) { return kHasBias || t.kb < 0 || t.kb + kStrip > seq_len; };
 
         Tile cur = {};
         float bias_pref = 0.f;
@@ -595,7 +608,7 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(kBarTmemFree));
-            if (row < p.S && part * kOutCols < p.d) {  // head_dim 32 runs zero-padded to 64 (FaParams::d)
+            if (row < seq_len && part * kOutCols < p.d) {  // head_dim 32 runs zero-padded to 64 (FaParams::d)
                 if (p.out_dtype == 2) {
                     float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
 #pragma unroll
@@ -656,8 +669,17 @@ cudaError_t launch_fa_fwd_sm100_local(const CUtensorMap& tmq, const CUtensorMap&
     // the carve-out must leave room for two CTAs' shared memory
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kThreads, smem, stream>>>(tmq, tmk, tmv, p, pad_bias);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tmq, tmk, tmv, p, pad_bias);
 }
 
 }  // namespace rf

@@ -155,7 +155,9 @@ def test_persistent_schedule_matches_one_pair_per_cta(torch_mod, P, oracle):
         spec = P.AttentionSpec(0.0, wl, wr, pbt)
         st3 = P.FlashStats()
         c_ = P.flash_attention(q, k, v, spec, stats=st3, out_dtype=torch.float32)
-        assert st3.grid_ctas < B * H * 9
+        # persistent either way: fewer CTAs than query-tile pairs (dense kernel, one CTA per SM) or than query tiles
+        # (narrow-window kernel, two CTAs per SM)
+        assert st3.grid_ctas < B * H * (18 if (wl, wr) == (63, 64) else 9)
         d_ = P.flash_attention(q, k, v, spec, kernel="simt", out_dtype=torch.float32)
         assert not torch.isnan(c_).any() and (c_ - d_).abs().max().item() <= 5e-3, (wl, wr)
     assert torch.equal(a, P.flash_attention(q, k, v, P.AttentionSpec(), out_dtype=torch.float32))
