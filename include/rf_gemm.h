@@ -1,0 +1,46 @@
+/* rf_gemm.h -- C ABI of the hand-written sm_100a projections either side of the FusedFlashAttention operator
+ * ("QKV projection + RoPE + head-split layout glue -> kernel, and O -> out-proj").
+ *
+ * The reference has no GEMM of its own on this path: its fused node consumes the raw (unscaled) Q and the
+ * un-transposed K of whatever produced them (proj/core/src/rewrite.cpp:183,336-353), and its graph fixtures feed
+ * Q = K = V = hidden (proj/tests/support/graph_fixtures.cpp:76-103).  In the ModernBERT-style encoder this build
+ * wraps around the operator those producers are nn.Linear projections; rf_gemm_nt is that projection with the
+ * encoder's element-wise steps fused into its epilogue.  Plain pointers and sizes, asynchronous on `stream`, no
+ * allocation, no CPU fallback (RF_ERR_CUDA without a device).  Status codes and rf_last_error() as in rf_fa.h.
+ */
+#ifndef RF_GEMM_H_
+#define RF_GEMM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum rf_gemm_epilogue_kind {
+    RF_GEMM_EPI_NONE = 0,  /* y = a w^T                                                                      */
+    RF_GEMM_EPI_ROPE = 1,  /* y = packed [tokens, 3, H, 64] QKV projection, rotary embedding ("rotate_half"
+                              pairing i, i + 32) applied to the Q and K thirds (what rf_rope_qkv does in place)  */
+    RF_GEMM_EPI_GEGLU = 2  /* w = [2*I, K] (input half, then gate half); y[tokens, I] = gelu(in) * gate (erf
+                              GELU; what rf_geglu does on a materialised [tokens, 2*I] buffer)                   */
+};
+
+typedef struct rf_gemm_epilogue {
+    int32_t kind;            /* rf_gemm_epilogue_kind */
+    int32_t head_dim;        /* ROPE: must be 64 */
+    int64_t S;               /* ROPE: token t sits at position t % S */
+    const float* cos_table;  /* ROPE: [S, head_dim / 2] f32, device */
+    const float* sin_table;
+} rf_gemm_epilogue;
+
+/* y[M, N'] = epilogue(a[M, K] * w[N, K]^T): 16-bit operands and output (dtype = RF_DTYPE_BF16 | RF_DTYPE_F16), f32
+ * accumulation.  lda / ldw / ldy are the element strides between rows (0 = dense).  N' = N, or N / 2 for GEGLU.
+ * Requirements (else RF_ERR_UNSUPPORTED): N % 256 == 0, K % 8 == 0, 16-byte aligned pointers and row strides;
+ * ROPE: N = 3 * hidden with hidden % 256 == 0; GEGLU: (N / 2) % 128 == 0.  epi == NULL means RF_GEMM_EPI_NONE. */
+int rf_gemm_nt(const void* a, const void* w, void* y, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldw,
+               int64_t ldy, int32_t dtype, const rf_gemm_epilogue* epi, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RF_GEMM_H_ */

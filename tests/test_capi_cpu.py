@@ -18,7 +18,7 @@ def lib():
 
 def header_functions():
     names = set()
-    for header in ("rf_fa.h", "rf_graph.h", "rf_clf.h"):
+    for header in ("rf_fa.h", "rf_graph.h", "rf_clf.h", "rf_gemm.h"):
         text = open(os.path.join(ROOT, "include", header)).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         names |= set(re.findall(r"\b(rf_[a-z0-9_]+)\s*\(", text))
