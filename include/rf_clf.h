@@ -20,9 +20,10 @@
  *
  * The session owns its device memory: the weights and one activation arena that grows to the largest
  * (B, S) seen and is reused by every forward (slots are recycled inside a layer, so a 32K-token forward
- * stays under 800 MB including the weights).  The GEMMs are plain library GEMMs (cuBLAS, resolved with
- * dlopen at session creation; a missing library is an error, never a fallback); everything else is the
- * hand-written kernels of this library.  A (B, S, mask?) shape seen twice in a row is captured into a CUDA
+ * stays under 800 MB including the weights).  The projections are this library's own tcgen05 GEMM (rf_gemm.h)
+ * with RoPE and GeGLU fused into its epilogues; selecting RF_CLF_GEMM_CUBLAS routes them to the library GEMM instead
+ * (resolved with dlopen at session creation; a missing library is an error, never a fallback).  Everything else
+ * is the hand-written kernels of this library.  A (B, S, mask?) shape seen twice in a row is captured into a CUDA
  * graph and replayed from then on (ids / mask / logits go through page-locked staging owned by the session),
  * which removes the launch gaps between the ~200 kernels of a forward (8K tokens: 5.6 -> 5.2 ms).
  * A session is NOT thread-safe; use one per thread or per stream.
@@ -58,7 +59,13 @@ typedef struct rf_clf_config {
     float rope_theta_global; /* 160000 */
     float rope_theta_local;  /* 10000 */
     float eps;               /* 1e-5 */
+    int32_t gemm_backend;    /* RF_CLF_GEMM_OWN (default): rf_gemm_nt (rf_gemm.h) with RoPE fused into the QKV projection
+                                and GeGLU into the MLP up-projection -- no library on the path, cuBLAS is not even
+                                loaded; RF_CLF_GEMM_CUBLAS: library GEMMs + rf_rope_qkv / rf_geglu (the round-1 path,
+                                kept as the A/B baseline) */
 } rf_clf_config;
+
+enum rf_clf_gemm_backend { RF_CLF_GEMM_OWN = 0, RF_CLF_GEMM_CUBLAS = 1 };
 
 /* ModernBERT-base shape (the defaults of classifier.py's ClassifierConfig). */
 void rf_clf_config_default(rf_clf_config* cfg);

@@ -36,6 +36,7 @@ EXPORTS = [
 ]
 
 RF_GEMM_EPI_NONE, RF_GEMM_EPI_ROPE, RF_GEMM_EPI_GEGLU = 0, 1, 2
+RF_CLF_GEMM_OWN, RF_CLF_GEMM_CUBLAS = 0, 1
 
 
 class RfGemmEpilogue(C.Structure):
@@ -48,7 +49,7 @@ class RfClfConfig(C.Structure):
         ("vocab_size", C.c_int32), ("hidden", C.c_int32), ("n_layers", C.c_int32), ("heads", C.c_int32),
         ("head_dim", C.c_int32), ("mlp", C.c_int32), ("global_every", C.c_int32), ("local_window", C.c_int32),
         ("n_labels", C.c_int32), ("mlp_chunk_rows", C.c_int32), ("act_dtype", C.c_int32), ("rope_theta_global", C.c_float),
-        ("rope_theta_local", C.c_float), ("eps", C.c_float),
+        ("rope_theta_local", C.c_float), ("eps", C.c_float), ("gemm_backend", C.c_int32),
     ]
 
 

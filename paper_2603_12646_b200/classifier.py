@@ -11,12 +11,12 @@ heads, MLP 1152, vocab 50368).
 
 Data path per layer (16-bit GEMM operands -- f16 by default, bf16 selectable -- and an f32 residual stream):
   h   = LN(x)                       rf_add_layernorm (fused with the previous residual add)
-  qkv = h @ Wqkv^T                  library GEMM -> [B,S,3,H,d]
-  rope(q, k) in place               rf_rope_qkv
+  qkv = rope(h @ Wqkv^T)            rf_gemm_nt, rotary embedding in the epilogue -> [B,S,3,H,d]
   o   = FusedFlashAttention(q,k,v)  strided views of qkv in, [B,S,H*d] out: no transposes
-  x  += o @ Wo^T ; h2 = LN(x)       library GEMM + rf_add_layernorm
-  x  += (gelu(h2 Wi_a) * h2 Wi_g) Wo2    in row chunks (bounds activation memory), rf_geglu
-GEMMs are plain library GEMMs (cuBLAS via torch.matmul); all glue and the attention are the
+  x  += o @ Wo^T ; h2 = LN(x)       rf_gemm_nt + rf_add_layernorm
+  x  += (gelu(h2 Wi_a) * h2 Wi_g) Wo2    in row chunks (bounds activation memory); GeGLU in the up-projection's epilogue
+The projections are this library's own tcgen05 GEMM (rf_gemm.h); `gemm="cublas"` selects the round-1 path (library
+GEMMs through torch.matmul + rf_rope_qkv / rf_geglu) for A/B measurements.  All glue and the attention are the
 hand-written kernels of librf_fa.so.
 """
 from __future__ import annotations
@@ -29,6 +29,7 @@ import torch
 
 from . import capi
 from .attention import AttentionSpec, RewriteOptions, flash_attention, local_window_attrs, pad_bias_from_mask
+from .gemm import gemm_nt
 
 
 @dataclass
@@ -51,6 +52,9 @@ class ClassifierConfig:
     # the fp32 oracle with f16 (measured 2e-3..5e-3) and do not with bf16 (9e-3..2e-2).  The residual
     # stream is f32 either way.
     act_dtype: str = "f16"
+    # projections: "own" = rf_gemm_nt (this library's tcgen05 GEMM, RoPE fused into the QKV projection and GeGLU into
+    # the MLP up-projection); "cublas" = library GEMMs + rf_rope_qkv / rf_geglu (the round-1 path, kept for A/B runs)
+    gemm: str = "own"
 
     @property
     def torch_dtype(self):
@@ -134,6 +138,7 @@ class Classifier:
         B, S = input_ids.shape
         H, d, hid = cfg.heads, cfg.head_dim, cfg.hidden
         rows = B * S
+        own = cfg.gemm == "own"
         with torch.cuda.device(self.device):
             pad_bias = None
             if attention_mask is not None:
@@ -150,11 +155,14 @@ class Classifier:
                     e0.record()
                 if i > 0:
                     h = self._add_layernorm(x, delta, self.w[f"l{i}.attn_norm"])  # x += mlp(i-1); h = LN(x)
-                qkv = h @ self.w[f"l{i}.wqkv"].t()                                # [rows, 3*hid] == [B,S,3,H,d]
-                del h, delta                                                      # keep the live set small (32K)
                 glob = cfg.is_global(i)
                 cos, sin = self._rope_tables(S, glob)
-                capi.check(lib.rf_rope_qkv(qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), rows, S, H, d, cfg.rf_dtype, self._stream()))
+                if own:                                                           # [rows, 3*hid] == [B,S,3,H,d], RoPE fused
+                    qkv = gemm_nt(h, self.w[f"l{i}.wqkv"], epilogue="rope", rope_cos=cos, rope_sin=sin, seq_len=S)
+                else:
+                    qkv = h @ self.w[f"l{i}.wqkv"].t()
+                    capi.check(lib.rf_rope_qkv(qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), rows, S, H, d, cfg.rf_dtype, self._stream()))
+                del h, delta                                                      # keep the live set small (32K)
                 q5 = qkv.view(B, S, 3, H, d)
                 qv, kv, vv = (q5[:, :, j].permute(0, 2, 1, 3) for j in range(3))  # [B,H,S,d] views, no copy
                 attn = torch.empty((B, S, H * d), device=self.device, dtype=self.dt)
@@ -167,18 +175,23 @@ class Classifier:
                 if time_layers:
                     a1.record()
                 del qkv, q5, qv, kv, vv
-                o = attn.view(rows, hid) @ self.w[f"l{i}.wo"].t()
+                o = gemm_nt(attn.view(rows, hid), self.w[f"l{i}.wo"]) if own else attn.view(rows, hid) @ self.w[f"l{i}.wo"].t()
                 del attn
                 h2 = self._add_layernorm(x, o, self.w[f"l{i}.mlp_norm"])          # x += attn; h2 = LN(x)
                 del o
                 delta = torch.empty((rows, hid), device=self.device, dtype=self.dt)
                 for r0 in range(0, rows, cfg.mlp_chunk_rows):                     # bounded MLP intermediate
                     r1 = min(rows, r0 + cfg.mlp_chunk_rows)
-                    wi_out = h2[r0:r1] @ self.w[f"l{i}.wi"].t()                   # [chunk, 2*mlp]
-                    act = torch.empty((r1 - r0, cfg.mlp), device=self.device, dtype=self.dt)
-                    capi.check(lib.rf_geglu(wi_out.data_ptr(), act.data_ptr(), r1 - r0, cfg.mlp, cfg.rf_dtype, self._stream()))
-                    torch.matmul(act, self.w[f"l{i}.wo2"].t(), out=delta[r0:r1])
-                    del wi_out, act
+                    if own:                                                       # GeGLU fused into the up-projection
+                        act = gemm_nt(h2[r0:r1], self.w[f"l{i}.wi"], epilogue="geglu")
+                        gemm_nt(act, self.w[f"l{i}.wo2"], out=delta[r0:r1])
+                    else:
+                        wi_out = h2[r0:r1] @ self.w[f"l{i}.wi"].t()               # [chunk, 2*mlp]
+                        act = torch.empty((r1 - r0, cfg.mlp), device=self.device, dtype=self.dt)
+                        capi.check(lib.rf_geglu(wi_out.data_ptr(), act.data_ptr(), r1 - r0, cfg.mlp, cfg.rf_dtype, self._stream()))
+                        torch.matmul(act, self.w[f"l{i}.wo2"].t(), out=delta[r0:r1])
+                        del wi_out
+                    del act
                 del h2
                 h = None
                 if time_layers:
@@ -257,6 +270,7 @@ class NativeClassifier:
         c.mlp, c.global_every, c.local_window, c.n_labels = cfg.mlp, cfg.global_every, cfg.local_window, cfg.n_labels
         c.mlp_chunk_rows = cfg.mlp_chunk_rows
         c.act_dtype = cfg.rf_dtype
+        c.gemm_backend = capi.RF_CLF_GEMM_OWN if cfg.gemm == "own" else capi.RF_CLF_GEMM_CUBLAS
         c.rope_theta_global, c.rope_theta_local, c.eps = cfg.rope_theta_global, cfg.rope_theta_local, cfg.eps
         blob = pack_weights(cfg, weights)
         assert blob.numel() == self.lib.rf_clf_weight_elems(C.byref(c))

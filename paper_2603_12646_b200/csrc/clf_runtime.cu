@@ -35,6 +35,7 @@
 #include <vector>
 
 #include "../../include/rf_clf.h"
+#include "../../include/rf_gemm.h"
 #include "fa_internal.h"
 
 namespace {
@@ -280,8 +281,13 @@ int check_cfg(const rf_clf_config* c) {
     if (c->head_dim != 64) return fail(RF_ERR_HEAD_DIM, "the classifier session needs head_dim 64");
     if (c->hidden % 8 || c->hidden > 1024 || c->mlp % 8 || c->n_layers < 1 || c->vocab_size < 1 || c->n_labels < 1 ||
         c->global_every < 1 || c->local_window < 2 || c->mlp_chunk_rows < 1 ||
-        (c->act_dtype != RF_DTYPE_F16 && c->act_dtype != RF_DTYPE_BF16))
+        (c->act_dtype != RF_DTYPE_F16 && c->act_dtype != RF_DTYPE_BF16) ||
+        (c->gemm_backend != RF_CLF_GEMM_OWN && c->gemm_backend != RF_CLF_GEMM_CUBLAS))
         return fail(RF_ERR_ARG, "bad classifier config");
+    // rf_gemm_nt: accumulator tiles of 256 (or 192) columns, GeGLU slices of 128
+    if (c->gemm_backend == RF_CLF_GEMM_OWN && ((c->hidden % 256 && c->hidden % 192) || c->mlp % 128))
+        return fail(RF_ERR_UNSUPPORTED, "rf_gemm_nt needs hidden a multiple of 256 (or 192) and mlp a multiple of 128; "
+                                        "select RF_CLF_GEMM_CUBLAS for other shapes");
     return RF_OK;
 }
 
@@ -305,6 +311,7 @@ void rf_clf_config_default(rf_clf_config* c) {
     c->rope_theta_global = 160000.0f;
     c->rope_theta_local = 10000.0f;
     c->eps = 1e-5f;
+    c->gemm_backend = RF_CLF_GEMM_OWN;
 }
 
 size_t rf_clf_weight_elems(const rf_clf_config* c) {
@@ -332,7 +339,8 @@ int rf_clf_create(const rf_clf_config* cfg, const float* weights, size_t n_elems
     s->cfg = *cfg;
     s->device = device;
     std::string why;
-    if (!s->blas.load(&why)) {
+    const bool use_blas = cfg->gemm_backend == RF_CLF_GEMM_CUBLAS;
+    if (use_blas && !s->blas.load(&why)) {
         delete s;
         return fail(RF_ERR_CUDA, why);
     }
@@ -343,11 +351,13 @@ int rf_clf_create(const rf_clf_config* cfg, const float* weights, size_t n_elems
     if ((e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking)) != cudaSuccess) return bail(RF_ERR_CUDA, "cudaStreamCreate");
     cudaEventCreate(&s->ev0);
     cudaEventCreate(&s->ev1);
-    if (s->blas.create(&s->handle) != 0) return bail(RF_ERR_CUDA, "cublasCreate failed");
-    s->blas.set_stream(s->handle, s->stream);
-    constexpr size_t kBlasWorkspace = 32u << 20;
-    if ((e = cudaMalloc(&s->blas_ws, kBlasWorkspace)) != cudaSuccess) return bail(RF_ERR_CUDA, "cudaMalloc(cuBLAS workspace)");
-    if (s->blas.set_workspace(s->handle, s->blas_ws, kBlasWorkspace) != 0) return bail(RF_ERR_CUDA, "cublasSetWorkspace failed");
+    if (use_blas) {
+        if (s->blas.create(&s->handle) != 0) return bail(RF_ERR_CUDA, "cublasCreate failed");
+        s->blas.set_stream(s->handle, s->stream);
+        constexpr size_t kBlasWorkspace = 32u << 20;
+        if ((e = cudaMalloc(&s->blas_ws, kBlasWorkspace)) != cudaSuccess) return bail(RF_ERR_CUDA, "cudaMalloc(cuBLAS workspace)");
+        if (s->blas.set_workspace(s->handle, s->blas_ws, kBlasWorkspace) != 0) return bail(RF_ERR_CUDA, "cublasSetWorkspace failed");
+    }
 
     // split the blob: matrices -> bf16 block, vectors -> f32 block
     const size_t hid = cfg->hidden, mlp = cfg->mlp, V = cfg->vocab_size, NL = cfg->n_labels;
@@ -554,7 +564,9 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
         if (rc != RF_OK) return rc;
     }
 
+    const bool own_gemm = c.gemm_backend == RF_CLF_GEMM_OWN;
     auto gemm = [&](const uint16_t* a, const uint16_t* w, uint16_t* y, int64_t m, int n, int k) {
+        if (own_gemm) return rf_gemm_nt(a, w, y, m, n, k, 0, 0, 0, c.act_dtype, nullptr, st);
         // y[m, n] = a[m, k] @ w[n, k]^T, row-major == column-major y^T[n, m] = w^T(k x n)^T * a^T(k x m)
         const float alpha = 1.f, beta = 0.f;
         const int ty = c.act_dtype == RF_DTYPE_BF16 ? kCudaR16BF : kCudaR16F;
@@ -583,9 +595,19 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
         const LayerW& w = s->layers[i];
         // (for i > 0 the LN that produced h also added the previous layer's MLP output into x: see the loop tail)
         uint16_t* h = slot[cur];
-        RF_TRY(gemm(h, w.wqkv, big, rows, 3 * hid, hid));                       // qkv [rows, 3*hid] == [B,S,3,H,d]
         const bool glob = i % c.global_every == 0;
-        RF_TRY(rf_rope_qkv(big, rope[glob ? 0 : 2], rope[glob ? 1 : 3], rows, S, H, d, dt, st));
+        if (own_gemm) {  // qkv [rows, 3*hid] == [B,S,3,H,d], rotary embedding applied in the projection's epilogue
+            rf_gemm_epilogue ep{};
+            ep.kind = RF_GEMM_EPI_ROPE;
+            ep.head_dim = d;
+            ep.S = S;
+            ep.cos_table = rope[glob ? 0 : 2];
+            ep.sin_table = rope[glob ? 1 : 3];
+            RF_TRY(rf_gemm_nt(h, w.wqkv, big, rows, 3 * hid, hid, 0, 0, 0, dt, &ep, st));
+        } else {
+            RF_TRY(gemm(h, w.wqkv, big, rows, 3 * hid, hid));
+            RF_TRY(rf_rope_qkv(big, rope[glob ? 0 : 2], rope[glob ? 1 : 3], rows, S, H, d, dt, st));
+        }
         uint16_t* attn = slot[cur ^ 1];
         fp.q = big;
         fp.k = big + hid;
@@ -603,8 +625,14 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
             const int64_t r1 = std::min(rows, r0 + chunk);
             uint16_t* wi_out = big;                                         // qkv is dead
             uint16_t* act = big + static_cast<size_t>(chunk) * 2 * c.mlp;
-            RF_TRY(gemm(h2 + r0 * hid, w.wi, wi_out, r1 - r0, 2 * c.mlp, hid));
-            RF_TRY(rf_geglu(wi_out, act, r1 - r0, c.mlp, dt, st));
+            if (own_gemm) {  // act = gelu(h2 Wi_in^T) * (h2 Wi_gate^T) straight out of the up-projection
+                rf_gemm_epilogue ep{};
+                ep.kind = RF_GEMM_EPI_GEGLU;
+                RF_TRY(rf_gemm_nt(h2 + r0 * hid, w.wi, act, r1 - r0, 2 * c.mlp, hid, 0, 0, 0, dt, &ep, st));
+            } else {
+                RF_TRY(gemm(h2 + r0 * hid, w.wi, wi_out, r1 - r0, 2 * c.mlp, hid));
+                RF_TRY(rf_geglu(wi_out, act, r1 - r0, c.mlp, dt, st));
+            }
             RF_TRY(gemm(act, w.wo2, delta + r0 * hid, r1 - r0, hid, c.mlp));
         }
         // x += mlp out; h = LN(x) with the next layer's attn_norm (or the final norm)

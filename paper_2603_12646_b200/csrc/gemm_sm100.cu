@@ -37,14 +37,14 @@ namespace {
 
 using namespace rfptx;
 
-constexpr int kBM = 128, kBN = 256, kBK = 64;
+constexpr int kBM = 128, kBK = 64;
+constexpr int kBNMax = 256;                   // accumulator tile width: 256, or 192 where that saves a round of tiles
 constexpr int kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;        // 16 KiB
-constexpr int kBBytes = kBN * kBK * 2;        // 32 KiB (two 128-row boxes)
-constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kStageBytes = kABytes + kBNMax * kBK * 2;  // A + W tile (two boxes of kBN / 2 rows)
 constexpr int kThreads = 192;
 constexpr int kEpiWarps = 4;
-constexpr uint32_t kTmemCols = 512;           // two accumulators of 256 columns
+constexpr uint32_t kTmemCols = 512;           // two accumulators of up to 256 columns
 constexpr int kCluster = 2;                   // CTA pair: adjacent row tiles of the same column tile share W
 constexpr int kOutBoxBytes = 32 * 64 * 2;     // one TMA-store box: 32 rows x 64 columns of 16-bit output
 
@@ -91,10 +91,13 @@ __device__ __forceinline__ void stage16(uint32_t box, int lane, int chunk, const
                  : "memory");
 }
 
-template <bool kBf16, int kEpi>
+template <bool kBf16, int kEpi, int kBN>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_nt_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_w,
                      const __grid_constant__ CUtensorMap tm_y, const GemmParams p) {
+    static_assert(kBN == 256 || (kBN == 192 && kEpi != RF_GEMM_EPI_GEGLU), "tile widths");
+    constexpr int kBBytes = kBN * kBK * 2;     // W tile: two boxes of kBN / 2 rows
+    constexpr uint32_t kTxBytes = kABytes + kBBytes;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem_gen = smem_raw + (smem_base - smem_u32(smem_raw));
@@ -149,13 +152,13 @@ gemm_nt_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
             const int nb = t % p.n_tiles;
             // weight rows of the tile's two 128-row boxes; box `rank` is ours to load
             const int w_row = kEpi == RF_GEMM_EPI_GEGLU ? (rank == 0 ? nb * 128 : p.gate_row0 + nb * 128)
-                                                        : nb * kBN + static_cast<int>(rank) * 128;
+                                                        : nb * kBN + static_cast<int>(rank) * (kBN / 2);
             for (int kb = 0; kb < k_blocks; ++kb, ++it) {
                 const uint32_t s = it % kStages;
                 mbar_wait(bar(kBarEmpty + s), ((it / kStages) & 1) ^ 1, wctx);
                 if (lane == 0) {
                     const uint32_t dst = smem_base + Smem::tiles + s * kStageBytes;
-                    mbar_arrive_expect_tx(bar(kBarFull + s), kStageBytes);
+                    mbar_arrive_expect_tx(bar(kBarFull + s), kTxBytes);
                     tma_load_2d(dst, &tm_a, bar(kBarFull + s), kb * kBK, m0);
                     tma_load_2d_multicast(dst + kABytes + rank * (kBBytes / 2), &tm_w, bar(kBarFull + s), kb * kBK, w_row,
                                           static_cast<uint16_t>((1u << kCluster) - 1u));
@@ -173,7 +176,7 @@ gemm_nt_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
             // the epilogue has drained this accumulator (two tiles ago)
             mbar_wait(bar(kBarAccEmpty + acc), ((tile_n >> 1) & 1) ^ 1, wctx);
             tc_fence_after();
-            const uint32_t td = tmem_base + acc * kBN;
+            const uint32_t td = tmem_base + acc * kBNMax;
             for (int kb = 0; kb < k_blocks; ++kb, ++it) {
                 const uint32_t s = it % kStages;
                 mbar_wait(bar(kBarFull + s), (it / kStages) & 1, wctx);
@@ -221,7 +224,7 @@ gemm_nt_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
             const int nb = t % p.n_tiles;
             mbar_wait(bar(kBarAccFull + acc), (tile_n >> 1) & 1, wctx);
             tc_fence_after();
-            const uint32_t ta = tmem_base + lane_base + acc * kBN;
+            const uint32_t ta = tmem_base + lane_base + acc * kBNMax;
             if (kEpi == RF_GEMM_EPI_NONE) {
 #pragma unroll 1
                 for (int c = 0; c < kBN / 64; ++c) {
@@ -346,10 +349,10 @@ int make_map(CUtensorMap* tm, const void* base, int dtype, int64_t rows, int64_t
     return RF_OK;
 }
 
-template <bool kBf16, int kEpi>
+template <bool kBf16, int kEpi, int kBN>
 cudaError_t launch(const CUtensorMap& tma, const CUtensorMap& tmw, const CUtensorMap& tmy, const GemmParams& p, int grid,
                    cudaStream_t stream) {
-    auto kern = gemm_nt_sm100_kernel<kBf16, kEpi>;
+    auto kern = gemm_nt_sm100_kernel<kBf16, kEpi, kBN>;
     const size_t smem = Smem::total + 1024;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -393,20 +396,30 @@ int rf_gemm_nt(const void* a, const void* w, void* y, int64_t M, int64_t N, int6
     if (ldy == 0) ldy = out_cols;
     if (!aligned16(a) || !aligned16(w) || !aligned16(y) || lda % 8 || ldw % 8 || ldy % 8 || K % 8)
         return fail(RF_ERR_UNSUPPORTED, "rf_gemm_nt: pointers must be 16-byte aligned, K and the leading dimensions multiples of 8");
-    if (N % kBN) return fail(RF_ERR_UNSUPPORTED, "rf_gemm_nt: N must be a multiple of 256");
-    if (M > (1ll << 31) - kBM || N > (1 << 30) || K > (1 << 30)) return fail(RF_ERR_ARG, "rf_gemm_nt: dimension too large");
+    if (M > (1ll << 31) - 2 * kBM || N > (1 << 30) || K > (1 << 30)) return fail(RF_ERR_ARG, "rf_gemm_nt: dimension too large");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t m_pairs = (M + kCluster * kBM - 1) / (kCluster * kBM);
+    const int64_t slots = std::max(1, sms / kCluster);  // CTA pairs resident at once
+    // Accumulator tile width: 256 columns, or 192 where that takes fewer (rounds of tiles) x (tile width) -- e.g. the
+    // 768-wide projections at 8K tokens: 96 pair-tiles of 256 run as 2 rounds on 74 pairs, 128 of 192 too, in 3/4 of the time
+    auto cost = [&](int bn) { return (N % bn) ? INT64_MAX : ((m_pairs * (N / bn) + slots - 1) / slots) * bn; };
+    const bool can192 = kind != RF_GEMM_EPI_GEGLU && (kind != RF_GEMM_EPI_ROPE || (N / 3) % 192 == 0);
+    const int bn = (can192 && cost(192) < cost(256)) ? 192 : 256;
+    if (N % bn) return fail(RF_ERR_UNSUPPORTED, "rf_gemm_nt: N must be a multiple of 256 (or of 192)");
     GemmParams p{};
     p.M = M;
     p.N = static_cast<int>(N);
     p.K = static_cast<int>(K);
-    p.m_pairs = static_cast<int>((M + kCluster * kBM - 1) / (kCluster * kBM));
-    p.n_tiles = static_cast<int>(N / kBN);
+    p.m_pairs = static_cast<int>(m_pairs);
+    p.n_tiles = static_cast<int>(N / bn);
     p.status = nullptr;
     if (kind == RF_GEMM_EPI_ROPE) {
         if (epi->cos_table == nullptr || epi->sin_table == nullptr || epi->S <= 0 || epi->head_dim != 64)
             return fail(RF_ERR_ARG, "rf_gemm_nt: the RoPE epilogue needs cos/sin tables [S, 32], S > 0 and head_dim 64");
-        if (N % 3 || (N / 3) % kBN)
-            return fail(RF_ERR_UNSUPPORTED, "rf_gemm_nt: the RoPE epilogue needs a packed QKV width 3 * hidden with hidden a multiple of 256");
+        if (N % 3 || (N / 3) % bn)
+            return fail(RF_ERR_UNSUPPORTED, "rf_gemm_nt: the RoPE epilogue needs a packed QKV width 3 * hidden with hidden a multiple of the tile width");
         p.cos_t = epi->cos_table;
         p.sin_t = epi->sin_table;
         p.S = static_cast<int>(epi->S);
@@ -418,25 +431,28 @@ int rf_gemm_nt(const void* a, const void* w, void* y, int64_t M, int64_t N, int6
     CUtensorMap tma, tmw, tmy;
     int rc = make_map(&tma, a, dtype, M, K, lda, 128);
     if (rc != RF_OK) return rc;
-    if ((rc = make_map(&tmw, w, dtype, N, K, ldw, 128)) != RF_OK) return rc;
+    if ((rc = make_map(&tmw, w, dtype, N, K, ldw, bn / 2)) != RF_OK) return rc;
     if ((rc = make_map(&tmy, y, dtype, M, out_cols, ldy, 32)) != RF_OK) return rc;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // one CTA pair per two SMs, persistent over the (row-tile pair, column tile) space
-    const int grid = kCluster * static_cast<int>(std::min<int64_t>(static_cast<int64_t>(p.m_pairs) * p.n_tiles, sms / kCluster));
+    const int grid = kCluster * static_cast<int>(std::min<int64_t>(static_cast<int64_t>(p.m_pairs) * p.n_tiles, slots));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const bool bf = dtype == RF_DTYPE_BF16;
     cudaError_t e;
     switch (kind) {
         case RF_GEMM_EPI_ROPE:
-            e = bf ? launch<true, RF_GEMM_EPI_ROPE>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_ROPE>(tma, tmw, tmy, p, grid, st);
+            if (bn == 192)
+                e = bf ? launch<true, RF_GEMM_EPI_ROPE, 192>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_ROPE, 192>(tma, tmw, tmy, p, grid, st);
+            else
+                e = bf ? launch<true, RF_GEMM_EPI_ROPE, 256>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_ROPE, 256>(tma, tmw, tmy, p, grid, st);
             break;
         case RF_GEMM_EPI_GEGLU:
-            e = bf ? launch<true, RF_GEMM_EPI_GEGLU>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_GEGLU>(tma, tmw, tmy, p, grid, st);
+            e = bf ? launch<true, RF_GEMM_EPI_GEGLU, 256>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_GEGLU, 256>(tma, tmw, tmy, p, grid, st);
             break;
         default:
-            e = bf ? launch<true, RF_GEMM_EPI_NONE>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_NONE>(tma, tmw, tmy, p, grid, st);
+            if (bn == 192)
+                e = bf ? launch<true, RF_GEMM_EPI_NONE, 192>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_NONE, 192>(tma, tmw, tmy, p, grid, st);
+            else
+                e = bf ? launch<true, RF_GEMM_EPI_NONE, 256>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_NONE, 256>(tma, tmw, tmy, p, grid, st);
     }
     if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("rf_gemm_nt launch: ") + cudaGetErrorString(e));
     return RF_OK;
