@@ -30,18 +30,18 @@ EXPORTS = [
     "rf_graph_result_is_f16", "rf_graph_result_stats", "rf_graph_result_free",
     # include/rf_clf.h
     "rf_clf_config_default", "rf_clf_weight_elems", "rf_clf_create", "rf_clf_forward", "rf_clf_session_bytes",
-    "rf_clf_last_forward_ms", "rf_clf_destroy",
+    "rf_clf_last_forward_ms", "rf_clf_destroy", "rf_clf_head",
     # include/rf_gemm.h
     "rf_gemm_nt",
 ]
 
-RF_GEMM_EPI_NONE, RF_GEMM_EPI_ROPE, RF_GEMM_EPI_GEGLU = 0, 1, 2
+RF_GEMM_EPI_NONE, RF_GEMM_EPI_ROPE, RF_GEMM_EPI_GEGLU, RF_GEMM_EPI_RESIDUAL = 0, 1, 2, 3
 RF_CLF_GEMM_OWN, RF_CLF_GEMM_CUBLAS = 0, 1
 
 
 class RfGemmEpilogue(C.Structure):
     _fields_ = [("kind", C.c_int32), ("head_dim", C.c_int32), ("S", C.c_int64), ("cos_table", C.c_void_p),
-                ("sin_table", C.c_void_p)]
+                ("sin_table", C.c_void_p), ("out_dtype", C.c_int32), ("head_major", C.c_int32)]
 
 
 class RfClfConfig(C.Structure):
@@ -162,6 +162,8 @@ def load(build_if_missing: bool = True):
     lib.rf_clf_last_forward_ms.restype = C.c_float
     lib.rf_clf_destroy.argtypes = [vp]
     lib.rf_clf_destroy.restype = None
+    lib.rf_clf_head.argtypes = [vp, i64, i64, i32, vp, vp, vp, vp, i32, C.c_float, i32, vp, vp]
+    lib.rf_clf_head.restype = C.c_int
     lib.rf_gemm_nt.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i32, C.POINTER(RfGemmEpilogue), vp]
     lib.rf_gemm_nt.restype = C.c_int
     for name in ("rf_fa_validate", "rf_fa_fwd_workspace_bytes", "rf_fa_stats_query", "rf_fa_fwd", "rf_fa_merge",

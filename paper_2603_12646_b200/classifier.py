@@ -13,8 +13,9 @@ Data path per layer (16-bit GEMM operands -- f16 by default, bf16 selectable -- 
   h   = LN(x)                       rf_add_layernorm (fused with the previous residual add)
   qkv = rope(h @ Wqkv^T)            rf_gemm_nt, rotary embedding in the epilogue -> [B,S,3,H,d]
   o   = FusedFlashAttention(q,k,v)  strided views of qkv in, [B,S,H*d] out: no transposes
-  x  += o @ Wo^T ; h2 = LN(x)       rf_gemm_nt + rf_add_layernorm
-  x  += (gelu(h2 Wi_a) * h2 Wi_g) Wo2    in row chunks (bounds activation memory); GeGLU in the up-projection's epilogue
+  x  += o @ Wo^T ; h2 = LN(x)       rf_gemm_nt (f32 accumulators added into the stream by TMA reduce-add) + rf_add_layernorm
+  x  += (gelu(h2 Wi_a) * h2 Wi_g) Wo2    in row chunks (bounds activation memory); GeGLU in the up-projection's epilogue,
+                                    the residual add in the down-projection's
 The projections are this library's own tcgen05 GEMM (rf_gemm.h); `gemm="cublas"` selects the round-1 path (library
 GEMMs through torch.matmul + rf_rope_qkv / rf_geglu) for A/B measurements.  All glue and the attention are the
 hand-written kernels of librf_fa.so.
@@ -55,6 +56,12 @@ class ClassifierConfig:
     # projections: "own" = rf_gemm_nt (this library's tcgen05 GEMM, RoPE fused into the QKV projection and GeGLU into
     # the MLP up-projection); "cublas" = library GEMMs + rf_rope_qkv / rf_geglu (the round-1 path, kept for A/B runs)
     gemm: str = "own"
+    # f16 encoder, global layers only (gemm="own"): the QKV projection writes Q, K, V as bf16 and the dense attention
+    # kernel runs its bf16 instantiation (output still f16).  bf16 P has f32's exponent range, so the kernel's lazy
+    # rescale slack is 2^20 instead of 2^14 and its row-max skip keeps passing on normal-distributed projections
+    # (8K op: 267 -> 215 us); Q/K/V lose 3 significant bits in 1 layer of 3.  Off by default: with random-init
+    # weights the projections are small and the f16 skip test passes anyway (no measurable difference).
+    global_qkv_bf16: bool = False
 
     @property
     def torch_dtype(self):
@@ -158,13 +165,19 @@ class Classifier:
                 glob = cfg.is_global(i)
                 cos, sin = self._rope_tables(S, glob)
                 if own:                                                           # [rows, 3*hid] == [B,S,3,H,d], RoPE fused
-                    qkv = gemm_nt(h, self.w[f"l{i}.wqkv"], epilogue="rope", rope_cos=cos, rope_sin=sin, seq_len=S)
+                    # head-major [3, H, B*S, d]: each head's Q / K / V rows are contiguous for the attention kernel's TMA
+                    qkv = gemm_nt(h, self.w[f"l{i}.wqkv"], epilogue="rope", rope_cos=cos, rope_sin=sin, seq_len=S,
+                                  out_dtype=torch.bfloat16 if (glob and cfg.global_qkv_bf16) else None, head_major=True)
                 else:
                     qkv = h @ self.w[f"l{i}.wqkv"].t()
                     capi.check(lib.rf_rope_qkv(qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), rows, S, H, d, cfg.rf_dtype, self._stream()))
                 del h, delta                                                      # keep the live set small (32K)
-                q5 = qkv.view(B, S, 3, H, d)
-                qv, kv, vv = (q5[:, :, j].permute(0, 2, 1, 3) for j in range(3))  # [B,H,S,d] views, no copy
+                if own:
+                    q5 = qkv.view(3, H, B, S, d)
+                    qv, kv, vv = (q5[j].permute(1, 0, 2, 3) for j in range(3))    # [B,H,S,d] views, no copy
+                else:
+                    q5 = qkv.view(B, S, 3, H, d)
+                    qv, kv, vv = (q5[:, :, j].permute(0, 2, 1, 3) for j in range(3))  # [B,H,S,d] views, no copy
                 attn = torch.empty((B, S, H * d), device=self.device, dtype=self.dt)
                 wl, wr = local_window_attrs(RewriteOptions(d, cfg.local_window), is_global=glob)
                 if time_layers:
@@ -175,16 +188,20 @@ class Classifier:
                 if time_layers:
                     a1.record()
                 del qkv, q5, qv, kv, vv
-                o = gemm_nt(attn.view(rows, hid), self.w[f"l{i}.wo"]) if own else attn.view(rows, hid) @ self.w[f"l{i}.wo"].t()
+                if own:                                                           # x += attn Wo^T in the epilogue; h2 = LN(x)
+                    gemm_nt(attn.view(rows, hid), self.w[f"l{i}.wo"], out=x, epilogue="residual")
+                    o = None
+                else:
+                    o = attn.view(rows, hid) @ self.w[f"l{i}.wo"].t()
                 del attn
-                h2 = self._add_layernorm(x, o, self.w[f"l{i}.mlp_norm"])          # x += attn; h2 = LN(x)
+                h2 = self._add_layernorm(x, o, self.w[f"l{i}.mlp_norm"])          # (x += attn;) h2 = LN(x)
                 del o
-                delta = torch.empty((rows, hid), device=self.device, dtype=self.dt)
+                delta = None if own else torch.empty((rows, hid), device=self.device, dtype=self.dt)
                 for r0 in range(0, rows, cfg.mlp_chunk_rows):                     # bounded MLP intermediate
                     r1 = min(rows, r0 + cfg.mlp_chunk_rows)
                     if own:                                                       # GeGLU fused into the up-projection
                         act = gemm_nt(h2[r0:r1], self.w[f"l{i}.wi"], epilogue="geglu")
-                        gemm_nt(act, self.w[f"l{i}.wo2"], out=delta[r0:r1])
+                        gemm_nt(act, self.w[f"l{i}.wo2"], out=x[r0:r1], epilogue="residual")   # x += mlp out
                     else:
                         wi_out = h2[r0:r1] @ self.w[f"l{i}.wi"].t()               # [chunk, 2*mlp]
                         act = torch.empty((r1 - r0, cfg.mlp), device=self.device, dtype=self.dt)
@@ -199,10 +216,16 @@ class Classifier:
                     e1.record()
                     ev.append((glob, e0, e1, a0, a1))
             hf = self._add_layernorm(x, delta, self.w["final_norm"])              # x += mlp(last); LN
-            pooled = hf.view(B, S, hid)[:, 0]                                     # CLS pooling
-            t = torch.nn.functional.gelu((pooled @ self.w["head_dense"].t()).float())
-            t = torch.nn.functional.layer_norm(t, (hid,), self.w["head_norm"], None, cfg.eps)
-            logits = t @ self.w["cls_w"].float().t() + self.w["cls_b"]
+            if own:                                                               # CLS pooling + head, one kernel
+                logits = torch.empty((B, cfg.n_labels), device=self.device, dtype=torch.float32)
+                capi.check(lib.rf_clf_head(hf.data_ptr(), B, S, hid, self.w["head_dense"].data_ptr(), self.w["head_norm"].data_ptr(),
+                                           self.w["cls_w"].data_ptr(), self.w["cls_b"].data_ptr(), cfg.n_labels, cfg.eps,
+                                           cfg.rf_dtype, logits.data_ptr(), self._stream()))
+            else:
+                pooled = hf.view(B, S, hid)[:, 0]                                 # CLS pooling
+                t = torch.nn.functional.gelu((pooled @ self.w["head_dense"].t()).float())
+                t = torch.nn.functional.layer_norm(t, (hid,), self.w["head_norm"], None, cfg.eps)
+                logits = t @ self.w["cls_w"].float().t() + self.w["cls_b"]
             if time_layers:
                 torch.cuda.synchronize(self.device)
                 self.last_layer_ms = [{"layer": i, "global": g_, "layer_ms": e0.elapsed_time(e1), "attention_ms": a0.elapsed_time(a1)}

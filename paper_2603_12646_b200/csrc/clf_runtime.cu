@@ -441,8 +441,11 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
     fp.out_dtype = c.act_dtype;
     fp.B = B; fp.H = H; fp.S = S; fp.d = d;
     const int64_t tok = 3ll * hid;
-    const int64_t qs[3] = {S * tok, d, tok};
-    for (int i = 0; i < 3; ++i) fp.q_stride[i] = fp.k_stride[i] = fp.v_stride[i] = qs[i];
+    // library GEMM: packed [B,S,3,H,d]; own projection: head-major [3,H,B*S,d] (each head's rows contiguous for the TMA)
+    const bool head_major = c.gemm_backend == RF_CLF_GEMM_OWN;
+    const int64_t qs_packed[3] = {S * tok, d, tok};
+    const int64_t qs_heads[3] = {S * static_cast<int64_t>(d), B * S * static_cast<int64_t>(d), d};
+    for (int i = 0; i < 3; ++i) fp.q_stride[i] = fp.k_stride[i] = fp.v_stride[i] = head_major ? qs_heads[i] : qs_packed[i];
     fp.o_stride[0] = S * static_cast<int64_t>(hid); fp.o_stride[1] = d; fp.o_stride[2] = hid;
     // workspace: the larger of the global and the local layer's needs (the pointers only matter for alignment checks)
     size_t ws_need = 0;
@@ -603,6 +606,7 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
             ep.S = S;
             ep.cos_table = rope[glob ? 0 : 2];
             ep.sin_table = rope[glob ? 1 : 3];
+            ep.head_major = 1;
             RF_TRY(rf_gemm_nt(h, w.wqkv, big, rows, 3 * hid, hid, 0, 0, 0, dt, &ep, st));
         } else {
             RF_TRY(gemm(h, w.wqkv, big, rows, 3 * hid, hid));
@@ -610,16 +614,23 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
         }
         uint16_t* attn = slot[cur ^ 1];
         fp.q = big;
-        fp.k = big + hid;
-        fp.v = big + 2 * hid;
+        fp.k = big + (head_major ? rows * hid : hid);
+        fp.v = big + 2 * (head_major ? rows * hid : hid);
         fp.out = attn;
         fp.window_left = glob ? -1 : c.local_window / 2 - 1;                    // rewrite.cpp:355-361
         fp.window_right = glob ? -1 : c.local_window / 2;
         RF_TRY(rf_fa_fwd(&fp, base + L.ws, L.ws_bytes, st));
         uint16_t* o = slot[cur];                                            // h is dead
-        RF_TRY(gemm(attn, w.wo, o, rows, hid, hid));
-        uint16_t* h2 = slot[cur ^ 1];                                       // attn is dead
-        RF_TRY(rf_add_layernorm(x, o, w.mlp_norm, h2, rows, hid, c.eps, dt, st));    // x += attn out; h2 = LN(x)
+        uint16_t* h2 = slot[cur ^ 1];                                       // (attn is dead once the projection has run)
+        rf_gemm_epilogue res{};
+        res.kind = RF_GEMM_EPI_RESIDUAL;
+        if (own_gemm) {  // x += attn Wo^T inside the projection (TMA reduce-add of the f32 accumulators); h2 = LN(x)
+            RF_TRY(rf_gemm_nt(attn, w.wo, x, rows, hid, hid, 0, 0, 0, dt, &res, st));
+            RF_TRY(rf_add_layernorm(x, nullptr, w.mlp_norm, h2, rows, hid, c.eps, dt, st));
+        } else {
+            RF_TRY(gemm(attn, w.wo, o, rows, hid, hid));
+            RF_TRY(rf_add_layernorm(x, o, w.mlp_norm, h2, rows, hid, c.eps, dt, st));    // x += attn out; h2 = LN(x)
+        }
         uint16_t* delta = slot[cur];                                        // o is dead
         for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
             const int64_t r1 = std::min(rows, r0 + chunk);
@@ -629,6 +640,8 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
                 rf_gemm_epilogue ep{};
                 ep.kind = RF_GEMM_EPI_GEGLU;
                 RF_TRY(rf_gemm_nt(h2 + r0 * hid, w.wi, act, r1 - r0, 2 * c.mlp, hid, 0, 0, 0, dt, &ep, st));
+                RF_TRY(rf_gemm_nt(act, w.wo2, x + r0 * hid, r1 - r0, hid, c.mlp, 0, 0, 0, dt, &res, st));  // x += mlp out
+                continue;
             } else {
                 RF_TRY(gemm(h2 + r0 * hid, w.wi, wi_out, r1 - r0, 2 * c.mlp, hid));
                 RF_TRY(rf_geglu(wi_out, act, r1 - r0, c.mlp, dt, st));
@@ -637,7 +650,7 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
         }
         // x += mlp out; h = LN(x) with the next layer's attn_norm (or the final norm)
         const float* next_norm = i + 1 < c.n_layers ? s->layers[i + 1].attn_norm : s->final_norm;
-        RF_TRY(rf_add_layernorm(x, delta, next_norm, slot[cur ^ 1], rows, hid, c.eps, dt, st));  // h2 is dead
+        RF_TRY(rf_add_layernorm(x, own_gemm ? nullptr : delta, next_norm, slot[cur ^ 1], rows, hid, c.eps, dt, st));  // h2 is dead
         cur ^= 1;
     }
     if (bf)
@@ -685,6 +698,26 @@ int rf_clf_session_bytes(const rf_clf* s, size_t* weight_bytes, size_t* arena_by
 }
 
 float rf_clf_last_forward_ms(const rf_clf* s) { return s != nullptr ? s->last_ms : 0.f; }
+
+int rf_clf_head(const void* hf, int64_t B, int64_t S, int32_t hidden, const void* head_dense, const float* head_norm,
+                const void* cls_w, const float* cls_b, int32_t n_labels, float eps, int32_t dtype, float* logits,
+                void* stream) {
+    if (hf == nullptr || head_dense == nullptr || head_norm == nullptr || cls_w == nullptr || cls_b == nullptr || logits == nullptr)
+        return fail(RF_ERR_ARG, "rf_clf_head: null pointer");
+    if (B < 0 || S < 1 || hidden < 2 || hidden > 1024 || hidden % 2 || n_labels < 1) return fail(RF_ERR_SHAPE, "rf_clf_head: bad shape");
+    if (dtype != RF_DTYPE_F16 && dtype != RF_DTYPE_BF16) return fail(RF_ERR_ARG, "rf_clf_head: dtype must be bf16 or f16");
+    if (B == 0) return RF_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint16_t* h16 = static_cast<const uint16_t*>(hf);
+    const uint16_t* wd = static_cast<const uint16_t*>(head_dense);
+    const uint16_t* wc = static_cast<const uint16_t*>(cls_w);
+    if (dtype == RF_DTYPE_BF16)
+        clf_head_kernel<true><<<static_cast<unsigned>(B), 256, 0, st>>>(h16, S, hidden, wd, head_norm, wc, cls_b, n_labels, eps, logits);
+    else
+        clf_head_kernel<false><<<static_cast<unsigned>(B), 256, 0, st>>>(h16, S, hidden, wd, head_norm, wc, cls_b, n_labels, eps, logits);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RF_OK : cuda_fail(e, "rf_clf_head launch");
+}
 
 void rf_clf_destroy(rf_clf* s) {
     if (s == nullptr) return;

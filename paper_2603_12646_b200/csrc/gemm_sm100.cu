@@ -9,6 +9,9 @@
 //   RF_GEMM_EPI_GEGLU   w is the MLP up-projection [2*I, K] (input half, then gate half); the kernel computes both
 //                       halves of a 128-column slice in one tile and stores act[m, j] = gelu(in) * gate, [M, I]
 //                                                                            (replaces rf_geglu and its 2*I-wide buffer)
+//   RF_GEMM_EPI_RESIDUAL y is the f32 residual stream: y += a w^T, the f32 accumulators added in place by TMA reduce-add
+//                       (out-projection and MLP down-projection inside the encoder: the residual add leaves
+//                       rf_add_layernorm, which then only reads the stream)
 //
 // One persistent CTA per SM, 6 warps:
 //   warp 0      TMA producer: per 64-wide K block one 128 x 64 box of A and two 128 x 64 boxes of W (128B swizzle)
@@ -57,6 +60,8 @@ struct GemmParams {
     const float* sin_t;
     int S;                // ROPE: token t has position t % S
     int rope_cols;        // ROPE: columns [0, rope_cols) are rotated (the Q and K thirds)
+    int head_major;       // ROPE: y is [3*H, tokens, 64] (3-D tensor map) instead of [tokens, 3*H*64]
+    int out_bf16;         // ROPE: 16-bit type of the output (may differ from the operands': rf_gemm_epilogue.out_dtype)
     int* status;          // bounded-wait status word (ptx.cuh), may be null
 };
 
@@ -212,7 +217,9 @@ gemm_nt_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-                tma_store_2d(&tm_y, out_base + (boxes & 1) * kOutBoxBytes, col, row0);
+                if (kEpi == RF_GEMM_EPI_RESIDUAL) tma_reduce_add_2d(&tm_y, out_base + (boxes & 1) * kOutBoxBytes, col, row0);
+                else if (kEpi == RF_GEMM_EPI_ROPE && p.head_major) tma_store_3d(&tm_y, out_base + (boxes & 1) * kOutBoxBytes, 0, row0, col >> 6);
+                else tma_store_2d(&tm_y, out_base + (boxes & 1) * kOutBoxBytes, col, row0);
                 bulk_commit_group();
             }
             ++boxes;
@@ -241,6 +248,23 @@ gemm_nt_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
                         stage16<kBf16>(box, lane, u, f);
                     }
                     end_box(nb * kBN + c * 64, row0);
+                }
+            } else if (kEpi == RF_GEMM_EPI_RESIDUAL) {
+                // f32 boxes of 32 x 32 (128-byte rows): 16-byte chunk u of row `lane` holds columns 4u .. 4u + 3
+#pragma unroll 1
+                for (int c = 0; c < kBN / 32; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(ta + c * 32, v);
+                    tc_wait_ld();
+                    const uint32_t box = begin_box();
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t addr = box + lane * 128 + ((u ^ (lane & 7)) << 4);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v[4 * u]), "r"(v[4 * u + 1]),
+                                     "r"(v[4 * u + 2]), "r"(v[4 * u + 3])
+                                     : "memory");
+                    }
+                    end_box(nb * kBN + c * 32, row0);
                 }
             } else if (kEpi == RF_GEMM_EPI_ROPE) {
                 const int col0 = nb * kBN;
@@ -273,8 +297,13 @@ gemm_nt_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
                             f1[e] = rotate ? x1 * cs[8 * u + e] - x2 * sn[8 * u + e] : x1;
                             f2[e] = rotate ? x2 * cs[8 * u + e] + x1 * sn[8 * u + e] : x2;
                         }
-                        stage16<kBf16>(box, lane, u, f1);
-                        stage16<kBf16>(box, lane, 4 + u, f2);
+                        if (p.out_bf16) {
+                            stage16<true>(box, lane, u, f1);
+                            stage16<true>(box, lane, 4 + u, f2);
+                        } else {
+                            stage16<false>(box, lane, u, f1);
+                            stage16<false>(box, lane, 4 + u, f2);
+                        }
                     }
                     end_box(col0 + hd * 64, row0);
                 }
@@ -336,13 +365,14 @@ EncodeTiledFn encode_fn() {
 
 // [rows, cols] row-major 16-bit matrix with `ld` elements between rows; box = 64 columns x box_rows rows, 128B swizzle
 int make_map(CUtensorMap* tm, const void* base, int dtype, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+    const bool f32 = dtype == RF_DTYPE_F32;  // (the residual stream: 32-column boxes, still 128-byte rows)
     EncodeTiledFn enc = encode_fn();
     if (enc == nullptr) return set_last_error(RF_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable (driver too old?)");
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-    const cuuint32_t box[2] = {kBK, static_cast<cuuint32_t>(box_rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * (f32 ? 4 : 2)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(f32 ? 32 : kBK), static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult res = enc(tm, dtype == RF_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+    const CUresult res = enc(tm, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : dtype == RF_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
                              const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res != CUDA_SUCCESS) return set_last_error(RF_ERR_CUDA, "cuTensorMapEncodeTiled failed, CUresult " + std::to_string(res));
@@ -391,10 +421,10 @@ int rf_gemm_nt(const void* a, const void* w, void* y, int64_t M, int64_t N, int6
     if (lda == 0) lda = K;
     if (ldw == 0) ldw = K;
     const int kind = epi != nullptr ? epi->kind : RF_GEMM_EPI_NONE;
-    if (kind < RF_GEMM_EPI_NONE || kind > RF_GEMM_EPI_GEGLU) return fail(RF_ERR_ARG, "rf_gemm_nt: bad epilogue kind");
+    if (kind < RF_GEMM_EPI_NONE || kind > RF_GEMM_EPI_RESIDUAL) return fail(RF_ERR_ARG, "rf_gemm_nt: bad epilogue kind");
     const int64_t out_cols = kind == RF_GEMM_EPI_GEGLU ? N / 2 : N;
     if (ldy == 0) ldy = out_cols;
-    if (!aligned16(a) || !aligned16(w) || !aligned16(y) || lda % 8 || ldw % 8 || ldy % 8 || K % 8)
+    if (!aligned16(a) || !aligned16(w) || !aligned16(y) || lda % 8 || ldw % 8 || ldy % (kind == RF_GEMM_EPI_RESIDUAL ? 4 : 8) || K % 8)
         return fail(RF_ERR_UNSUPPORTED, "rf_gemm_nt: pointers must be 16-byte aligned, K and the leading dimensions multiples of 8");
     if (M > (1ll << 31) - 2 * kBM || N > (1 << 30) || K > (1 << 30)) return fail(RF_ERR_ARG, "rf_gemm_nt: dimension too large");
     int dev = 0, sms = 148;
@@ -424,6 +454,9 @@ int rf_gemm_nt(const void* a, const void* w, void* y, int64_t M, int64_t N, int6
         p.sin_t = epi->sin_table;
         p.S = static_cast<int>(epi->S);
         p.rope_cols = static_cast<int>(N / 3 * 2);
+        if (epi->out_dtype != 0 && epi->out_dtype != 1 + RF_DTYPE_BF16 && epi->out_dtype != 1 + RF_DTYPE_F16)
+            return fail(RF_ERR_ARG, "rf_gemm_nt: bad out_dtype");
+        p.out_bf16 = epi->out_dtype == 0 ? (dtype == RF_DTYPE_BF16) : (epi->out_dtype == 1 + RF_DTYPE_BF16);
     } else if (kind == RF_GEMM_EPI_GEGLU) {
         if ((N / 2) % 128) return fail(RF_ERR_UNSUPPORTED, "rf_gemm_nt: the GeGLU epilogue needs an intermediate width that is a multiple of 128");
         p.gate_row0 = static_cast<int>(N / 2);
@@ -432,7 +465,22 @@ int rf_gemm_nt(const void* a, const void* w, void* y, int64_t M, int64_t N, int6
     int rc = make_map(&tma, a, dtype, M, K, lda, 128);
     if (rc != RF_OK) return rc;
     if ((rc = make_map(&tmw, w, dtype, N, K, ldw, bn / 2)) != RF_OK) return rc;
-    if ((rc = make_map(&tmy, y, dtype, M, out_cols, ldy, 32)) != RF_OK) return rc;
+    if (kind == RF_GEMM_EPI_ROPE && epi->head_major) {
+        // [3*H, tokens, 64]: one 32-token x 64 box per (head, 32 tokens)
+        EncodeTiledFn enc = encode_fn();
+        if (enc == nullptr) return fail(RF_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable (driver too old?)");
+        const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(N / 64)};
+        const cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(M) * 128};
+        const cuuint32_t box[3] = {64, 32, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        const CUresult res = enc(&tmy, dtype == RF_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, y,
+                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (res != CUDA_SUCCESS) return fail(RF_ERR_CUDA, "cuTensorMapEncodeTiled failed, CUresult " + std::to_string(res));
+        p.head_major = 1;
+    } else if ((rc = make_map(&tmy, y, kind == RF_GEMM_EPI_RESIDUAL ? RF_DTYPE_F32 : dtype, M, out_cols, ldy, 32)) != RF_OK) {
+        return rc;
+    }
     // one CTA pair per two SMs, persistent over the (row-tile pair, column tile) space
     const int grid = kCluster * static_cast<int>(std::min<int64_t>(static_cast<int64_t>(p.m_pairs) * p.n_tiles, slots));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -447,6 +495,12 @@ int rf_gemm_nt(const void* a, const void* w, void* y, int64_t M, int64_t N, int6
             break;
         case RF_GEMM_EPI_GEGLU:
             e = bf ? launch<true, RF_GEMM_EPI_GEGLU, 256>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_GEGLU, 256>(tma, tmw, tmy, p, grid, st);
+            break;
+        case RF_GEMM_EPI_RESIDUAL:
+            if (bn == 192)
+                e = bf ? launch<true, RF_GEMM_EPI_RESIDUAL, 192>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_RESIDUAL, 192>(tma, tmw, tmy, p, grid, st);
+            else
+                e = bf ? launch<true, RF_GEMM_EPI_RESIDUAL, 256>(tma, tmw, tmy, p, grid, st) : launch<false, RF_GEMM_EPI_RESIDUAL, 256>(tma, tmw, tmy, p, grid, st);
             break;
         default:
             if (bn == 192)

@@ -93,3 +93,40 @@ def test_gemm_is_bitwise_deterministic():
     first = gemm_nt(a, w)
     for _ in range(20):
         assert torch.equal(first, gemm_nt(a, w))
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("M,N,K", [(1000, 768, 768), (8192, 768, 1152), (130, 256, 64)])
+def test_gemm_residual_epilogue(dtype, M, N, K):
+    """x (f32) += a @ w^T by TMA reduce-add of the f32 accumulators: nothing is rounded to 16 bit on the way."""
+    from paper_2603_12646_b200.gemm import gemm_nt
+    a, w = _rand((M, K), dtype, 13), _rand((N, K), dtype, 14, 0.05)
+    x0 = torch.randn(M, N, device="cuda")
+    x = x0.clone()
+    gemm_nt(a, w, out=x, epilogue="residual")
+    torch.cuda.synchronize()
+    want = x0.double() + a.double() @ w.double().t()
+    assert (x.double() - want).abs().max().item() <= 1e-4 * max(1.0, want.abs().max().item())
+    # a second call accumulates again
+    gemm_nt(a, w, out=x, epilogue="residual")
+    torch.cuda.synchronize()
+    want2 = want + a.double() @ w.double().t()
+    assert (x.double() - want2).abs().max().item() <= 2e-4 * max(1.0, want2.abs().max().item())
+
+
+def test_gemm_rope_head_major_layout_and_bf16_output():
+    """The QKV projection can write [3*H, tokens, 64] (every head's rows contiguous) and in the other 16-bit type."""
+    from paper_2603_12646_b200.classifier import rope_tables
+    from paper_2603_12646_b200.gemm import gemm_nt
+    B, S, H, d, hid = 2, 200, 12, 64, 768
+    a, w = _rand((B * S, hid), torch.float16, 15), _rand((3 * hid, hid), torch.float16, 16, 0.05)
+    cos, sin = rope_tables(S, d, 160000.0, "cuda")
+    packed = gemm_nt(a, w, epilogue="rope", rope_cos=cos, rope_sin=sin, seq_len=S)
+    heads = gemm_nt(a, w, epilogue="rope", rope_cos=cos, rope_sin=sin, seq_len=S, head_major=True)
+    torch.cuda.synchronize()
+    assert heads.shape == (3 * H, B * S, d)
+    assert torch.equal(heads, packed.view(B * S, 3 * H, d).permute(1, 0, 2))
+    heads_bf = gemm_nt(a, w, epilogue="rope", rope_cos=cos, rope_sin=sin, seq_len=S, head_major=True, out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    assert heads_bf.dtype == torch.bfloat16
+    assert (heads_bf.float() - heads.float()).abs().max().item() <= 2.0 ** -7 * heads.float().abs().max().item()
