@@ -375,6 +375,33 @@ def run_ours(args):
             extra["S16384_B4_local_63_64"] = {"ms": ms4, "gbs": bytes4 / ms4 / 1e6, "frac_of_hbm": bytes4 / ms4 / 1e6 / peaks["hbm"],
                                               "bound": "hbm"}
             del sets4, outs4
+            # the projections either side of the op (rf_gemm_nt, include/rf_gemm.h) at the 8K-token shapes of the encoder
+            try:
+                from paper_2603_12646_b200.classifier import rope_tables
+                from paper_2603_12646_b200.gemm import gemm_nt
+                cos_t, sin_t = rope_tables(S, 64, 10000.0, "cuda")
+                for name, n_, k_, epi in (("qkv_rope", 2304, 768, "rope"), ("out_proj_residual", 768, 768, "residual"),
+                                          ("mlp_up_geglu", 2304, 768, "geglu"), ("mlp_down_residual", 768, 1152, "residual")):
+                    ga = torch.randn(S, k_, device="cuda").to(torch.bfloat16)
+                    gw = (torch.randn(n_, k_, device="cuda") * 0.05).to(torch.bfloat16)
+                    gy = torch.zeros(S, n_ // 2 if epi == "geglu" else n_, device="cuda",
+                                     dtype=torch.float32 if epi == "residual" else torch.bfloat16)
+                    kw = dict(rope_cos=cos_t, rope_sin=sin_t, seq_len=S) if epi == "rope" else {}
+                    for _ in range(3):
+                        gemm_nt(ga, gw, out=gy, epilogue=epi, **kw)
+                    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    g0.record()
+                    for _ in range(20):
+                        gemm_nt(ga, gw, out=gy, epilogue=epi, **kw)
+                    g1.record()
+                    torch.cuda.synchronize()
+                    gms = g0.elapsed_time(g1) / 20
+                    extra[f"gemm_{name}_M8192_N{n_}_K{k_}"] = {"ms": gms, "tflops": 2.0 * S * n_ * k_ / gms / 1e9,
+                                                             "frac_of_peak": 2.0 * S * n_ * k_ / gms / 1e9 / peaks["bf16"],
+                                                             "kernel": "gemm_nt_sm100_kernel (tcgen05, CTA-pair multicast, fused epilogue)"}
+                    del ga, gw, gy
+            except Exception as e:  # noqa: BLE001
+                extra["gemm_error"] = repr(e)[:200]
             # classifier forward (configs[1]): ModernBERT-base shape, B=1, S=8192, random-init weights
             try:
                 from paper_2603_12646_b200.classifier import Classifier, ClassifierConfig, init_weights
@@ -398,11 +425,11 @@ def run_ours(args):
                     "attention_ms_total": sum(x["attention_ms"] for x in lm),
                     "global_attention_ms_avg": sum(x["attention_ms"] for x in lm if x["global"]) / max(1, sum(1 for x in lm if x["global"])),
                     "local_attention_ms_avg": sum(x["attention_ms"] for x in lm if not x["global"]) / max(1, sum(1 for x in lm if not x["global"])),
-                    "weights_MB": clf.weight_bytes() / 1e6, "cuda_graph": True,
+                    "weights_MB": clf.weight_bytes() / 1e6, "cuda_graph": True, "projections": ccfg.gemm + " (rf_gemm_nt, no library GEMM on the path)",
                     "paper_mi300x_ms": 105.0, "note": "random-init weights, synthetic token ids; paper number is other hardware (PAPER.md:402)"}
                 del clf, run
                 # the same forward through the native session (rf_clf.h): host token ids in, host logits out,
-                # cuBLAS GEMMs + this library's kernels, no Python between the launches
+                # this library's kernels only (projections included), no Python between the launches
                 from paper_2603_12646_b200.classifier import NativeClassifier
                 nat = NativeClassifier(ccfg, init_weights(ccfg, 7), device=local_rank)
                 ids_h = ids.cpu()

@@ -566,6 +566,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const WaitCtx wctx{bars_r + kWaitBlockOff};  // (shadows the outer one: derived from the pinned register)
 
         uint32_t oi = 0;    // items this warpgroup worked on so far (O-full barrier phase)
+        uint32_t oa = 0;    // items tile A worked on so far (== oi for tile A's warps): phase of the O_A-full barrier
         uint32_t vc = 0;    // V tiles consumed by the tensor pipe in earlier items (V ring position)
         uint32_t g = x;     // sequence index 2*t + x of this warpgroup's next tile
         uint32_t par_bits = 0;  // bit s = phase parity of the next use of S buffer s (both tiles' uses counted)
@@ -801,7 +802,13 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     if (sb >= kSBufs) sb -= kSBufs;
                 }
             } else if (num_live > 0) {
-                // tile B sits this item out: account for tile A's uses of the shared S buffers
+                // Tile B sits this item out (the last pair of a sequence whose length is 1..128 mod 256).  Its warps
+                // must not run ahead into the next item: the S-full barriers carry one phase bit, and a wait issued an
+                // odd number of tile-A uses early is satisfied by the phase that is still in flight (a persistent
+                // schedule then hung at S = 8193: found by the concurrency driver, tools/cpp/concurrency_table.cpp).
+                // O_A-full of this item completes after tile A's last use of every S buffer.
+                mbar_wait(bars_r + 8u * (kBarOFull + 0), oa & 1u, wctx);
+                // account for tile A's uses of the shared S buffers
                 for (int i = 0; i < num_live; ++i) {
                     par_bits ^= 1u << ((g - 1u + 2u * i) % kSBufs);
                     if (kPingPong) {  // keep the turn protocol going: pass every turn straight back
@@ -922,6 +929,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 }
             }
             if (active && num_live > 0) ++oi;
+            if (num_live > 0) ++oa;
         }
     }
 

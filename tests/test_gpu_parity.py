@@ -800,3 +800,35 @@ def test_classifier_bf16_activations_still_supported(torch_mod, P, oracle):
         assert np.abs(got - want).max() <= 2e-2
         assert (got.argmax(1) == want.argmax(1)).all()
     assert np.abs(hosted - native).max() <= 5e-3
+
+
+@pytest.mark.parametrize("S", [4097, 8193])
+def test_persistent_schedule_with_a_half_pair_at_the_end(torch_mod, P, S):
+    """S = 1 (mod 256): the last query-tile pair of every head has tile A only.  Under the persistent schedule tile B's
+    warps used to run ahead into the next item and alias the one-bit phase of the shared S-full barriers (hang at
+    S = 8193, found by tools/cpp/concurrency_table.cpp whose tokenizer prepends [CLS]).  Checked against the generic
+    kernel on the ragged tail and a full interior block; runs in a child process under a timeout so that a
+    regression fails instead of hanging the suite."""
+    import os
+    import subprocess
+    import sys
+    code = f"""
+import sys, torch
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+import paper_2603_12646_b200 as P
+g = torch.Generator(device="cuda").manual_seed(3)
+S = {S}
+q, k, v = [(torch.rand(1, 12, S, 64, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+st = P.FlashStats()
+o = P.flash_attention(q, k, v, P.AttentionSpec(), stats=st, out_dtype=torch.float32)
+torch.cuda.synchronize()
+assert st.grid_ctas < 12 * ((S + 255) // 256), st.grid_ctas      # persistent
+# the generic kernel takes whole problems only: compare two heads in full
+r2 = P.flash_attention(q[:, 5:7].contiguous(), k[:, 5:7].contiguous(), v[:, 5:7].contiguous(), P.AttentionSpec(), kernel="simt", out_dtype=torch.float32)
+err = (o[:, 5:7] - r2).abs().max().item()
+assert err <= 5e-3, err
+assert torch.equal(o, P.flash_attention(q, k, v, P.AttentionSpec(), out_dtype=torch.float32))
+print("ok", err)
+"""
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0 and "ok" in res.stdout, (res.stdout[-500:], res.stderr[-1500:])
