@@ -99,7 +99,8 @@ void rf_clf_destroy(rf_clf* clf);
  * mirror of the session so that no library GEMM is left on its path): pooled = hf[b * S, :] (CLS token of sequence
  * b); t = gelu(pooled Wd^T) rounded to the 16-bit type; t = LayerNorm(t) * head_norm; logits[b, :] = t Wc^T + cls_b.
  * hf [B*S, hidden], head_dense [hidden, hidden], cls_w [n_labels, hidden] in `dtype` (RF_DTYPE_F16 | RF_DTYPE_BF16);
- * head_norm [hidden], cls_b [n_labels], logits [B, n_labels] f32.  hidden <= 1024.  Asynchronous on `stream`. */
+ * head_norm [hidden], cls_b [n_labels], logits [B, n_labels] f32.  hidden <= 1024, a multiple of 8; head_dense rows
+ * 16-byte aligned.  Asynchronous on `stream`. */
 int rf_clf_head(const void* hf, int64_t B, int64_t S, int32_t hidden, const void* head_dense, const float* head_norm,
                 const void* cls_w, const float* cls_b, int32_t n_labels, float eps, int32_t dtype, float* logits,
                 void* stream);

@@ -140,56 +140,71 @@ __global__ void __launch_bounds__(256) half_to_f32_kernel(const uint16_t* __rest
 }
 
 // Classification head for one sequence per CTA: pooled = hf[b, 0, :] (CLS); t = gelu(round16(pooled Wd^T));
-// t = LN(t) * head_norm; logits = t Wc^T + b.  hidden <= 1024.
+// t = LN(t) * head_norm; logits = t Wc^T + b.  hidden <= 1024, hidden % 8 == 0.
+// 32 warps; the dense layer (hidden x hidden weights, 1.2 MB at 768: all of it read by this one SM) takes four
+// output features per warp at a time with 16-byte loads and independent accumulators -- the first version (8 warps,
+// one feature per warp, 4-byte loads) was a chain of dependent L2 round trips: 216 us of the 4.4 ms forward.
+constexpr int kHeadThreads = 1024;
 template <bool kBf16>
-__global__ void __launch_bounds__(256) clf_head_kernel(const uint16_t* __restrict__ hf, long long S, int hidden,
-                                                       const uint16_t* __restrict__ wd, const float* __restrict__ head_norm,
-                                                       const uint16_t* __restrict__ wc, const float* __restrict__ bc,
-                                                       int n_labels, float eps, float* __restrict__ logits) {
-    __shared__ float pooled[1024];
+__global__ void __launch_bounds__(kHeadThreads) clf_head_kernel(const uint16_t* __restrict__ hf, long long S, int hidden,
+                                                                const uint16_t* __restrict__ wd, const float* __restrict__ head_norm,
+                                                                const uint16_t* __restrict__ wc, const float* __restrict__ bc,
+                                                                int n_labels, float eps, float* __restrict__ logits) {
+    __shared__ __align__(16) float pooled[1024];
     __shared__ float t[1024];
-    __shared__ float red[2][8];
+    __shared__ float red[2][32];
     const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kWarps = kHeadThreads / 32;
     const uint16_t* row = hf + static_cast<long long>(b) * S * hidden;
-    for (int c = tid; c < hidden; c += blockDim.x) pooled[c] = elem_to_float<kBf16>(row[c]);
+    for (int c = tid; c < hidden; c += kHeadThreads) pooled[c] = elem_to_float<kBf16>(row[c]);
     __syncthreads();
-    // dense: one warp per output feature, lanes stride over the input features
-    for (int j = warp; j < hidden; j += 8) {
-        const uint16_t* wr = wd + static_cast<long long>(j) * hidden;
-        float acc = 0.f;
-        for (int c = lane * 2; c < hidden; c += 64) {
-            const float2 w2 = pair_to_float2<kBf16>(*reinterpret_cast<const uint32_t*>(wr + c));
-            acc += pooled[c] * w2.x + pooled[c + 1] * w2.y;
+    // dense: four output features per warp per step, lanes stride over the input features in 8-element groups
+    for (int j0 = warp * 4; j0 < hidden; j0 += kWarps * 4) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int c = lane * 8; c < hidden; c += 256) {
+            const float4 p0 = *reinterpret_cast<const float4*>(pooled + c), p1 = *reinterpret_cast<const float4*>(pooled + c + 4);
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+                if (j0 + f < hidden) {
+                    const uint4 w8 = __ldg(reinterpret_cast<const uint4*>(wd + static_cast<long long>(j0 + f) * hidden + c));
+                    const float2 w0 = pair_to_float2<kBf16>(w8.x), w1 = pair_to_float2<kBf16>(w8.y);
+                    const float2 w2 = pair_to_float2<kBf16>(w8.z), w3 = pair_to_float2<kBf16>(w8.w);
+                    acc[f] += p0.x * w0.x + p0.y * w0.y + p0.z * w1.x + p0.w * w1.y + p1.x * w2.x + p1.y * w2.y + p1.z * w3.x + p1.w * w3.y;
+                }
+            }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-            const float v = round_to_16<kBf16>(acc);  // the GEMM output is 16-bit
-            t[j] = 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+        for (int f = 0; f < 4; ++f) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[f] += __shfl_xor_sync(0xffffffffu, acc[f], o);
+            if (lane == 0 && j0 + f < hidden) {
+                const float v = round_to_16<kBf16>(acc[f]);  // the GEMM output is 16-bit
+                t[j0 + f] = 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+            }
         }
     }
     __syncthreads();
     float s = 0.f;
-    for (int c = tid; c < hidden; c += blockDim.x) s += t[c];
+    for (int c = tid; c < hidden; c += kHeadThreads) s += t[c];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) red[0][warp] = s;
     __syncthreads();
     float mean = 0.f;
-    for (int w = 0; w < 8; ++w) mean += red[0][w];
+    for (int w = 0; w < kWarps; ++w) mean += red[0][w];
     mean /= hidden;
     float v = 0.f;
-    for (int c = tid; c < hidden; c += blockDim.x) v += (t[c] - mean) * (t[c] - mean);
+    for (int c = tid; c < hidden; c += kHeadThreads) v += (t[c] - mean) * (t[c] - mean);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) red[1][warp] = v;
     __syncthreads();
     float var = 0.f;
-    for (int w = 0; w < 8; ++w) var += red[1][w];
+    for (int w = 0; w < kWarps; ++w) var += red[1][w];
     const float rstd = rsqrtf(var / hidden + eps);
-    for (int c = tid; c < hidden; c += blockDim.x) pooled[c] = (t[c] - mean) * rstd * head_norm[c];
+    for (int c = tid; c < hidden; c += kHeadThreads) pooled[c] = (t[c] - mean) * rstd * head_norm[c];
     __syncthreads();
-    for (int k = warp; k < n_labels; k += 8) {
+    for (int k = warp; k < n_labels; k += kWarps) {
         const uint16_t* wr = wc + static_cast<long long>(k) * hidden;
         float acc = 0.f;
         for (int c = lane; c < hidden; c += 32) acc += pooled[c] * elem_to_float<kBf16>(wr[c]);
@@ -654,10 +669,10 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
         cur ^= 1;
     }
     if (bf)
-        clf_head_kernel<true><<<static_cast<unsigned>(B), 256, 0, st>>>(slot[cur], S, hid, s->head_dense, s->head_norm, s->cls_w,
+        clf_head_kernel<true><<<static_cast<unsigned>(B), kHeadThreads, 0, st>>>(slot[cur], S, hid, s->head_dense, s->head_norm, s->cls_w,
                                                                         s->cls_b, c.n_labels, c.eps, dlogits);
     else
-        clf_head_kernel<false><<<static_cast<unsigned>(B), 256, 0, st>>>(slot[cur], S, hid, s->head_dense, s->head_norm, s->cls_w,
+        clf_head_kernel<false><<<static_cast<unsigned>(B), kHeadThreads, 0, st>>>(slot[cur], S, hid, s->head_dense, s->head_norm, s->cls_w,
                                                                          s->cls_b, c.n_labels, c.eps, dlogits);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "classifier kernels");
     if ((e = cudaMemcpyAsync(pin + pin_logits, dlogits, static_cast<size_t>(B) * c.n_labels * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
@@ -704,7 +719,7 @@ int rf_clf_head(const void* hf, int64_t B, int64_t S, int32_t hidden, const void
                 void* stream) {
     if (hf == nullptr || head_dense == nullptr || head_norm == nullptr || cls_w == nullptr || cls_b == nullptr || logits == nullptr)
         return fail(RF_ERR_ARG, "rf_clf_head: null pointer");
-    if (B < 0 || S < 1 || hidden < 2 || hidden > 1024 || hidden % 2 || n_labels < 1) return fail(RF_ERR_SHAPE, "rf_clf_head: bad shape");
+    if (B < 0 || S < 1 || hidden < 8 || hidden > 1024 || hidden % 8 || n_labels < 1) return fail(RF_ERR_SHAPE, "rf_clf_head: bad shape (hidden must be a multiple of 8, at most 1024)");
     if (dtype != RF_DTYPE_F16 && dtype != RF_DTYPE_BF16) return fail(RF_ERR_ARG, "rf_clf_head: dtype must be bf16 or f16");
     if (B == 0) return RF_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -712,9 +727,9 @@ int rf_clf_head(const void* hf, int64_t B, int64_t S, int32_t hidden, const void
     const uint16_t* wd = static_cast<const uint16_t*>(head_dense);
     const uint16_t* wc = static_cast<const uint16_t*>(cls_w);
     if (dtype == RF_DTYPE_BF16)
-        clf_head_kernel<true><<<static_cast<unsigned>(B), 256, 0, st>>>(h16, S, hidden, wd, head_norm, wc, cls_b, n_labels, eps, logits);
+        clf_head_kernel<true><<<static_cast<unsigned>(B), kHeadThreads, 0, st>>>(h16, S, hidden, wd, head_norm, wc, cls_b, n_labels, eps, logits);
     else
-        clf_head_kernel<false><<<static_cast<unsigned>(B), 256, 0, st>>>(h16, S, hidden, wd, head_norm, wc, cls_b, n_labels, eps, logits);
+        clf_head_kernel<false><<<static_cast<unsigned>(B), kHeadThreads, 0, st>>>(h16, S, hidden, wd, head_norm, wc, cls_b, n_labels, eps, logits);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? RF_OK : cuda_fail(e, "rf_clf_head launch");
 }

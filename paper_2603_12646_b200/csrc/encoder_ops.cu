@@ -83,6 +83,12 @@ template <int kVecPerLane, bool kBf16>
 __global__ void __launch_bounds__(128) add_layernorm_kernel(float* __restrict__ x, const uint16_t* __restrict__ delta,
                                                             const float* __restrict__ w, uint16_t* __restrict__ y,
                                                             long long rows, int n, float eps) {
+    // programmatic dependent launch (no-ops under a plain launch): this grid was allowed to start while the previous
+    // kernel of the stream -- the projection whose epilogue adds into x -- was still draining; its results are visible
+    // after the wait.  The next kernel (a projection: barrier init, TMEM allocation, tensor-map prefetch) may start its
+    // prologue right away.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     const long long row = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
     if (row >= rows) return;
     const int lane = threadIdx.x & 31;
@@ -197,14 +203,24 @@ int rf_add_layernorm(float* x, const void* delta, const float* w, void* y, int64
     const uint16_t* dl = static_cast<const uint16_t*>(delta);
     uint16_t* yy = static_cast<uint16_t*>(y);
     const int ni = static_cast<int>(n);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
     if (n <= 1024) {
-        if (dtype == RF_DTYPE_BF16) add_layernorm_kernel<8, true><<<grid, 128, 0, st>>>(x, dl, w, yy, rows, ni, eps);
-        else add_layernorm_kernel<8, false><<<grid, 128, 0, st>>>(x, dl, w, yy, rows, ni, eps);
+        if (dtype == RF_DTYPE_BF16) e = cudaLaunchKernelEx(&cfg, add_layernorm_kernel<8, true>, x, dl, w, yy, static_cast<long long>(rows), ni, eps);
+        else e = cudaLaunchKernelEx(&cfg, add_layernorm_kernel<8, false>, x, dl, w, yy, static_cast<long long>(rows), ni, eps);
     } else {
-        if (dtype == RF_DTYPE_BF16) add_layernorm_kernel<32, true><<<grid, 128, 0, st>>>(x, dl, w, yy, rows, ni, eps);
-        else add_layernorm_kernel<32, false><<<grid, 128, 0, st>>>(x, dl, w, yy, rows, ni, eps);
+        if (dtype == RF_DTYPE_BF16) e = cudaLaunchKernelEx(&cfg, add_layernorm_kernel<32, true>, x, dl, w, yy, static_cast<long long>(rows), ni, eps);
+        else e = cudaLaunchKernelEx(&cfg, add_layernorm_kernel<32, false>, x, dl, w, yy, static_cast<long long>(rows), ni, eps);
     }
-    return fail_cuda(cudaGetLastError());
+    return fail_cuda(e);
 }
 
 int rf_geglu(const void* wi_out, void* act, int64_t rows, int64_t I, int32_t dtype, void* stream) {
