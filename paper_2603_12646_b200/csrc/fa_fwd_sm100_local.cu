@@ -239,20 +239,23 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         // =============================== TMA producer ===============================
         // warp-uniform control flow; only lane 0 issues
         uint32_t bc = 0;  // K/V boxes requested so far: K slot bc % kRingK, V slot bc % kRingV
-        auto load_box = [&](const Tile& t, int key0) {
-            const uint32_t ks = bc % kRingK, vs = bc % kRingV;
-            mbar_wait(bar(kBarKEmpty + ks), ((bc / kRingK) & 1) ^ 1, wctx);
+        auto load_k = [&](const Tile& t, uint32_t box, int key0) {
+            const uint32_t ks = box % kRingK;
+            mbar_wait(bar(kBarKEmpty + ks), ((box / kRingK) & 1) ^ 1, wctx);
             if (lane == 0) {
                 mbar_arrive_expect_tx(bar(kBarKFull + ks), kTileBytes);
                 tma_load_4d(smem_base + Smem::k + ks * kTileBytes, &tm_k, bar(kBarKFull + ks), 0, key0, t.h, t.b);
             }
-            mbar_wait(bar(kBarVEmpty + vs), ((bc / kRingV) & 1) ^ 1, wctx);
+            __syncwarp();
+        };
+        auto load_v = [&](const Tile& t, uint32_t box, int key0) {
+            const uint32_t vs = box % kRingV;
+            mbar_wait(bar(kBarVEmpty + vs), ((box / kRingV) & 1) ^ 1, wctx);
             if (lane == 0) {
                 mbar_arrive_expect_tx(bar(kBarVFull + vs), kTileBytes);
                 tma_load_4d(smem_base + Smem::v + vs * kTileBytes, &tm_v, bar(kBarVFull + vs), 0, key0, t.h, t.b);
             }
             __syncwarp();
-            ++bc;
         };
         for (int n = 0; n < my_tiles; ++n) {
             const Tile t = decode_tile(p, g0 + n, q_tiles);
@@ -262,8 +265,19 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
                 tma_load_4d(smem_base + Smem::q, &tm_q, bar(kBarQFull), 0, t.r0, t.h, t.b);
             }
             __syncwarp();
-            if (n == 0 || t.head_start) load_box(t, t.kb);
-            load_box(t, t.kb + kBlockN);
+            if (n == 0 || t.head_start) {
+                // a fresh strip: both K boxes before the V boxes, so that Q K^T can start on 3/5 of the tile's bytes
+                // (every CTA of the grid starts with such a tile: the first 80 KiB per CTA are pure HBM time)
+                load_k(t, bc, t.kb);
+                load_k(t, bc + 1, t.kb + kBlockN);
+                load_v(t, bc, t.kb);
+                load_v(t, bc + 1, t.kb + kBlockN);
+                bc += 2;
+            } else {
+                load_k(t, bc, t.kb + kBlockN);
+                load_v(t, bc, t.kb + kBlockN);
+                bc += 1;
+            }
         }
     } else if (warp == kMmaWarp) {
         // =============================== UMMA issuer ===============================
