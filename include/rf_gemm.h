@@ -49,6 +49,12 @@ typedef struct rf_gemm_epilogue {
 int rf_gemm_nt(const void* a, const void* w, void* y, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldw,
                int64_t ldy, int32_t dtype, const rf_gemm_epilogue* epi, void* stream);
 
+/* Every wait inside the kernel is bounded: a protocol failure cannot hang the GPU or kill the context, it leaves a
+ * status word behind and lets the grid run to its end with invalid output.  Synchronises `stream`, returns RF_OK or
+ * RF_ERR_DEVICE_TIMEOUT (and clears the word): call it where the results of earlier rf_gemm_nt launches on this
+ * device are consumed (rf_clf_forward does, once per forward). */
+int rf_gemm_launch_status(void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,7 +32,7 @@ EXPORTS = [
     "rf_clf_config_default", "rf_clf_weight_elems", "rf_clf_create", "rf_clf_forward", "rf_clf_session_bytes",
     "rf_clf_last_forward_ms", "rf_clf_destroy", "rf_clf_head",
     # include/rf_gemm.h
-    "rf_gemm_nt",
+    "rf_gemm_nt", "rf_gemm_launch_status",
 ]
 
 RF_GEMM_EPI_NONE, RF_GEMM_EPI_ROPE, RF_GEMM_EPI_GEGLU, RF_GEMM_EPI_RESIDUAL = 0, 1, 2, 3
@@ -166,6 +166,8 @@ def load(build_if_missing: bool = True):
     lib.rf_clf_head.restype = C.c_int
     lib.rf_gemm_nt.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, i32, C.POINTER(RfGemmEpilogue), vp]
     lib.rf_gemm_nt.restype = C.c_int
+    lib.rf_gemm_launch_status.argtypes = [vp]
+    lib.rf_gemm_launch_status.restype = C.c_int
     for name in ("rf_fa_validate", "rf_fa_fwd_workspace_bytes", "rf_fa_stats_query", "rf_fa_fwd", "rf_fa_merge",
                  "rf_fa_rescale_partial", "rf_fa_normalize", "rf_pad_bias_from_mask", "rf_cast_f32_to",
                  "rf_cast_to_f32", "rf_fa_fwd_host", "rf_fused_flash_attention_op", "rf_device_check",

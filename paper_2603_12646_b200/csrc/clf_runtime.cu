@@ -554,6 +554,10 @@ int rf_clf_forward(rf_clf* s, const int64_t* input_ids, const float* attention_m
             const int rc_st = rf_fa_launch_status(base + L.ws, st);
             if (rc_st != RF_OK) return rc_st;
         }
+        if (c.gemm_backend == RF_CLF_GEMM_OWN) {  // ... or inside a projection
+            const int rc_g = rf_gemm_launch_status(st);
+            if (rc_g != RF_OK) return rc_g;
+        }
         cudaEventElapsedTime(&s->last_ms, s->ev0, s->ev1);
         std::memcpy(logits, pin + pin_logits, static_cast<size_t>(B) * c.n_labels * 4);
         return RF_OK;

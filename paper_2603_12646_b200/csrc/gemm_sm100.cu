@@ -347,6 +347,20 @@ gemm_nt_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_cons
     }
 }
 
+// Launch status of the projections (ptx.cuh: written only when a bounded wait inside a CTA runs out, which then lets
+// the kernel run through to its teardown with invalid output).  One word per device context; rf_gemm_launch_status
+// reads and clears it.
+__device__ int g_gemm_status;
+
+int* gemm_status_ptr() {
+    void* ptr = nullptr;
+    if (cudaGetSymbolAddress(&ptr, g_gemm_status) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return static_cast<int*>(ptr);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                                   const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -444,7 +458,7 @@ int rf_gemm_nt(const void* a, const void* w, void* y, int64_t M, int64_t N, int6
     p.K = static_cast<int>(K);
     p.m_pairs = static_cast<int>(m_pairs);
     p.n_tiles = static_cast<int>(N / bn);
-    p.status = nullptr;
+    p.status = gemm_status_ptr();
     if (kind == RF_GEMM_EPI_ROPE) {
         if (epi->cos_table == nullptr || epi->sin_table == nullptr || epi->S <= 0 || epi->head_dim != 64)
             return fail(RF_ERR_ARG, "rf_gemm_nt: the RoPE epilogue needs cos/sin tables [S, 32], S > 0 and head_dim 64");
@@ -510,6 +524,21 @@ int rf_gemm_nt(const void* a, const void* w, void* y, int64_t M, int64_t N, int6
     }
     if (e != cudaSuccess) return fail(RF_ERR_CUDA, std::string("rf_gemm_nt launch: ") + cudaGetErrorString(e));
     return RF_OK;
+}
+
+int rf_gemm_launch_status(void* stream_v) {
+    using namespace rf;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+    int* ptr = gemm_status_ptr();
+    if (ptr == nullptr) return set_last_error(RF_ERR_CUDA, "rf_gemm_launch_status: no CUDA device");
+    uint32_t word = 0;
+    cudaError_t e = cudaMemcpyAsync(&word, ptr, sizeof(word), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return set_last_error(RF_ERR_CUDA, std::string("rf_gemm_launch_status: ") + cudaGetErrorString(e));
+    if ((word & 0xffff0000u) != kLaunchStatusMagic) return RF_OK;
+    cudaMemsetAsync(ptr, 0, sizeof(word), stream);  // reported once
+    return set_last_error(RF_ERR_DEVICE_TIMEOUT, "a barrier wait inside a projection CTA timed out (CTA " + std::to_string(word & 0xfffu) +
+                                                     "); the output of that launch is invalid");
 }
 
 }  // extern "C"

@@ -130,3 +130,12 @@ def test_gemm_rope_head_major_layout_and_bf16_output():
     torch.cuda.synchronize()
     assert heads_bf.dtype == torch.bfloat16
     assert (heads_bf.float() - heads.float()).abs().max().item() <= 2.0 ** -7 * heads.float().abs().max().item()
+
+
+def test_gemm_launch_status_reports_ok():
+    """Bounded waits: the status word of the projections is clean after normal launches (include/rf_gemm.h)."""
+    from paper_2603_12646_b200 import capi
+    from paper_2603_12646_b200.gemm import gemm_nt
+    a, w = _rand((512, 768), torch.bfloat16, 17), _rand((768, 768), torch.bfloat16, 18, 0.05)
+    gemm_nt(a, w)
+    assert capi.load().rf_gemm_launch_status(torch.cuda.current_stream().cuda_stream) == capi.RF_OK
