@@ -832,3 +832,40 @@ print("ok", err)
 """
     res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
     assert res.returncode == 0 and "ok" in res.stdout, (res.stdout[-500:], res.stderr[-1500:])
+
+
+@pytest.mark.parametrize("B,S,wl,wr,pad", [(2, 4097, -1, -1, 1), (5, 1281, 300, 10, 1), (3, 2305, -1, -1, 0), (8, 4097, 63, 64, 1)])
+def test_ragged_batches_through_the_persistent_schedules(B, S, wl, wr, pad):
+    """Ragged lengths x batches x masks x windows (a subset of tools/stress_ragged.py): sequence lengths 1 (mod 256 / 128) so
+    that the last query-tile pair of every sequence is half empty, more pairs than SMs so that the persistent schedules
+    (balanced slices, round-robin) and the two-CTA narrow-window kernel run, padded tails per sequence.  Two heads are
+    checked against the generic kernel, the whole output for bitwise repeatability.  Child process under a timeout: a hang
+    fails the test instead of the suite."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys, torch
+sys.path.insert(0, {root!r})
+import paper_2603_12646_b200 as P
+B, S, wl, wr, pad = {B}, {S}, {wl}, {wr}, {pad}
+g = torch.Generator(device="cuda").manual_seed(S + B)
+q, k, v = [(torch.rand(B, 12, S, 64, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+pb = None
+if pad:
+    mask = torch.ones(B, 1, 1, S, device="cuda")
+    for b in range(B):
+        mask[b, ..., S - (b * 997 + 130) % S:] = 0
+    pb = P.pad_bias_from_mask(mask)
+spec = P.AttentionSpec(0.0, wl, wr, pb)
+o = P.flash_attention(q, k, v, spec, out_dtype=torch.float32)
+torch.cuda.synchronize()
+r = P.flash_attention(q[:, 3:5].contiguous(), k[:, 3:5].contiguous(), v[:, 3:5].contiguous(), spec, kernel="simt", out_dtype=torch.float32)
+err = (o[:, 3:5] - r).abs().max().item()
+assert err <= 5e-3, err
+assert torch.equal(o, P.flash_attention(q, k, v, spec, out_dtype=torch.float32))
+print("ok", err)
+"""
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=180)
+    assert res.returncode == 0 and "ok" in res.stdout, (res.stdout[-500:], res.stderr[-1500:])
