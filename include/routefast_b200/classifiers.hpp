@@ -13,7 +13,7 @@
 // in) and the encoder weights (the reference has no model; random-init from a seed unless a weight blob is
 // supplied).  With random weights the signals are arbitrary but deterministic -- the plumbing, the shapes,
 // the error behaviour and the cost are what this layer pins down.
-// There is no CPU fallback: a missing GPU / cuBLAS surfaces as std::runtime_error at construction.
+// There is no CPU fallback: a missing GPU surfaces as std::runtime_error at construction.
 #pragma once
 
 #include <algorithm>

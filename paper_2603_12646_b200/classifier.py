@@ -241,7 +241,7 @@ class Classifier:
         side = torch.cuda.Stream(self.device)
         side.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(side):
-            for _ in range(2):  # warm-up outside capture (cuBLAS workspaces, lazy kernel loads)
+            for _ in range(2):  # warm-up outside capture (lazy kernel loads, library workspaces)
                 self.forward(ids_buf, mask_buf)
         torch.cuda.current_stream(self.device).wait_stream(side)
         torch.cuda.synchronize(self.device)
@@ -280,7 +280,8 @@ def pack_weights(cfg: ClassifierConfig, weights: Dict[str, torch.Tensor]) -> tor
 
 class NativeClassifier:
     """rf_clf session: token ids (host) -> logits (host) in one C call.  Same weights, same data path and
-    the same kernels as `Classifier`; the GEMMs go to cuBLAS directly instead of through torch."""
+    the same kernels as `Classifier` (rf_gemm_nt projections by default; with gemm="cublas" the GEMMs go to cuBLAS directly
+    instead of through torch)."""
 
     def __init__(self, cfg: ClassifierConfig, weights: Dict[str, torch.Tensor], device: int = 0):
         import ctypes as C

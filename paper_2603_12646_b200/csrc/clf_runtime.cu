@@ -3,12 +3,13 @@
 //
 // Same data path as paper_2603_12646_b200/classifier.py (which stays as the torch-hosted mirror):
 //   x = LN(emb[ids])                                   embed_gather + rf_add_layernorm
-//   per layer: h = LN(x += mlp_prev); qkv = h Wqkv^T   library GEMM -> [B,S,3,H,d]
-//              rope(q, k) in place                     rf_rope_qkv
+//   per layer: h = LN(x); qkv = rope(h Wqkv^T)         rf_gemm_nt, RoPE in the epilogue -> head-major [3,H,B*S,d]
 //              attn = FusedFlashAttention(q, k, v)     rf_fa_fwd on strided views, [B,S,H*d] out
-//              x += attn Wo^T; h2 = LN(x)              library GEMM + rf_add_layernorm
-//              x += (gelu(h2 Wi_a) * h2 Wi_g) Wo2^T    library GEMMs + rf_geglu, in row chunks
+//              x += attn Wo^T; h2 = LN(x)              rf_gemm_nt (residual epilogue: TMA reduce-add into x) + rf_add_layernorm
+//              x += (gelu(h2 Wi_a) * h2 Wi_g) Wo2^T    rf_gemm_nt (GeGLU epilogue), rf_gemm_nt (residual epilogue), in row chunks
 //   logits = head(LN(x)[CLS])                          clf_head_kernel
+// (gemm_backend = RF_CLF_GEMM_CUBLAS keeps the round-1 path for A/B runs: library GEMMs into the packed [B,S,3,H,d]
+// layout + rf_rope_qkv / rf_geglu / the add half of rf_add_layernorm.)
 // The pad-bias chain is built once per forward and shared by every layer (reference rewrite.cpp:303-318);
 // layer i is global iff i % global_every == 0, else local_window -> (w/2-1, w/2) (rewrite.cpp:355-361).
 //
@@ -19,8 +20,9 @@
 // A shape seen twice in a row is captured into a CUDA graph and replayed afterwards; ids, mask and logits
 // travel through page-locked staging so that the captured copies have fixed addresses.
 //
-// cuBLAS is resolved with dlopen/dlsym (five entry points) so that librf_fa.so itself has no link-time
-// dependency on it; a missing library is RF_ERR_CUDA at session creation, never a fallback.
+// cuBLAS is only loaded when RF_CLF_GEMM_CUBLAS is selected: resolved with dlopen/dlsym (five entry points) so that
+// librf_fa.so itself has no link-time dependency on it; a missing library is then RF_ERR_CUDA at session creation,
+// never a fallback.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>

@@ -5,7 +5,8 @@
 //   rope_qkv      rotary embedding on the Q and K thirds of a packed QKV tensor, in place
 //   add_layernorm residual add into the f32 stream + LayerNorm (no bias) -> bf16 GEMM operand
 //   geglu         act = gelu(x[:, :I]) * x[:, I:]  on the Wi GEMM output
-// The GEMMs themselves are plain library GEMMs (cuBLAS through torch.matmul).
+// The projections themselves are rf_gemm_nt (gemm_sm100.cu), which fuses rope_qkv, geglu and the residual add into its
+// epilogues; the stand-alone kernels here serve the library-GEMM A/B path and the tests.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
