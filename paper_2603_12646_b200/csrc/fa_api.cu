@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -186,11 +187,15 @@ struct Plan {
     int grid;         // CTAs
     int64_t total_pairs, pairs_per_head, tiles_per_pair;
     size_t status_bytes;
+    // Split-pair flags of the persistent balanced schedule: ALWAYS the first block after the status block in a
+    // workspace that has anything after the status block at all, whatever the plan, so that plans of different
+    // shapes sharing one workspace never put data where another plan keeps flags.  The flags are zero between
+    // launches: a plan zeroes them with its first launch, the kernel leaves them as it found them.
+    size_t sched_flag_bytes;
     size_t bias_bytes, flag_bytes_bias, part_bytes;
-    size_t qnorm_bytes, kmax_bytes;  // row-max skip test inputs (dense kernel, S >= 1024)
-    size_t workspace_bytes() const {
-        return status_bytes + bias_bytes + flag_bytes_bias + part_bytes + qnorm_bytes + kmax_bytes;
-    }
+    size_t kmax_bytes;  // row-max skip test, key side: largest key norm per (head, key tile) (dense kernel, S >= 1024)
+    size_t tail_bytes() const { return bias_bytes + flag_bytes_bias + part_bytes + kmax_bytes; }
+    size_t workspace_bytes() const { return status_bytes + (tail_bytes() > 0 ? sched_flag_bytes + tail_bytes() : 0); }
 };
 
 Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
@@ -202,6 +207,8 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         return pl;
     }
     pl.status_bytes = kStatusBlockBytes;
+    const int sms = sm_count_or_default();
+    pl.sched_flag_bytes = align_up(rf::fa_fwd_sm100_flag_bytes(sms), 256);
     pl.pairs_per_head = (p->S + rf::kRowsPerCta - 1) / rf::kRowsPerCta;
     pl.total_pairs = pl.pairs_per_head * p->H * p->B;
     if (r.partial && r.kv_begin == r.kv_end) {  // empty key block: one fill kernel, no workspace
@@ -240,13 +247,12 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         }
         pl.tiles_per_pair = std::max<int64_t>(tiles, 1);
     }
-    // Row-max skip test (fa_fwd_sm100.cu): |q_i| per row and max |k_j| per key tile, O(S) floats.
-    // RF_FA_SKIP_MAX=0 turns it off (A/B measurements).
+    // Row-max skip test (fa_fwd_sm100.cu): max |k_j| per key tile from a pre-pass over K (4 B per (head, tile));
+    // |q_i| is taken inside the kernel.  RF_FA_SKIP_MAX=0 turns it off (A/B measurements).
     static const bool skip_max_enabled = [] {
         const char* env = std::getenv("RF_FA_SKIP_MAX");
         return env == nullptr || env[0] != '0';
     }();
-    const int sms = sm_count_or_default();
     if (p->d == 128) {
         // head_dim 128: whole pairs only -- one per CTA while they fit a wave (and for split-KV partials),
         // else dealt round-robin over a persistent grid
@@ -257,10 +263,8 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         }
         return pl;
     }
-    if (skip_max_enabled && p->S >= 1024) {
-        pl.qnorm_bytes = align_up(static_cast<size_t>(p->B) * p->H * p->S * sizeof(float), 256);
+    if (skip_max_enabled && p->S >= 1024)
         pl.kmax_bytes = align_up(static_cast<size_t>(p->B) * p->H * n_kv_tiles(p->S) * sizeof(float), 256);
-    }
     if (!r.partial && pl.total_pairs > sms) {
         pl.sched_mode = 1;
         pl.grid = sms;
@@ -351,17 +355,16 @@ struct Launch {
     // pre-pass
     float* bias2 = nullptr;
     uint8_t* tile_flags = nullptr;
-    bool norms = false;
-    const void* q = nullptr;
-    const void* k = nullptr;
-    long long qs[3] = {0, 0, 0}, ks[3] = {0, 0, 0};
-    int dtype = 0;
-    float* qnorm = nullptr;
-    float* kmax = nullptr;
-    int* zero_ptr = nullptr;
-    int zero_words = 0;
+    // split-pair flag block of the persistent balanced schedule: zeroed in-stream by the first launch (and by
+    // the first one after any launch reported a timeout), left zero by the kernel itself
     void* memset_ptr = nullptr;
     size_t memset_bytes = 0;
+    mutable std::atomic<int> zeroed_epoch{-1};
+    // key-norm pre-pass of the row-max skip test
+    float* kmax = nullptr;
+    const void* k = nullptr;
+    long long ks[3] = {0, 0, 0};
+    int dtype = 0;
     // neutral partial
     float* o_partial = nullptr;
     float* m_partial = nullptr;
@@ -428,6 +431,11 @@ int build_launch(const rf_fa_params* p, void* workspace, size_t workspace_bytes,
     if ((rc = make_tmap(&L->tmk, p->k, p->dtype, p->d, p->S, p->H, p->B, r.ks)) != RF_OK) return rc;
     if ((rc = make_tmap(&L->tmv, p->v, p->dtype, p->d, p->S, p->H, p->B, r.vs)) != RF_OK) return rc;
     if (pl.local) return RF_OK;
+    void* sched_flags = nullptr;
+    if (pl.tail_bytes() > 0) {
+        sched_flags = ws;
+        ws += pl.sched_flag_bytes;
+    }
     if (pl.bias_bytes > 0) {
         L->bias2 = reinterpret_cast<float*>(ws);
         L->tile_flags = ws + pl.bias_bytes;
@@ -439,35 +447,23 @@ int build_launch(const rf_fa_params* p, void* workspace, size_t workspace_bytes,
     f.pairs_per_head = static_cast<int>(pl.pairs_per_head);
     f.tiles_per_pair = static_cast<int>(pl.tiles_per_pair);
     if (pl.sched_mode == 1) {
-        // split-pair flag block: zeroed by the norms pre-pass when that runs, else by a memset node
-        void* flag_ptr = nullptr;
-        size_t flag_bytes = 0;
-        rf::fa_fwd_sm100_partial_carve(ws + pl.bias_bytes + pl.flag_bytes_bias, pl.grid, &f, &flag_ptr, &flag_bytes);
-        if (pl.qnorm_bytes > 0) {
-            L->zero_ptr = static_cast<int*>(flag_ptr);
-            L->zero_words = static_cast<int>(flag_bytes / sizeof(int));
-        } else {
-            L->memset_ptr = flag_ptr;
-            L->memset_bytes = flag_bytes;
-        }
+        rf::fa_fwd_sm100_partial_carve(ws + pl.bias_bytes + pl.flag_bytes_bias, sched_flags, pl.grid, &f);
+        L->memset_ptr = sched_flags;
+        L->memset_bytes = rf::fa_fwd_sm100_flag_bytes(pl.grid);
     }
-    if (pl.qnorm_bytes > 0) {
-        uint8_t* nb = ws + pl.bias_bytes + pl.flag_bytes_bias + pl.part_bytes;
-        L->norms = true;
-        L->q = p->q;
+    if (pl.kmax_bytes > 0) {
+        L->kmax = reinterpret_cast<float*>(ws + pl.bias_bytes + pl.flag_bytes_bias + pl.part_bytes);
         L->k = p->k;
-        for (int i = 0; i < 3; ++i) {
-            L->qs[i] = r.qs[i];
-            L->ks[i] = r.ks[i];
-        }
+        for (int i = 0; i < 3; ++i) L->ks[i] = r.ks[i];
         L->dtype = p->dtype;
-        L->qnorm = reinterpret_cast<float*>(nb);
-        L->kmax = reinterpret_cast<float*>(nb + pl.qnorm_bytes);
-        f.qnorm = L->qnorm;
         f.kmax = L->kmax;
     }
     return RF_OK;
 }
+
+// Bumped whenever a launch reported a timed-out wait (rf_fa_launch_status): the kernel that gave up may have left
+// split-pair flags set, so every plan zeroes its flag block again with its next launch.
+std::atomic<int> g_flag_epoch{0};
 
 int run_launch(const Launch& L, cudaStream_t stream) {
     if (L.empty) return RF_OK;
@@ -491,18 +487,20 @@ int run_launch(const Launch& L, cudaStream_t stream) {
         if (e != cudaSuccess) return cuda_fail(e, "bias_prepare launch");
     }
     if (L.memset_bytes > 0) {
-        e = cudaMemsetAsync(L.memset_ptr, 0, L.memset_bytes, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(partial flags)");
+        const int epoch = g_flag_epoch.load(std::memory_order_acquire);
+        if (L.zeroed_epoch.exchange(epoch, std::memory_order_acq_rel) != epoch) {
+            e = cudaMemsetAsync(L.memset_ptr, 0, L.memset_bytes, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(split-pair flags)");
+        }
     }
-    if (L.norms) {
-        e = rf::launch_qk_norms(L.q, L.k, L.qs, L.ks, L.dtype, f.B, f.H, f.S, f.d, f.n_kv_tiles, L.qnorm, L.kmax, L.zero_ptr,
-                                L.zero_words, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "qk_norms launch");
+    if (L.kmax != nullptr) {
+        e = rf::launch_k_tile_norms(L.k, L.ks, L.dtype, f.B, f.H, f.S, f.d, f.n_kv_tiles, L.kmax, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "k_tile_norms launch");
     }
     if (L.pl.d128)
         e = rf::launch_fa_fwd_sm100_d128(L.tmq, L.tmk, L.tmv, f, L.bf16, L.pl.grid, stream);
     else
-        e = rf::launch_fa_fwd_sm100(L.tmq, L.tmk, L.tmv, f, L.bf16, L.pl.grid, stream, /*pdl=*/L.norms);
+        e = rf::launch_fa_fwd_sm100(L.tmq, L.tmk, L.tmv, f, L.bf16, L.pl.grid, stream, /*pdl=*/true);
     return e == cudaSuccess ? RF_OK : cuda_fail(e, "fa_fwd_sm100 launch");
 }
 
@@ -611,6 +609,7 @@ int rf_fa_launch_status(void* workspace, void* stream_v) {
     if (e != cudaSuccess) return cuda_fail(e, "launch status read");
     if ((word & 0xffff0000u) != rf::kLaunchStatusMagic) return RF_OK;
     cudaMemsetAsync(workspace, 0, sizeof(word), stream);  // reported once
+    g_flag_epoch.fetch_add(1, std::memory_order_acq_rel);  // plans zero their split-pair flags again
     const unsigned code = (word >> 12) & 0xfu, cta = word & 0xfffu;
     return fail(RF_ERR_DEVICE_TIMEOUT,
                 std::string(code == 2 ? "a CTA timed out waiting for the partial of its predecessor"

@@ -36,66 +36,59 @@ __global__ void __launch_bounds__(128) bias_prepare_kernel(const float* __restri
 }
 
 
-// One CTA per (128-row tile, head, batch).  Eight threads share a row (16 bytes each, so a warp reads four whole
-// 128-byte rows per load instruction whatever the row stride is), eight passes cover the tile's 128 rows; the
-// row's sum of squares is an 8-lane shuffle reduction, the tile's largest key norm a block reduction.
+// One CTA per (128-key tile, head, batch): the largest key norm of the tile, an upper bound within 1.6 % (the odd
+// element of a bf16 pair is squared as it sits in its 32-bit word: the even element's bits below it only lengthen
+// the mantissa).  Eight threads share a row (16 bytes each, so a warp reads four whole 128-byte rows per load
+// instruction whatever the row stride is), eight passes cover the tile's 128 rows, all loads in flight at once.
 // Rows >= S count as 0.
 template <bool kBf16>
-__device__ __forceinline__ float sumsq8(const uint4& v) {
+__device__ __forceinline__ float sumsq8_bound(const uint4& v) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    float acc = 0.f;
+    float a0 = 0.f, a1 = 0.f;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        const float2 f = kBf16 ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]))
-                               : __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
-        acc = fmaf(f.x, f.x, acc);
-        acc = fmaf(f.y, f.y, acc);
+        float lo, hi;
+        if (kBf16) {
+            lo = __uint_as_float(w[e] << 16);
+            hi = __uint_as_float(w[e]);
+        } else {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+            lo = f.x;
+            hi = f.y;
+        }
+        a0 = fmaf(lo, lo, a0);
+        a1 = fmaf(hi, hi, a1);
     }
-    return acc;
+    return a0 + a1;
 }
 
 template <bool kBf16>
-__global__ void __launch_bounds__(128) qk_norms_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
-                                                       long long q_sb, long long q_sh, long long q_ss, long long k_sb,
-                                                       long long k_sh, long long k_ss, int H, int S, int d, int n_kv_tiles,
-                                                       float* __restrict__ qnorm, float* __restrict__ kmax,
-                                                       int* __restrict__ zero_ptr, int zero_words) {
+__global__ void __launch_bounds__(128) k_tile_norms_kernel(const uint16_t* __restrict__ k, long long k_sb, long long k_sh,
+                                                           long long k_ss, int H, int S, int d, int n_kv_tiles,
+                                                           float* __restrict__ kmax) {
     __shared__ float red[4];
     // let the attention kernel (launched with programmatic stream serialization) start its prologue now; it
     // waits for this grid to complete before it reads anything written here
     asm volatile("griddepcontrol.launch_dependents;");
     const int n = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-    // this launch also zeroes the split-pair flag block of the persistent schedule (saves a memset node)
-    {
-        const int gtid = ((b * gridDim.y + h) * gridDim.x + n) * kBlockN + threadIdx.x;
-        for (int i = gtid; i < zero_words; i += gridDim.x * gridDim.y * gridDim.z * kBlockN) zero_ptr[i] = 0;
-    }
-    const int sub = threadIdx.x & 7;   // 16-byte chunk of the row
-    const int rgrp = threadIdx.x >> 3; // row inside a pass of 16 rows
-    const uint16_t* qb = q + b * q_sb + h * q_sh + sub * 8;
+    const int sub = threadIdx.x & 7;    // 16-byte chunk of the row
+    const int rgrp = threadIdx.x >> 3;  // row inside a pass of 16 rows
     const uint16_t* kb = k + b * k_sb + h * k_sh + sub * 8;
-    float kn_max = 0.f;
     constexpr int kPasses = kBlockN / 16;
-    uint4 qv[kPasses], kv[kPasses];  // all sixteen loads of the thread are in flight before the first use
+    uint4 kv[kPasses];
 #pragma unroll
     for (int pass = 0; pass < kPasses; ++pass) {
         const int row = n * kBlockN + pass * 16 + rgrp;
-        qv[pass] = kv[pass] = make_uint4(0u, 0u, 0u, 0u);
-        if (row < S && sub * 8 < d) {  // head_dim 32: rows are four 16-byte chunks
-            qv[pass] = __ldg(reinterpret_cast<const uint4*>(qb + row * q_ss));
+        kv[pass] = make_uint4(0u, 0u, 0u, 0u);
+        if (row < S && sub * 8 < d)  // head_dim 32: rows are four 16-byte chunks
             kv[pass] = __ldg(reinterpret_cast<const uint4*>(kb + row * k_ss));
-        }
     }
+    float kn_max = 0.f;
 #pragma unroll
     for (int pass = 0; pass < kPasses; ++pass) {
-        const int row = n * kBlockN + pass * 16 + rgrp;
-        float qs = sumsq8<kBf16>(qv[pass]), ks = sumsq8<kBf16>(kv[pass]);
+        float ks = sumsq8_bound<kBf16>(kv[pass]);
 #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-            qs += __shfl_xor_sync(0xffffffffu, qs, o);
-            ks += __shfl_xor_sync(0xffffffffu, ks, o);
-        }
-        if (sub == 0 && row < S) qnorm[(static_cast<size_t>(b) * H + h) * S + row] = sqrtf(qs);
+        for (int o = 4; o > 0; o >>= 1) ks += __shfl_xor_sync(0xffffffffu, ks, o);
         kn_max = fmaxf(kn_max, ks);
     }
 #pragma unroll
@@ -257,18 +250,14 @@ cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias
     return cudaGetLastError();
 }
 
-cudaError_t launch_qk_norms(const void* q, const void* k, const long long qs[3], const long long ks[3], int dtype, int B,
-                            int H, int S, int d, int n_kv_tiles, float* qnorm, float* kmax, int* zero_ptr, int zero_words,
-                            cudaStream_t stream) {
+cudaError_t launch_k_tile_norms(const void* k, const long long ks[3], int dtype, int B, int H, int S, int d, int n_kv_tiles,
+                                float* kmax, cudaStream_t stream) {
     dim3 grid(n_kv_tiles, H, B);
-    const uint16_t* q16 = static_cast<const uint16_t*>(q);
     const uint16_t* k16 = static_cast<const uint16_t*>(k);
     if (dtype == 0)
-        qk_norms_kernel<true><<<grid, kBlockN, 0, stream>>>(q16, k16, qs[0], qs[1], qs[2], ks[0], ks[1], ks[2], H, S, d,
-                                                                      n_kv_tiles, qnorm, kmax, zero_ptr, zero_words);
+        k_tile_norms_kernel<true><<<grid, kBlockN, 0, stream>>>(k16, ks[0], ks[1], ks[2], H, S, d, n_kv_tiles, kmax);
     else
-        qk_norms_kernel<false><<<grid, kBlockN, 0, stream>>>(q16, k16, qs[0], qs[1], qs[2], ks[0], ks[1], ks[2], H, S, d,
-                                                               n_kv_tiles, qnorm, kmax, zero_ptr, zero_words);
+        k_tile_norms_kernel<false><<<grid, kBlockN, 0, stream>>>(k16, ks[0], ks[1], ks[2], H, S, d, n_kv_tiles, kmax);
     return cudaGetLastError();
 }
 

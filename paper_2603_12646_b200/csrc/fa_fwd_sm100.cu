@@ -20,10 +20,14 @@
 //               exchange their row max through shared memory (one 64-thread named barrier per
 //               tile); row sums stay per-thread until the epilogue.  exp2 with the scale folded in,
 //               packed f32x2 math, lazy rescale of O (only when the running max grows by > 2^20 with
-//               bf16 P, 2^14 with f16 P).  Row-max skip: when c |q_row| max_j |k_j| (norms from the
-//               qk_norms pre-pass) cannot exceed the reference max by more than that slack, the tile's
+//               bf16 P, 2^14 with f16 P).  Row-max skip: when c |q_row| max_j |k_j| cannot exceed the reference max by more than that slack, the tile's
 //               max pass, the exchange and its barrier are skipped (see the softmax loop).
 //               setmaxnreg moves registers from the producer/MMA warpgroup to the softmax ones.
+//               |q_row| is taken from the Q tile in shared memory by the softmax thread itself; the largest |k_j| of
+//               every key tile comes from a pre-pass over K (fa_aux.cu: k_tile_norms_kernel, 4 B per (head, tile)).
+//               (Taking the key norms in the kernel too -- two idle warps reading each K tile as it lands -- was
+//               measured: 224 us against 212 us at 8K, the extra shared-memory reads and issue slots cost more than
+//               the 3 us pre-pass.)
 //
 // Work distribution.  A work item is (query-tile pair, key-tile range).
 //   mode 0: one item per CTA (grid = number of pairs); used when the pairs fit one wave and for split-KV.
@@ -141,6 +145,57 @@ enum : uint32_t {
 constexpr uint32_t kTmemSlotOff = kNumBars * 8;                     // u32: TMEM base address
 constexpr uint32_t kWaitBlockOff = (kTmemSlotOff + 8 + 15) & ~15u;  // 16 bytes: abort word + status pointer (ptx.cuh)
 static_assert(kWaitBlockOff + 16 <= Smem::bar_bytes, "barrier block too small");
+
+// An UPPER bound (within 1.6 %) of the sum of squares of the eight 16-bit values of a 16-byte chunk, added to two
+// independent accumulators.  bf16: the odd element of a word is used as it sits in the word -- the even element's
+// bits below it only lengthen the mantissa, |w| >= |hi| and at most 2^-7 larger -- which saves the mask; the skip test
+// needs a bound, not the norm.
+template <bool kBf16>
+__device__ __forceinline__ void sumsq_chunk(const uint4& v, float& a0, float& a1) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        float lo, hi;
+        if (kBf16) {
+            lo = __uint_as_float(w[e] << 16);
+            hi = __uint_as_float(w[e]);
+        } else {
+            const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+            lo = f2.x;
+            hi = f2.y;
+        }
+        a0 = fmaf(lo, lo, a0);
+        a1 = fmaf(hi, hi, a1);
+    }
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+// Bound of |row|^2 for kRows 128-byte rows (kStride bytes apart) of a 128B-swizzled tile at once.  The swizzle
+// permutes a row's eight chunks, which a sum does not care about; lane l starts at chunk l mod 8 so that the warp's
+// 32 rows hit all banks (4 wavefronts per LDS.128).  Loads go out in batches, and every row has two accumulators.
+template <bool kBf16, int kRows, uint32_t kStride>
+__device__ __forceinline__ void rows_sumsq(uint32_t row_addr, int lane, float (&out)[kRows]) {
+    float a0[kRows], a1[kRows];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) a0[r] = a1[r] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; c += 2) {
+        uint4 v[kRows][2];
+#pragma unroll
+        for (int r = 0; r < kRows; ++r)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) v[r][u] = lds128(row_addr + r * kStride + (((c + u + lane) & 7) << 4));
+#pragma unroll
+        for (int r = 0; r < kRows; ++r)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) sumsq_chunk<kBf16>(v[r][u], a0[r], a1[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) out[r] = a0[r] + a1[r];
+}
 
 // kItemPublish: the CTA owns the LEADING key tiles of a pair cut at the end of its slice: processed first, partial
 // published for the next CTA.  kItemMerge: it owns the TRAILING key tiles of the pair its slice starts in:
@@ -280,7 +335,8 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         prefetch_tensormap(&tm_k);
         prefetch_tensormap(&tm_v);
         mbar_init(bar(kBarQFull), 1);
-        mbar_init(bar(kBarQEmpty), 1);
+        // Q is also read by every softmax warp (row norms): their arrivals join the UMMA commit on its empty barrier
+        mbar_init(bar(kBarQEmpty), 1 + kNumSoftmaxWarps);
         for (int s = 0; s < kStagesK; ++s) {
             mbar_init(bar(kBarKFull + s), 1);
             mbar_init(bar(kBarKEmpty + s), 1);
@@ -307,8 +363,8 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // Programmatic dependent launch: everything above overlapped the tail of the previous kernel in the stream
-    // (the norms pre-pass); its results -- and the zeroed flag block -- are visible after this.  A no-op when
-    // the kernel was launched normally.
+    // when that one triggers its dependents early; its results are visible after this.  A no-op when the kernel
+    // was launched normally.
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
     Sched sched;
@@ -593,10 +649,20 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // score of this row in that tile (Cauchy-Schwarz)
             float qn_c = CUDART_INF_F;
             const float* kmax_row = nullptr;
-            if (p.kmax != nullptr && active && num_live > 0) {
-                const size_t bh = static_cast<size_t>(b) * p.H + h;
-                qn_c = (row < p.S ? __ldg(p.qnorm + bh * p.S + row) : 0.f) * c * 1.001f;
-                kmax_row = p.kmax + bh * p.n_kv_tiles;
+            if (num_live > 0) {
+                // |q_row| from the Q tile in shared memory (rows past S arrive as zeros).  Every softmax warp waits
+                // for Q and arrives on its empty barrier, tile B's also when it sits the item out: the producer
+                // cannot run a Q phase ahead of any of them.
+                mbar_wait(bars_r + 8u * kBarQFull, oa & 1u, wctx);
+                if (active && p.kmax != nullptr) {
+                    kmax_row = p.kmax + (static_cast<size_t>(b) * p.H + h) * p.n_kv_tiles;
+                    const uint32_t qrow = bars_r - Smem::bars + Smem::q + x * kTileBytes + static_cast<uint32_t>(r) * 128u;
+                    float sq[1];
+                    rows_sumsq<kBf16, 1, 0u>(qrow, lane, sq);
+                    qn_c = sqrtf(sq[0]) * c * 1.001f;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bars_r + 8u * kBarQEmpty);
             }
 
             if (active && num_live > 0) {
@@ -889,6 +955,10 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         }
                         l_tot = l_tot * w1 + l2 * w2;
                         m_ref = ms;
+                        // The flags are left as they were found (zero): this warp and its twin of the other half
+                        // are the only readers of the two flags they waited for, and both are done with them.
+                        named_bar_sync(bar_id, kPairThreads);
+                        if (lane == 0) p.part_flag[(blockIdx.x - 1) * kNumSoftmaxWarps + warp] = 0;
                     }
                     if (row < p.S && col0 < p.d) {  // head_dim 32 runs zero-padded to 64: its columns [32, 64) do not exist
                         if (p.o_partial != nullptr) {
@@ -949,20 +1019,22 @@ size_t fa_fwd_sm100_smem_bytes() {
 }
 
 size_t fa_fwd_sm100_partial_bytes(int grid) {
-    // per CTA: O partial [2][128][64] f32, (m, l) [2][128][2] f32, 16 warp flags
-    return static_cast<size_t>(grid) * (2 * kBlockM * kHeadDim * 4 + 2 * kBlockM * 2 * 4 + kNumSoftmaxWarps * 4);
+    // per CTA: O partial [2][128][64] f32, (m, l) [2][128][2] f32
+    return static_cast<size_t>(grid) * (2 * kBlockM * kHeadDim * 4 + 2 * kBlockM * 2 * 4);
 }
 
-// Carves the split-pair workspace; the flag block must be zero when the kernel starts.
-void fa_fwd_sm100_partial_carve(void* base, int grid, FaParams* p, void** flags, size_t* flag_bytes) {
+size_t fa_fwd_sm100_flag_bytes(int grid) {
+    return static_cast<size_t>(grid) * kNumSoftmaxWarps * 4;  // one flag per (CTA, softmax warp)
+}
+
+// Carves the split-pair workspace.  `flags` (fa_fwd_sm100_flag_bytes) must be zero when the kernel starts; the
+// kernel leaves it zero.
+void fa_fwd_sm100_partial_carve(void* base, void* flags, int grid, FaParams* p) {
     uint8_t* b = static_cast<uint8_t*>(base);
     p->part_o = reinterpret_cast<float*>(b);
     b += static_cast<size_t>(grid) * 2 * kBlockM * kHeadDim * 4;
     p->part_ml = reinterpret_cast<float*>(b);
-    b += static_cast<size_t>(grid) * 2 * kBlockM * 2 * 4;
-    p->part_flag = reinterpret_cast<int*>(b);
-    *flags = b;
-    *flag_bytes = static_cast<size_t>(grid) * kNumSoftmaxWarps * 4;
+    p->part_flag = static_cast<int*>(flags);
 }
 
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,

@@ -59,8 +59,8 @@ struct FaParams {
     int* part_flag;
     // Cauchy-Schwarz bound on the scores of a (query row, key tile): |q_i| * max_j |k_j|.  When it cannot
     // exceed the running reference max by more than the lazy-rescale threshold, the softmax warps skip the
-    // row-max pass of that tile.  qnorm [B,H,S], kmax [B,H,n_kv_tiles] (qk_norms_kernel); nullptr = off.
-    const float* qnorm;
+    // row-max pass of that tile.  |q_i| is taken from the Q tile in shared memory inside the kernel; kmax
+    // [B,H,n_kv_tiles] comes from k_tile_norms_kernel (fa_aux.cu); nullptr = test off.
     const float* kmax;
 };
 
@@ -75,8 +75,8 @@ struct SimtParams {
 };
 
 // launchers (return cudaError_t of the launch)
-// pdl: launch with programmatic stream serialization (the previous kernel in the stream calls
-// griddepcontrol.launch_dependents; this one waits for it after its prologue)
+// pdl: launch with programmatic stream serialization (when the previous kernel in the stream calls
+// griddepcontrol.launch_dependents, this one's prologue overlaps its tail)
 cudaError_t launch_fa_fwd_sm100(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
                                 const FaParams& p, bool bf16, int grid, cudaStream_t stream, bool pdl = false);
 // narrow-window kernel (fa_fwd_sm100_local.cu): wl + wr <= 127, one 256-key strip per query tile;
@@ -94,17 +94,16 @@ size_t fa_fwd_sm100_d128_smem_bytes();
 bool fa_fwd_sm100_d128_available();
 size_t fa_fwd_sm100_smem_bytes();
 size_t fa_fwd_sm100_partial_bytes(int grid);
-void fa_fwd_sm100_partial_carve(void* base, int grid, FaParams* p, void** flags, size_t* flag_bytes);
+size_t fa_fwd_sm100_flag_bytes(int grid);
+void fa_fwd_sm100_partial_carve(void* base, void* flags, int grid, FaParams* p);
 cudaError_t launch_fa_fwd_simt(const SimtParams& p, cudaStream_t stream, int* grid_ctas);
 
 cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias2, uint8_t* tile_flags,
                                 int n_kv_tiles, cudaStream_t stream);
-// |q_i| per query row and max_j |k_j| per 128-key tile (inputs of the row-max skip test)
-// (also zeroes zero_words ints at zero_ptr -- the persistent schedule's flag block -- and triggers
-// programmatic launch of the next kernel in the stream)
-cudaError_t launch_qk_norms(const void* q, const void* k, const long long q_strides[3], const long long k_strides[3],
-                            int dtype, int B, int H, int S, int d, int n_kv_tiles, float* qnorm, float* kmax, int* zero_ptr,
-                            int zero_words, cudaStream_t stream);
+// max_j |k_j| per (head, 128-key tile): the key side of the row-max skip test.  Triggers programmatic launch of the
+// next kernel in the stream right away (the attention kernel's prologue overlaps it).
+cudaError_t launch_k_tile_norms(const void* k, const long long k_strides[3], int dtype, int B, int H, int S, int d,
+                                int n_kv_tiles, float* kmax, cudaStream_t stream);
 cudaError_t launch_merge(const float* const* o_parts, const float* const* m_parts, const float* const* l_parts,
                          int G, long long rows, int d, void* out, int out_dtype, cudaStream_t stream);
 // split-KV partial of an empty key block: O = 0, m = -inf, l = 0
