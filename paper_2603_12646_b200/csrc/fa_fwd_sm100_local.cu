@@ -165,6 +165,13 @@ __device__ __forceinline__ void advance_tile(const FaParams& p, Tile& t, int q_t
     t.kb = t.r0 - p.wl;
 }
 
+// 256-bit global store (sm_100): eight 32-bit words, 32-byte aligned
+__device__ __forceinline__ void st_global_v8(void* dst, const uint32_t (&w)[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                 "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+}
+
 // tcgen05.wait::ld tied to the registers the loads wrote: nothing that reads them can be scheduled above it
 __device__ __forceinline__ void wait_ld16(uint32_t (&r)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"
@@ -375,6 +382,10 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         constexpr float kTau = kBf16 ? 20.0f : 14.0f;
         const float* sbias = reinterpret_cast<const float*>(smem_gen + Smem::bias);
         const uint32_t row_bar = 1 + quad;     // named barrier of the two warps that share 32 rows
+        // every (batch, head, row, half-row) output segment starts on a 32-byte boundary
+        const int osz = p.out_dtype == 2 ? 4 : 2;
+        const bool wide_ok = (reinterpret_cast<uintptr_t>(p.out) & 31) == 0 && ((p.o_sb * osz) & 31) == 0 &&
+                             ((p.o_sh * osz) & 31) == 0 && ((p.o_ss * osz) & 31) == 0;
 
         // Band mask as an additive table instead of two compares and a select per element: f(col - r) = 0 on
         // [0, band], -inf elsewhere.  Four copies, copy k shifted by k entries, so that the lane of row r reads
@@ -527,16 +538,19 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
             // band for the most rows: the last one of the lower half, the first one of the upper half.
             auto piece_of = [&](int j) { return first_piece + (part ? j : mine - 1 - j); };  // processing order
             auto piece_var_of = [&](int j) { return piece_var(piece_of(j) - first_piece); };
-            uint32_t su[16];
-            tmem_ld16(t_s + piece_of(0) * kPiece, su);
-            wait_ld16(su);
+            // Two piece buffers: the load of piece j + 1 is in flight while piece j is worked on (a tcgen05.ld round trip
+            // is 100-200 clk under load, five of them in a row were a third of the pass).
+            uint32_t su[2][16];
+            tmem_ld16(t_s + piece_of(0) * kPiece, su[0]);
+            wait_ld16(su[0]);
+            if (mine > 1) tmem_ld16(t_s + piece_of(1) * kPiece, su[1]);  // lands during the exchange below
             {
                 float mx = -CUDART_INF_F;
                 const int c0 = piece_of(0) * kPiece;
                 const int var = piece_var_of(0);
-                if (var == 0) max_piece(su, c0, std::integral_constant<int, 0>{}, mx);
-                else if (var == 1) max_piece(su, c0, std::integral_constant<int, 1>{}, mx);
-                else max_piece(su, c0, std::integral_constant<int, 2>{}, mx);
+                if (var == 0) max_piece(su[0], c0, std::integral_constant<int, 0>{}, mx);
+                else if (var == 1) max_piece(su[0], c0, std::integral_constant<int, 1>{}, mx);
+                else max_piece(su[0], c0, std::integral_constant<int, 2>{}, mx);
                 xchg[part * kBlockM + r] = mx;
             }
             named_bar_sync(row_bar, 32 * kParts);
@@ -547,22 +561,32 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
             uint64_t sum2 = 0;
             float xmax = -CUDART_INF_F;
             uint32_t pk[kMaxPieces][8];  // pk[j] = piece piece_of(j)
-            auto run_pass = [&](float neg_m, auto first_loaded_tag) {
-                constexpr bool kFirstLoaded = decltype(first_loaded_tag)::value;
+            auto run_piece = [&](const uint32_t (&sj)[16], int j, float neg_m) {
+                const int c0 = piece_of(j) * kPiece;
+                const int var = piece_var_of(j);
+                if (var == 0) exp_piece(sj, c0, std::integral_constant<int, 0>{}, neg_m, sum2, xmax, pk[j]);
+                else if (var == 1) exp_piece(sj, c0, std::integral_constant<int, 1>{}, neg_m, sum2, xmax, pk[j]);
+                else exp_piece(sj, c0, std::integral_constant<int, 2>{}, neg_m, sum2, xmax, pk[j]);
+            };
+            // kPrefetched: piece 0 is in su[0] and the load of piece 1 into su[1] has been issued (first pass);
+            // otherwise (redo with the exact maximum, rare) everything is loaded again
+            auto run_pass = [&](float neg_m, auto prefetched_tag) {
+                constexpr bool kPrefetched = decltype(prefetched_tag)::value;
                 sum2 = 0;
                 xmax = -CUDART_INF_F;
+                if (!kPrefetched) {
+                    tmem_ld16(t_s + piece_of(0) * kPiece, su[0]);
+                    if (mine > 1) tmem_ld16(t_s + piece_of(1) * kPiece, su[1]);
+                    wait_ld16(su[0]);
+                }
 #pragma unroll
                 for (int j = 0; j < kMaxPieces; ++j) {
                     if (j < mine) {
-                        if (j > 0 || !kFirstLoaded) {
-                            tmem_ld16(t_s + piece_of(j) * kPiece, su);
-                            wait_ld16(su);
+                        if (j >= 1) {
+                            wait_ld16(su[j & 1]);  // (waits for every load issued so far)
+                            if (j + 1 < mine) tmem_ld16(t_s + piece_of(j + 1) * kPiece, su[(j + 1) & 1]);
                         }
-                        const int c0 = piece_of(j) * kPiece;
-                        const int var = piece_var_of(j);
-                        if (var == 0) exp_piece(su, c0, std::integral_constant<int, 0>{}, neg_m, sum2, xmax, pk[j]);
-                        else if (var == 1) exp_piece(su, c0, std::integral_constant<int, 1>{}, neg_m, sum2, xmax, pk[j]);
-                        else exp_piece(su, c0, std::integral_constant<int, 2>{}, neg_m, sum2, xmax, pk[j]);
+                        run_piece(su[j & 1], j, neg_m);
                     }
                 }
                 float sum0, sum1;
@@ -623,25 +647,41 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(kBarTmemFree));
             if (row < seq_len && part * kOutCols < p.d) {  // head_dim 32 runs zero-padded to 64 (FaParams::d)
+                // A lane owns one row, so a warp-wide store touches 32 rows whatever its width: 32-byte stores (sm_100's
+                // 256-bit st.global) halve the number of store instructions -- and of LSU passes, 32 per instruction --
+                // against 16-byte ones.  wide_ok: base and strides keep every row segment 32-byte aligned (host-checked).
                 if (p.out_dtype == 2) {
-                    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
-#pragma unroll
-                    for (int u = 0; u < kOutCols / 4; ++u)
-                        dst[u] = make_float4(__uint_as_float(ou[4 * u]) * inv, __uint_as_float(ou[4 * u + 1]) * inv,
-                                             __uint_as_float(ou[4 * u + 2]) * inv, __uint_as_float(ou[4 * u + 3]) * inv);
-                } else {
-                    const bool out_bf16 = p.out_dtype == 0;
-                    uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + off);
+                    float* dst = static_cast<float*>(p.out) + off;
 #pragma unroll
                     for (int u = 0; u < kOutCols / 8; ++u) {
-                        uint32_t w[4];
+                        uint32_t w[8];
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float a0 = __uint_as_float(ou[8 * u + 2 * e]) * inv;
-                            const float a1 = __uint_as_float(ou[8 * u + 2 * e + 1]) * inv;
+                        for (int e = 0; e < 8; ++e) w[e] = __float_as_uint(__uint_as_float(ou[8 * u + e]) * inv);
+                        if (wide_ok) {
+                            st_global_v8(dst + 8 * u, w);
+                        } else {
+                            *reinterpret_cast<uint4*>(dst + 8 * u) = make_uint4(w[0], w[1], w[2], w[3]);
+                            *reinterpret_cast<uint4*>(dst + 8 * u + 4) = make_uint4(w[4], w[5], w[6], w[7]);
+                        }
+                    }
+                } else {
+                    const bool out_bf16 = p.out_dtype == 0;
+                    uint16_t* dst = static_cast<uint16_t*>(p.out) + off;
+#pragma unroll
+                    for (int u = 0; u < kOutCols / 16; ++u) {
+                        uint32_t w[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const float a0 = __uint_as_float(ou[16 * u + 2 * e]) * inv;
+                            const float a1 = __uint_as_float(ou[16 * u + 2 * e + 1]) * inv;
                             w[e] = out_bf16 ? pack2<true>(a0, a1) : pack2<false>(a0, a1);
                         }
-                        dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+                        if (wide_ok) {
+                            st_global_v8(dst + 16 * u, w);
+                        } else {
+                            *reinterpret_cast<uint4*>(dst + 16 * u) = make_uint4(w[0], w[1], w[2], w[3]);
+                            *reinterpret_cast<uint4*>(dst + 16 * u + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+                        }
                     }
                 }
             }
