@@ -108,11 +108,14 @@ constexpr bool kPingPong = RF_FA_PINGPONG != 0;
 #ifndef RF_FA_VK_IN_SOFTMAX
 #define RF_FA_VK_IN_SOFTMAX 0
 #endif
+#ifndef RF_FA_TRACE_TILES
+#define RF_FA_TRACE_TILES 64  // key tiles of CTA 0 the trace buffer holds per warp
+#endif
 #if RF_FA_TRACE
 #define RF_STAMP(slot)                                                                               \
     do {                                                                                             \
-        if (blockIdx.x == 0 && lane == 0 && trace_n < 64 && p.debug_scores != nullptr)               \
-            reinterpret_cast<uint32_t*>(p.debug_scores)[(warp * 64 + trace_n) * 8 + (slot)] = clock(); \
+        if (blockIdx.x == 0 && lane == 0 && trace_n < RF_FA_TRACE_TILES && p.debug_scores != nullptr)               \
+            reinterpret_cast<uint32_t*>(p.debug_scores)[(warp * RF_FA_TRACE_TILES + trace_n) * 8 + (slot)] = clock(); \
     } while (0)
 #else
 #define RF_STAMP(slot) do { } while (0)
@@ -328,6 +331,17 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 
     const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform by construction: lets roles, buffer indices and TMEM addresses live in uniform registers
     const int lane = threadIdx.x & 31;
+#if RF_FA_TRACE
+    // kernel-level stamps of CTA 0 in the row of (idle) warp 18: 0 entry, 1 prologue done, 2 dependencies resolved, 3 teardown
+#define RF_KSTAMP(slot)                                                                                          \
+    do {                                                                                                         \
+        if (blockIdx.x == 0 && threadIdx.x == 18 * 32 && p.debug_scores != nullptr)                              \
+            reinterpret_cast<uint32_t*>(p.debug_scores)[(18 * RF_FA_TRACE_TILES) * 8 + (slot)] = clock();        \
+    } while (0)
+#else
+#define RF_KSTAMP(slot) do { } while (0)
+#endif
+    RF_KSTAMP(0);
 
     // ---------------- prologue ----------------
     if (warp == kProducerWarp && lane == 0) {
@@ -362,10 +376,12 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    RF_KSTAMP(1);
     // Programmatic dependent launch: everything above overlapped the tail of the previous kernel in the stream
     // when that one triggers its dependents early; its results are visible after this.  A no-op when the kernel
     // was launched normally.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    RF_KSTAMP(2);
 
     Sched sched;
     sched_init(p, sched);
@@ -616,6 +632,10 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         float* xrow_base = xchg + (x * 2) * kBlockM + r;
         // named barrier shared by the two warps that own the same 32 rows (ids 1..8)
         const uint32_t bar_id = 1 + x * 4 + (warp & 3);
+        // every (batch, head, row, half-row) output segment starts on a 32-byte boundary: 256-bit stores are legal
+        const int osz = p.out_dtype == 2 ? 4 : 2;
+        const bool wide_ok = (reinterpret_cast<uintptr_t>(p.out) & 31) == 0 && ((p.o_sb * osz) & 31) == 0 &&
+                             ((p.o_sh * osz) & 31) == 0 && ((p.o_ss * osz) & 31) == 0;
         constexpr uint32_t kPairThreads = 64;
         uint32_t bars_r = bars;
         asm volatile("mov.u32 %0, %0;" : "+r"(bars_r));
@@ -635,6 +655,13 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const uint32_t turn_other = bars_r + 8u * (kBarTurn + (x ^ 1) * 4 + (warp & 3));
         uint32_t tn = static_cast<uint32_t>(x) + 1u;  // parity of the next turn wait is tn & 1
 
+        bool pub_pending = false;  // this warp wrote a split-pair partial whose flag is not raised yet (warp-uniform)
+        auto raise_flag = [&]() {
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) st_release_gpu(p.part_flag + blockIdx.x * kNumSoftmaxWarps + warp, 1);
+            pub_pending = false;
+        };
         while (next_item<kHasBias>(p, sched, item)) {
             const int b = item.b, h = item.h;
             const int num_live = item.num_live;
@@ -853,6 +880,7 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     RF_STAMP(6);
                     tc_fence_before();
                     mbar_arrive(bars_r + 8u * (kBarPFull + sb));
+                    if (pub_pending && it >= 3) raise_flag();  // the partial's stores drained long ago: a short fence
                     RF_STAMP(7);
 #if RF_FA_TRACE
                     ++trace_n;
@@ -915,17 +943,18 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     // this CTA owns only the leading key tiles of the pair: publish an un-normalised partial
                     // for CTA blockIdx.x + 1, which holds the trailing key tiles and merges at the end of its slice
                     const size_t slot = (static_cast<size_t>(blockIdx.x) * 2 + x) * kBlockM + r;
-                    float4* dst = reinterpret_cast<float4*>(p.part_o + slot * kHeadDim + col0);
+                    float* dst = p.part_o + slot * kHeadDim + col0;  // 128-byte aligned
 #pragma unroll
-                    for (int u = 0; u < kOutCols / 4; ++u)
-                        dst[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+                    for (int u = 0; u < kOutCols / 8; ++u)
+                        st_global_v8(dst + 8 * u, reinterpret_cast<const uint32_t(&)[8]>(o[8 * u]));
                     if (hf == 0) {
                         p.part_ml[slot * 2] = m_ref;
                         p.part_ml[slot * 2 + 1] = l_tot;
                     }
-                    __threadfence();
-                    __syncwarp();
-                    if (lane == 0) st_release_gpu(p.part_flag + blockIdx.x * kNumSoftmaxWarps + warp, 1);
+                    // The flag is raised a few key tiles into the next item (or at the end of the kernel): a fence right
+                    // here waits for these 128 KiB of stores to drain (~5 us at every publishing CTA, phase trace), and
+                    // the reader only wants the partial at the very end of its own slice.
+                    pub_pending = true;
                 } else {
                     if (item.kind == kItemMerge) {
                         // merge with the partial CTA blockIdx.x - 1 published for the same rows at the START of
@@ -975,23 +1004,38 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             const float inv = l_tot > 0.f ? 1.0f / l_tot : 0.f;
                             const size_t off = static_cast<size_t>(b) * p.o_sb + static_cast<size_t>(h) * p.o_sh +
                                                static_cast<size_t>(row) * p.o_ss + col0;
+                            // A lane owns one row, so a warp-wide store touches 32 rows whatever its width: 32-byte
+                            // stores (sm_100's 256-bit st.global) halve the store instructions and their LSU passes.
                             if (p.out_dtype == 2) {
-                                float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
-#pragma unroll
-                                for (int u = 0; u < kOutCols / 4; ++u)
-                                    dst[u] = make_float4(o[4 * u] * inv, o[4 * u + 1] * inv, o[4 * u + 2] * inv,
-                                                         o[4 * u + 3] * inv);
-                            } else {
-                                uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + off);
+                                float* dst = static_cast<float*>(p.out) + off;
 #pragma unroll
                                 for (int u = 0; u < kOutCols / 8; ++u) {
-                                    uint32_t w[4];
+                                    uint32_t w[8];
 #pragma unroll
-                                    for (int e = 0; e < 4; ++e) {
-                                        const float a0 = o[8 * u + 2 * e] * inv, a1 = o[8 * u + 2 * e + 1] * inv;
+                                    for (int e = 0; e < 8; ++e) w[e] = __float_as_uint(o[8 * u + e] * inv);
+                                    if (wide_ok) {
+                                        st_global_v8(dst + 8 * u, w);
+                                    } else {
+                                        *reinterpret_cast<uint4*>(dst + 8 * u) = make_uint4(w[0], w[1], w[2], w[3]);
+                                        *reinterpret_cast<uint4*>(dst + 8 * u + 4) = make_uint4(w[4], w[5], w[6], w[7]);
+                                    }
+                                }
+                            } else {
+                                uint16_t* dst = static_cast<uint16_t*>(p.out) + off;
+#pragma unroll
+                                for (int u = 0; u < kOutCols / 16; ++u) {
+                                    uint32_t w[8];
+#pragma unroll
+                                    for (int e = 0; e < 8; ++e) {
+                                        const float a0 = o[16 * u + 2 * e] * inv, a1 = o[16 * u + 2 * e + 1] * inv;
                                         w[e] = (p.out_dtype == 0) ? pack2<true>(a0, a1) : pack2<false>(a0, a1);
                                     }
-                                    dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+                                    if (wide_ok) {
+                                        st_global_v8(dst + 16 * u, w);
+                                    } else {
+                                        *reinterpret_cast<uint4*>(dst + 16 * u) = make_uint4(w[0], w[1], w[2], w[3]);
+                                        *reinterpret_cast<uint4*>(dst + 16 * u + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+                                    }
                                 }
                             }
                         }
@@ -1001,11 +1045,13 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             if (active && num_live > 0) ++oi;
             if (num_live > 0) ++oa;
         }
+        if (pub_pending) raise_flag();
     }
 
     // ---------------- teardown ----------------
     tc_fence_before();
     __syncthreads();
+    RF_KSTAMP(3);
     if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc(tmem_base, kTmemCols);

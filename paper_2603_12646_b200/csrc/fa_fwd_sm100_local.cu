@@ -165,13 +165,6 @@ __device__ __forceinline__ void advance_tile(const FaParams& p, Tile& t, int q_t
     t.kb = t.r0 - p.wl;
 }
 
-// 256-bit global store (sm_100): eight 32-bit words, 32-byte aligned
-__device__ __forceinline__ void st_global_v8(void* dst, const uint32_t (&w)[8]) {
-    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]),
-                 "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
-                 : "memory");
-}
-
 // tcgen05.wait::ld tied to the registers the loads wrote: nothing that reads them can be scheduled above it
 __device__ __forceinline__ void wait_ld16(uint32_t (&r)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"
