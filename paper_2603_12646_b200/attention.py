@@ -193,7 +193,10 @@ class FaPlan:
     change between launches, their addresses may not."""
 
     def __init__(self, q, k, v, spec: Optional[AttentionSpec] = None, *, out: Optional[torch.Tensor] = None,
-                 out_dtype: Optional[torch.dtype] = None, kernel: str = "auto", kv_range=None, partials=None):
+                 out_dtype: Optional[torch.dtype] = None, kernel: str = "auto", kv_range=None, partials=None,
+                 workspace: Optional[torch.Tensor] = None):
+        """workspace: a caller-owned uint8 CUDA tensor to carve the plan's workspace from instead of a private one
+        (a session shares one between the plans of its layers; launches that share a workspace must not overlap)."""
         _check_qkv_shapes(q, k, v)
         self.lib = capi.load()
         self.device = q.device
@@ -204,7 +207,12 @@ class FaPlan:
         self.stats = FlashStats()
         _fill_stats(self.stats, st)
         nbytes = int(st.workspace_bytes)
-        self._ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=self.device)
+        if workspace is not None:
+            if workspace.dtype != torch.uint8 or workspace.device != self.device or workspace.numel() < nbytes:
+                raise ShapeMismatch(capi.RF_ERR_WORKSPACE, f"workspace must be a uint8 tensor of >= {nbytes} bytes on {self.device}")
+            self._ws = workspace
+        else:
+            self._ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=self.device)
         self._h = C.c_void_p()
         with torch.cuda.device(self.device):
             capi.check(self.lib.rf_fa_plan_create(C.byref(p), self._ws.data_ptr() if nbytes else None, nbytes,

@@ -209,6 +209,63 @@ def test_plan_launch_equals_direct_call_and_reports_status(torch_mod, P, oracle)
         plan.close()
 
 
+def test_plans_of_different_layouts_share_one_workspace(torch_mod, P, oracle):
+    """The split-pair flags of the persistent balanced schedule sit at a fixed offset behind the status block whatever
+    else a plan keeps in its workspace, are zeroed by a plan's first launch only and left zero by the kernel.  Two
+    plans with different carve-ups (with and without a pad bias) therefore can take turns on ONE workspace, any number
+    of times, and give what they give alone."""
+    torch = torch_mod
+    from paper_2603_12646_b200 import capi
+    from paper_2603_12646_b200.attention import FaPlan
+    B, H, S, d = 2, 12, 4096, 64     # 384 pairs > 148 SMs: split pairs, partials, flags
+    g = torch.Generator(device="cuda").manual_seed(23)
+    q, k, v = [(torch.rand((B, H, S, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+    pb = torch.from_numpy(tail_pad(B, S, [4096, 3001])).cuda()
+    spec_a, spec_b = P.AttentionSpec(), P.AttentionSpec(0.0, -1, -1, pb)
+    st_a, st_b = P.FlashStats(), P.FlashStats()
+    ref_a = P.flash_attention(q, k, v, spec_a, stats=st_a).clone()
+    ref_b = P.flash_attention(q, k, v, spec_b, stats=st_b).clone()
+    assert st_a.workspace_bytes != st_b.workspace_bytes
+    ws = torch.empty(max(st_a.workspace_bytes, st_b.workspace_bytes), dtype=torch.uint8, device="cuda")
+    ws.fill_(0xAB)                   # a fresh arena is not zero
+    oa, ob = torch.empty_like(ref_a), torch.empty_like(ref_b)
+    pa = FaPlan(q, k, v, spec_a, out=oa, workspace=ws)
+    pbl = FaPlan(q, k, v, spec_b, out=ob, workspace=ws)
+    for _ in range(6):
+        pa.launch()
+        pbl.launch()
+        pbl.launch()
+        pa.launch()
+    torch.cuda.synchronize()
+    assert pa.status() == capi.RF_OK
+    assert torch.equal(oa, ref_a) and torch.equal(ob, ref_b)
+    pa.close()
+    pbl.close()
+
+
+@pytest.mark.parametrize("window", [(-1, -1), (63, 64)])
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_output_rows_off_the_32_byte_grid(torch_mod, P, oracle, window, dt):
+    """The kernels write their output rows with 32-byte stores when every row segment is 32-byte aligned and fall back to
+    16-byte stores when it is not: an output view that starts 16 bytes into its buffer gives the same bits."""
+    torch = torch_mod
+    B, H, S, d = 1, 3, 700, 64
+    g = torch.Generator(device="cuda").manual_seed(29)
+    q, k, v = [(torch.rand((B, H, S, d), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+    odt = torch.bfloat16 if dt == "bf16" else torch.float32
+    spec = P.AttentionSpec(0.0, *window)
+    aligned = P.flash_attention(q, k, v, spec, out_dtype=odt)
+    shift = 16 // aligned.element_size()
+    buf = torch.zeros(B * H * S * d + shift, device="cuda", dtype=odt)
+    view = buf[shift:].view(B, H, S, d)
+    assert view.data_ptr() % 32 == 16
+    P.flash_attention(q, k, v, spec, out=view)
+    torch.cuda.synchronize()
+    assert torch.equal(view, aligned)
+    want = oracle.flash_attention(*[t.float().cpu().numpy() for t in (q, k, v)], 0.0, window[0], window[1], None)
+    assert float(np.abs(aligned.float().cpu().numpy() - want).max()) <= TOL
+
+
 # ------------------------------------------------------------------ persistent schedule under contention
 def test_two_persistent_calls_on_two_streams_do_not_starve(torch_mod, P, oracle):
     """Two balanced-schedule (mode 1) launches run concurrently on two streams, each with its own workspace,
