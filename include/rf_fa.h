@@ -148,7 +148,11 @@ int rf_fa_fwd(const rf_fa_params* p, void* workspace, size_t workspace_bytes, vo
  * selection, workspace carve-up, the three TMA tensor maps -- once; rf_fa_plan_launch only enqueues the kernels
  * (asynchronous, any stream, any number of times; thread-safe for concurrent launches as long as concurrent
  * launches do not share one workspace).  The plan refers to the tensors and the workspace of `p` by address:
- * they must stay allocated, their contents may change between launches. */
+ * they must stay allocated, their contents may change between launches.
+ * Plans may share one workspace (a session's layers do) as long as their launches do not overlap in time: the
+ * only state that lives across launches -- the split-pair flags of the persistent balanced schedule -- sits at the
+ * same offset in every plan's carve-up, is zeroed in-stream by a plan's first launch (the workspace need not be
+ * zeroed by the caller) and is left zero by the kernel. */
 typedef struct rf_fa_plan rf_fa_plan;
 int rf_fa_plan_create(const rf_fa_params* p, void* workspace, size_t workspace_bytes, rf_fa_plan** plan);
 int rf_fa_plan_launch(const rf_fa_plan* plan, void* stream);

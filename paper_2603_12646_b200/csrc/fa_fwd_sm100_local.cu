@@ -523,8 +523,9 @@ fa_fwd_sm100_local_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
             RF_STAMP(n, 1);
 
             // ---- reference max: the maximum over ONE piece per thread, agreed between the two threads of a row ----
-            // TMEM delivers ~64 B/clk per SM: a separate max pass over the 80 KiB of live S would cost ~1300 clk per
-            // tile, more than the exponentials.  So S is read once: exponentials are taken relative to m_ref <= the
+            // A separate max pass would read the 80 KiB of live S twice, five dependent tcgen05.ld round trips of
+            // 100-200 clk each per thread and pass (the bandwidth is there -- 436 B/clk/SM with 16 warps,
+            // tools/probes/tmem_rate.cu -- the latency is what costs).  So S is read once: exponentials are taken relative to m_ref <= the
             // row max, the true maximum is tracked on the way, and only if it turns out more than kTau above m_ref
             // (P would overflow its 16-bit type) or m_ref was useless (every sampled key masked) the two warps of the
             // quad redo the pass with the exact maximum.  A thread samples the piece of its share that is inside the

@@ -4,7 +4,8 @@
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -x -q 2>&1 | tail -6 | tee gpurun_out/pytest_gpu.log
 python __graft_entry__.py smoke 2>&1 | tail -5 | tee gpurun_out/smoke.log
-python bench.py --steps 1000 --warmup 20 2>&1 | tail -1 > gpurun_out/bench.json; cut -c1-600 gpurun_out/bench.json
+python bench.py --gpus 1 --steps 20 --warmup 5 2>&1 | tail -1 > gpurun_out/bench.json; cut -c1-600 gpurun_out/bench.json
+python bench.py --steps 1000 --warmup 20 --quick --no-cpu 2>&1 | tail -1 > gpurun_out/bench_sustained.json; cut -c1-300 gpurun_out/bench_sustained.json
 python bench.py --impl reference --steps 2 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_ref.json; cut -c1-300 gpurun_out/bench_ref.json
 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 20 --warmup 5 --quick --no-cpu > gpurun_out/bench_under_ncu.log 2>&1
@@ -22,4 +23,6 @@ python tools/local_bench.py 2>&1 | tail -1 > gpurun_out/local_bench_line.json
 python tools/gemm_bench.py 2>&1 | tail -1 > gpurun_out/gemm_bench_8k.json
 python tools/gemm_bench.py 16384 2>&1 | tail -1 > gpurun_out/gemm_bench_16k.json
 python tools/clf_ab.py 2>&1 | tail -1 > gpurun_out/clf_ab.json
+timeout 120 tools/probes/tmem_rate.bin > gpurun_out/tmem_rate_probe.jsonl 2>&1
+python tools/plan_bench.py > gpurun_out/plan_bench.log 2>&1
 cat gpurun_out/local_bench_line.json gpurun_out/clf_ab.json | cut -c1-700
