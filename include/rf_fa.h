@@ -208,6 +208,18 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
                    int32_t compute_dtype, int32_t device, rf_fa_stats* stats);
 void rf_fa_host_release(void);
 
+/* The rounding rf_fa_fwd_host applies to Q, K, V before they cross the link: f32 -> bf16, round to nearest even (NaN
+ * stays NaN), on a small pool of host threads (RF_FA_HOST_CAST_THREADS, default min(16, cores - 1); RF_FA_HOST_CAST=0
+ * keeps the rounding on the device).  Bit-identical to the device cast.  No CUDA call; exposed for tests and for
+ * callers that keep their own 16-bit copies.  The reference has no counterpart (its Tensor is f32 only,
+ * proj/core/include/routefast/tensor.hpp). */
+int rf_host_round_bf16(const float* src, uint16_t* dst, int64_t n);
+
+/* Bytes the calling thread's rf_fa_fwd_host calls have moved over the link so far (cumulative since the thread's
+ * first call) and how many calls completed: what a benchmark reports as host-to-device / device-to-host bytes per
+ * call, whichever way the inputs were rounded.  Measurement aid; the reference has no counterpart. */
+void rf_fa_host_transfer_counters(uint64_t* h2d_bytes, uint64_t* d2h_bytes, uint64_t* calls);
+
 /* The interpreter's FusedFlashAttention case (interpreter.cpp:308-318) on host tensors:
  * n_inputs is 3 or 4 (4th = pad_bias), each with its rank and dims; attrs default to scale 0.0,
  * windows -1 exactly as node.attr_real/attr_int fall back.  has_* flags say which attrs the

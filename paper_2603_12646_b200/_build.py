@@ -12,7 +12,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librf_fa.so")
-SOURCES = ["fa_fwd_sm100.cu", "fa_fwd_sm100_d128.cu", "fa_fwd_sm100_local.cu", "fa_fwd_simt.cu", "fa_aux.cu", "fa_api.cu", "encoder_ops.cu", "gemm_sm100.cu", "clf_runtime.cu",
+SOURCES = ["fa_fwd_sm100.cu", "fa_fwd_sm100_d128.cu", "fa_fwd_sm100_local.cu", "fa_fwd_simt.cu", "fa_aux.cu", "fa_api.cu", "encoder_ops.cu", "gemm_sm100.cu", "clf_runtime.cu", "host_cast.cpp",
            # graph layer around the operator: IR, SDPA -> FusedFlashAttention rewriter, GPU executor, C ABI
            os.path.join("graph", "graph_ir.cpp"), os.path.join("graph", "sdpa_rewriter.cpp"),
            os.path.join("graph", "graph_executor.cu"), os.path.join("graph", "graph_capi.cpp")]
@@ -21,7 +21,7 @@ NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
     "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177", "-I", INCLUDE, "-ldl",
 ]
-HEADERS = ["ptx.cuh", "fa_internal.h", os.path.join("graph", "json.hpp"),
+HEADERS = ["ptx.cuh", "fa_internal.h", "host_cast.h", os.path.join("graph", "json.hpp"),
            os.path.join(INCLUDE, "rf_fa.h"), os.path.join(INCLUDE, "rf_graph.h"), os.path.join(INCLUDE, "rf_clf.h"), os.path.join(INCLUDE, "rf_gemm.h"),
            os.path.join(INCLUDE, "routefast_b200", "attention.hpp"), os.path.join(INCLUDE, "routefast_b200", "graph.hpp"),
            os.path.join(INCLUDE, "routefast_b200", "classifiers.hpp")]

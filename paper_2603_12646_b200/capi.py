@@ -20,7 +20,7 @@ EXPORTS = [
     "rf_last_error", "rf_abi_version", "rf_fa_params_init", "rf_fa_validate", "rf_fa_fwd_workspace_bytes",
     "rf_fa_stats_query", "rf_fa_fwd", "rf_fa_plan_create", "rf_fa_plan_launch", "rf_fa_plan_destroy",
     "rf_fa_launch_status", "rf_fa_merge", "rf_fa_rescale_partial", "rf_fa_normalize",
-    "rf_pad_bias_from_mask", "rf_cast_f32_to", "rf_cast_to_f32", "rf_fa_fwd_host", "rf_fa_host_release",
+    "rf_pad_bias_from_mask", "rf_cast_f32_to", "rf_cast_to_f32", "rf_fa_fwd_host", "rf_fa_host_release", "rf_host_round_bf16", "rf_fa_host_transfer_counters",
     "rf_fused_flash_attention_op", "rf_mask_memory_bytes", "rf_fa_memory_bytes", "rf_device_check",
     "rf_rope_qkv", "rf_add_layernorm", "rf_geglu",
     # include/rf_graph.h
@@ -148,6 +148,10 @@ def load(build_if_missing: bool = True):
     lib.rf_device_check.argtypes = [i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
     lib.rf_fa_host_release.argtypes = []
     lib.rf_fa_host_release.restype = None
+    lib.rf_host_round_bf16.argtypes = [C.POINTER(C.c_float), C.POINTER(C.c_uint16), C.c_int64]
+    lib.rf_host_round_bf16.restype = C.c_int
+    lib.rf_fa_host_transfer_counters.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+    lib.rf_fa_host_transfer_counters.restype = None
     lib.rf_clf_config_default.argtypes = [C.POINTER(RfClfConfig)]
     lib.rf_clf_config_default.restype = None
     lib.rf_clf_weight_elems.argtypes = [C.POINTER(RfClfConfig)]
@@ -193,3 +197,10 @@ def new_params() -> RfFaParams:
     p = RfFaParams()
     load().rf_fa_params_init(C.byref(p))
     return p
+
+
+def host_transfer_counters():
+    """(h2d_bytes, d2h_bytes, calls) of the calling thread's rf_fa_fwd_host calls so far (rf_fa_host_transfer_counters)."""
+    a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    load().rf_fa_host_transfer_counters(C.byref(a), C.byref(b), C.byref(c))
+    return int(a.value), int(b.value), int(c.value)

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <chrono>
 #include <cstdlib>
@@ -17,6 +18,7 @@
 
 #include "../../include/rf_fa.h"
 #include "fa_internal.h"
+#include "host_cast.h"
 
 namespace {
 
@@ -119,8 +121,45 @@ struct HostCtx {
     cudaStream_t streams[kHostStreams] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ready = nullptr;
     int n = 0;
+    // host-side cast (host_cast.h): page-locked 16-bit staging, one slot per stream, and the event that says a
+    // slot's upload has been read
+    uint16_t* stage[kHostStreams] = {nullptr, nullptr, nullptr, nullptr};
+    size_t stage_bytes = 0;  // per slot
+    cudaEvent_t uploaded[kHostStreams] = {nullptr, nullptr, nullptr, nullptr};
 };
 thread_local HostCtx g_host_ctx[kMaxDevices];
+
+// Which way large rf_fa_fwd_host calls round their inputs: seconds per byte of the best call seen each way.  The
+// first three eligible calls go through the host cores (the first pays for the pool and the page-locked staging),
+// the next three through the device, after that the faster way wins (ties to the host: fewer bytes on the link)
+// and every 16th call tries the other way again, so a choice made on a noisy start does not stick.
+// RF_FA_HOST_CAST=1 pins the host way, =0 the device way.
+struct HostCastChoice {
+    std::mutex m;
+    double best[2] = {1e30, 1e30};  // [0] device cast, [1] host cast
+    int calls[2] = {0, 0};
+    bool want_host() {
+        static const int pinned = [] {
+            const char* env = std::getenv("RF_FA_HOST_CAST");
+            return env == nullptr ? -1 : (env[0] == '0' ? 0 : 1);
+        }();
+        if (pinned >= 0) return pinned == 1;
+        std::lock_guard<std::mutex> lk(m);
+        if (calls[1] < 3) return true;
+        if (calls[0] < 3) return false;
+        const bool host = best[1] <= best[0];
+        return ((calls[0] + calls[1]) % 16 == 15) ? !host : host;
+    }
+    void record(bool host, double s_per_byte) {
+        std::lock_guard<std::mutex> lk(m);
+        const int i = host ? 1 : 0;
+        ++calls[i];
+        best[i] = std::min(best[i], s_per_byte);
+    }
+};
+HostCastChoice g_cast_choice;
+// bytes rf_fa_fwd_host moved over the link on the calling thread, cumulative (rf_fa_host_transfer_counters)
+thread_local uint64_t g_h2d_total = 0, g_d2h_total = 0, g_host_calls = 0;
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
 bool strides_ok_tma(const int64_t s[3]) { return s[0] > 0 && s[1] > 0 && s[2] > 0 && s[0] % 8 == 0 && s[1] % 8 == 0 && s[2] % 8 == 0; }
@@ -753,13 +792,27 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
     };
     constexpr int kStreams = kHostStreams;
     const size_t nb32 = static_cast<size_t>(n) * sizeof(float);
+    // Q, K, V rounded to bf16 on the host cores, chunk c + 1 under the transfers of chunk c: half the bytes cross the
+    // link (the call is PCIe-bound) and no f32 upload or cast kernel is needed on the device.  Not for f16, small
+    // calls, hosts without spare threads, or while another thread holds the pool; and since how fast the host cores
+    // round depends on the host, large calls try both ways twice and then stay with the faster one (HostCastChoice).
+    const bool cast_candidate = compute_dtype == RF_DTYPE_BF16 && 3 * nb32 >= (16u << 20) && rf::hostcast::threads() > 0;
+    bool cast_pool = cast_candidate && g_cast_choice.want_host() && rf::hostcast::try_acquire();  // this call holds the pool
+    bool cast_in_flight = false;
     const size_t slice_elems = static_cast<size_t>(S) * d;          // one (b, h) slice
     const size_t slice_in_bytes = 3 * slice_elems * sizeof(float);
     int64_t hpc = H;                                                // heads per chunk
     bool per_batch = false;                                         // chunks never cross a batch
     if (static_cast<size_t>(B) * H * slice_in_bytes >= (16u << 20)) {
         per_batch = true;
-        hpc = std::max<int64_t>(1, static_cast<int64_t>(((8u << 20) + slice_in_bytes - 1) / slice_in_bytes));
+        // ~8 MiB of f32 input per chunk (RF_FA_HOST_CHUNK_MB overrides: developer knob)
+        // ~8 MiB of f32 input per chunk, ~4 MiB when the host rounds (shorter pipeline fill and drain; measured)
+        static const long chunk_env = [] {
+            const char* env = std::getenv("RF_FA_HOST_CHUNK_MB");  // developer knob
+            return env != nullptr ? std::atol(env) : 0L;
+        }();
+        const size_t chunk_target = static_cast<size_t>(chunk_env > 0 ? chunk_env : (cast_pool ? 4 : 8)) << 20;
+        hpc = std::max<int64_t>(1, static_cast<int64_t>((chunk_target + slice_in_bytes - 1) / slice_in_bytes));
         hpc = std::max<int64_t>(hpc, (B * H + 63) / 64);            // at most ~64 chunks
         hpc = std::min<int64_t>(hpc, H);
     }
@@ -791,6 +844,10 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
     cudaEvent_t& bias_ready = ctx.ready;
     int rc = RF_OK;
     auto cleanup = [&]() {
+        if (cast_in_flight) rf::hostcast::wait();  // the workers read the caller's tensors
+        cast_in_flight = false;
+        if (cast_pool) rf::hostcast::release();
+        cast_pool = false;
         // work queued on any stream may still read the shared buffers: drain all of them before freeing
         for (int i = 0; i < kStreams; ++i)
             if (streams[i] != nullptr) cudaStreamSynchronize(streams[i]);
@@ -827,6 +884,23 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
         if (streams[i] == nullptr)
             RF_TRY_CUDA(cudaStreamCreateWithFlags(&streams[i], cudaStreamNonBlocking), "cudaStreamCreate");
 
+    if (cast_pool) {
+        const size_t need = 3 * chunk_elems * sizeof(uint16_t);
+        if (ctx.stage_bytes < need) {
+            for (int i = 0; i < kStreams; ++i) {
+                if (ctx.stage[i] != nullptr) cudaFreeHost(ctx.stage[i]);
+                ctx.stage[i] = nullptr;
+            }
+            ctx.stage_bytes = 0;
+            for (int i = 0; i < kStreams; ++i)
+                RF_TRY_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx.stage[i]), need, cudaHostAllocDefault), "cudaHostAlloc");
+            ctx.stage_bytes = need;
+        }
+        for (int i = 0; i < n_streams; ++i)
+            if (ctx.uploaded[i] == nullptr)
+                RF_TRY_CUDA(cudaEventCreateWithFlags(&ctx.uploaded[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+
     // the params of the largest chunk size the workspace of every stream
     p.B = cb;
     p.H = hpc;
@@ -850,6 +924,7 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
         const size_t nb = static_cast<size_t>(B) * S * sizeof(float);
         RF_TRY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bias), nb, streams[0]), "cudaMallocAsync");
         RF_TRY_CUDA(cudaMemcpyAsync(d_bias, pad_bias, nb, cudaMemcpyHostToDevice, streams[0]), "H2D copy");
+        g_h2d_total += nb;
     }
     if (pad_bias != nullptr || d_out_full != nullptr) {  // stream 0 allocated the shared buffers (and uploads the bias)
         RF_TRY_CUDA(cudaEventRecord(bias_ready, streams[0]), "cudaEventRecord");
@@ -865,28 +940,61 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
 
     lap("setup");
     const float* host_in[3] = {q, k, v};
-    for (int64_t c = 0; c < n_chunks; ++c) {
-        const int si = static_cast<int>(c % n_streams);
-        cudaStream_t st = streams[si];
-        const int64_t b0 = per_batch ? c / chunks_per_batch : 0;
+    struct ChunkGeom {
+        int si;
+        int64_t b0, nh;
+        size_t off, ne;
+    };
+    auto geom = [&](int64_t c) {
+        ChunkGeom g;
+        g.si = static_cast<int>(c % n_streams);
+        g.b0 = per_batch ? c / chunks_per_batch : 0;
         const int64_t h0 = per_batch ? (c % chunks_per_batch) * hpc : 0;
-        const int64_t nh = per_batch ? std::min<int64_t>(hpc, H - h0) : H;
-        const size_t off = (static_cast<size_t>(b0) * H + h0) * slice_elems;      // first element of the chunk
-        const size_t ne = static_cast<size_t>(cb) * nh * slice_elems;            // elements per tensor
-        for (int t = 0; t < 3; ++t)
-            RF_TRY_CUDA(cudaMemcpyAsync(d_f32[si] + static_cast<size_t>(t) * ne, host_in[t] + off, ne * sizeof(float),
-                                        cudaMemcpyHostToDevice, st),
-                        "H2D copy");
-        RF_TRY_CUDA(rf::launch_cast_from_f32(d_f32[si], d_qkv[si], static_cast<long long>(3 * ne), compute_dtype, st),
-                    "cast launch");
+        g.nh = per_batch ? std::min<int64_t>(hpc, H - h0) : H;
+        g.off = (static_cast<size_t>(g.b0) * H + h0) * slice_elems;      // first element of the chunk
+        g.ne = static_cast<size_t>(cb) * g.nh * slice_elems;            // elements per tensor
+        return g;
+    };
+    auto start_cast = [&](int64_t c) {
+        const ChunkGeom g = geom(c);
+        const float* src[3] = {host_in[0] + g.off, host_in[1] + g.off, host_in[2] + g.off};
+        rf::hostcast::start(src, ctx.stage[g.si], g.ne);
+        cast_in_flight = true;
+    };
+    if (cast_pool) start_cast(0);
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        const ChunkGeom g = geom(c);
+        const int si = g.si;
+        cudaStream_t st = streams[si];
+        const size_t off = g.off, ne = g.ne;
+        if (cast_pool) {
+            rf::hostcast::wait();
+            cast_in_flight = false;
+            if (c + 1 < n_chunks) {
+                // the next chunk's slot was last uploaded n_streams chunks ago: that copy must have read it
+                if (c + 1 >= n_streams) RF_TRY_CUDA(cudaEventSynchronize(ctx.uploaded[(c + 1) % n_streams]), "cudaEventSynchronize");
+                start_cast(c + 1);
+            }
+            RF_TRY_CUDA(cudaMemcpyAsync(d_qkv[si], ctx.stage[si], 3 * ne * sizeof(uint16_t), cudaMemcpyHostToDevice, st), "H2D copy");
+            g_h2d_total += 3 * ne * sizeof(uint16_t);
+            RF_TRY_CUDA(cudaEventRecord(ctx.uploaded[si], st), "cudaEventRecord");
+        } else {
+            for (int t = 0; t < 3; ++t)
+                RF_TRY_CUDA(cudaMemcpyAsync(d_f32[si] + static_cast<size_t>(t) * ne, host_in[t] + off, ne * sizeof(float),
+                                            cudaMemcpyHostToDevice, st),
+                            "H2D copy");
+            g_h2d_total += 3 * ne * sizeof(float);
+            RF_TRY_CUDA(rf::launch_cast_from_f32(d_f32[si], d_qkv[si], static_cast<long long>(3 * ne), compute_dtype, st),
+                        "cast launch");
+        }
         p.B = cb;
-        p.H = nh;
+        p.H = g.nh;
         p.q = d_qkv[si];
         p.k = d_qkv[si] + ne;
         p.v = d_qkv[si] + 2 * ne;
-        // inputs are already cast: the first staging slab is reused for O (f32)
+        // the f32 staging slab holds O (device cast: its inputs are already cast when the kernel runs)
         p.out = d_out_full != nullptr ? d_out_full + off : d_f32[si];
-        p.pad_bias = d_bias != nullptr ? d_bias + static_cast<size_t>(b0) * S : nullptr;
+        p.pad_bias = d_bias != nullptr ? d_bias + static_cast<size_t>(g.b0) * S : nullptr;
         RF_TRY_RC(rf_fa_fwd(&p, d_ws[si], ws, st));
         if (d_out_full == nullptr)
             RF_TRY_CUDA(cudaMemcpyAsync(out + off, d_f32[si], ne * sizeof(float), cudaMemcpyDeviceToHost, st), "D2H copy");
@@ -899,8 +1007,34 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
     if (d_out_full != nullptr) RF_TRY_CUDA(cudaMemcpy(out, d_out_full, nb32, cudaMemcpyDeviceToHost), "D2H copy");
 #undef RF_TRY_CUDA
 #undef RF_TRY_RC
+    const bool used_host_cast = cast_pool;
+    g_d2h_total += nb32;
+    ++g_host_calls;
     cleanup();
     lap("cleanup");
+    if (cast_candidate)
+        g_cast_choice.record(used_host_cast,
+                             std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count() / static_cast<double>(nb32));
+    return RF_OK;
+}
+
+void rf_fa_host_transfer_counters(uint64_t* h2d_bytes, uint64_t* d2h_bytes, uint64_t* calls) {
+    if (h2d_bytes != nullptr) *h2d_bytes = g_h2d_total;
+    if (d2h_bytes != nullptr) *d2h_bytes = g_d2h_total;
+    if (calls != nullptr) *calls = g_host_calls;
+}
+
+int rf_host_round_bf16(const float* src, uint16_t* dst, int64_t n) {
+    if (n < 0 || (n > 0 && (src == nullptr || dst == nullptr))) return fail(RF_ERR_ARG, "null pointer or negative count");
+    if (n == 0) return RF_OK;
+    if (n >= (1 << 16) && rf::hostcast::try_acquire()) {
+        const float* srcs[3] = {src, nullptr, nullptr};
+        rf::hostcast::start(srcs, dst, static_cast<size_t>(n), 1);
+        rf::hostcast::wait();
+        rf::hostcast::release();
+    } else {
+        rf::hostcast::round_bf16_serial(src, dst, static_cast<size_t>(n));
+    }
     return RF_OK;
 }
 
@@ -908,7 +1042,7 @@ void rf_fa_host_release(void) {
     for (int dev = 0; dev < kMaxDevices; ++dev) {
         HostCtx& ctx = g_host_ctx[dev];
         bool any = ctx.ready != nullptr;
-        for (int i = 0; i < kHostStreams; ++i) any = any || ctx.streams[i] != nullptr;
+        for (int i = 0; i < kHostStreams; ++i) any = any || ctx.streams[i] != nullptr || ctx.stage[i] != nullptr;
         if (!any) continue;
         int cur = 0;
         cudaGetDevice(&cur);
@@ -923,8 +1057,16 @@ void rf_fa_host_release(void) {
             cudaEventDestroy(ctx.ready);
             ctx.ready = nullptr;
         }
+        for (int i = 0; i < kHostStreams; ++i) {
+            if (ctx.stage[i] != nullptr) cudaFreeHost(ctx.stage[i]);
+            ctx.stage[i] = nullptr;
+            if (ctx.uploaded[i] != nullptr) cudaEventDestroy(ctx.uploaded[i]);
+            ctx.uploaded[i] = nullptr;
+        }
+        ctx.stage_bytes = 0;
         cudaSetDevice(cur);
     }
+    rf::hostcast::shutdown();
 }
 
 int rf_fused_flash_attention_op(const float* const* inputs, const int64_t* const* input_dims,

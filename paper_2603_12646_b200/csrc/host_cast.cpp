@@ -1,0 +1,202 @@
+// host_cast.cpp -- see host_cast.h.  Plain C++ (no CUDA): a fork-join pool with one job in flight.
+#include "host_cast.h"
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace rf {
+namespace hostcast {
+namespace {
+
+// f32 -> bf16, round to nearest even; NaN keeps its sign and becomes quiet (what __float2bfloat16_rn gives)
+inline uint16_t bf16_rne(uint32_t x) {
+    const uint32_t rounded = x + 0x7fffu + ((x >> 16) & 1u);
+    const uint32_t nan = x | 0x00400000u;
+    return static_cast<uint16_t>((((x & 0x7fffffffu) > 0x7f800000u) ? nan : rounded) >> 16);
+}
+
+void cast_range_generic(const float* src, uint16_t* dst, size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t x;
+        std::memcpy(&x, src + i, 4);
+        dst[i] = bf16_rne(x);
+    }
+}
+#if defined(__x86_64__) && defined(__GNUC__)
+// same loop, auto-vectorised for AVX2 (chosen at run time; the library itself is built for baseline x86-64)
+__attribute__((target("avx2"))) void cast_range_avx2(const float* src, uint16_t* dst, size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t x;
+        std::memcpy(&x, src + i, 4);
+        dst[i] = bf16_rne(x);
+    }
+}
+#endif
+
+using CastFn = void (*)(const float*, uint16_t*, size_t);
+CastFn pick_cast() {
+#if defined(__x86_64__) && defined(__GNUC__)
+    if (__builtin_cpu_supports("avx2")) return cast_range_avx2;
+#endif
+    return cast_range_generic;
+}
+
+inline void cpu_relax() {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+}
+
+// Jobs of one call arrive every ~0.2 ms; a futex wake-up of fifteen sleeping workers costs about as much as the job
+// itself.  So a worker that ran out of work polls the job counter for a while (kSpinUs) before it goes to sleep on the
+// condition variable, and the thread that waits for a job polls the completion counter.
+constexpr int kSpinUs = 400;
+
+struct Pool {
+    std::mutex m;
+    std::condition_variable cv_work;
+    std::vector<std::thread> workers;
+    const float* src[3] = {nullptr, nullptr, nullptr};
+    uint16_t* dst = nullptr;
+    size_t ne = 0;
+    int arrays = 3;
+    std::atomic<uint64_t> posted{0};  // jobs posted so far (release: the fields above are written first)
+    std::atomic<int> remaining{0};    // workers still busy with the current job
+    std::atomic<bool> stop{false};
+    int sleepers = 0;                 // workers blocked on cv_work (under m)
+    CastFn fn = nullptr;
+
+    void worker(int index, int count) {
+        uint64_t seen = 0;
+        for (;;) {
+            // poll, then sleep
+            const auto t0 = std::chrono::steady_clock::now();
+            while (posted.load(std::memory_order_acquire) == seen && !stop.load(std::memory_order_relaxed)) {
+                for (int i = 0; i < 64; ++i) cpu_relax();
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(kSpinUs)) {
+                    std::unique_lock<std::mutex> lk(m);
+                    ++sleepers;
+                    cv_work.wait(lk, [&] { return stop.load(std::memory_order_relaxed) || posted.load(std::memory_order_acquire) != seen; });
+                    --sleepers;
+                    break;
+                }
+            }
+            if (stop.load(std::memory_order_relaxed)) return;
+            seen = posted.load(std::memory_order_acquire);
+            const float* s[3] = {src[0], src[1], src[2]};
+            uint16_t* d = dst;
+            const size_t n = ne;
+            const int na = arrays;
+            // this worker's slice of each tensor (64-element granules: whole cache lines of output)
+            const size_t granules = (n + 63) / 64;
+            const size_t g0 = granules * index / count, g1 = granules * (index + 1) / count;
+            const size_t e0 = std::min(n, g0 * 64), e1 = std::min(n, g1 * 64);
+            if (e1 > e0)
+                for (int t = 0; t < na; ++t) fn(s[t] + e0, d + static_cast<size_t>(t) * n + e0, e1 - e0);
+            remaining.fetch_sub(1, std::memory_order_acq_rel);
+        }
+    }
+    void ensure_started(int count) {
+        if (!workers.empty()) return;
+        fn = pick_cast();
+        stop.store(false);
+        for (int i = 0; i < count; ++i) workers.emplace_back([this, i, count] { worker(i, count); });
+    }
+    void join_all() {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            stop.store(true);
+        }
+        cv_work.notify_all();
+        for (auto& t : workers) t.join();
+        workers.clear();
+        posted.store(0);
+        remaining.store(0);
+    }
+};
+
+Pool& pool() {
+    static Pool* p = new Pool();  // never destroyed: worker threads may outlive static destruction order otherwise
+    return *p;
+}
+std::atomic<bool> g_busy{false};
+
+int configured_threads() {
+    static const int n = [] {
+        const char* off = std::getenv("RF_FA_HOST_CAST");
+        if (off != nullptr && off[0] == '0') return 0;
+        int hw = static_cast<int>(std::thread::hardware_concurrency());
+        if (const char* lw = std::getenv("LOCAL_WORLD_SIZE")) {  // one process per GPU: share the cores
+            const int ranks = std::atoi(lw);
+            if (ranks > 1) hw /= ranks;
+        }
+        int t = std::min(16, hw - 1);  // leave a core to the thread that drives the copies
+        if (const char* env = std::getenv("RF_FA_HOST_CAST_THREADS")) t = std::atoi(env);
+        return t < 2 ? 0 : std::min(t, 64);
+    }();
+    return n;
+}
+
+}  // namespace
+
+int threads() { return configured_threads(); }
+
+bool try_acquire() {
+    if (configured_threads() == 0) return false;
+    bool expected = false;
+    return g_busy.compare_exchange_strong(expected, true, std::memory_order_acq_rel);
+}
+
+void release() { g_busy.store(false, std::memory_order_release); }
+
+void start(const float* const src[3], uint16_t* dst, size_t ne, int arrays) {
+    Pool& p = pool();
+    const int count = configured_threads();
+    p.ensure_started(count);  // (one caller at a time: try_acquire)
+    p.src[0] = src[0]; p.src[1] = arrays > 1 ? src[1] : nullptr; p.src[2] = arrays > 2 ? src[2] : nullptr;
+    p.dst = dst;
+    p.ne = ne;
+    p.arrays = arrays;
+    p.remaining.store(count, std::memory_order_relaxed);
+    p.posted.fetch_add(1, std::memory_order_release);
+    bool wake;
+    {
+        std::lock_guard<std::mutex> lk(p.m);
+        wake = p.sleepers > 0;
+    }
+    if (wake) p.cv_work.notify_all();
+}
+
+void wait() {
+    Pool& p = pool();
+    int spins = 0;
+    while (p.remaining.load(std::memory_order_acquire) != 0) {
+        cpu_relax();
+        if (++spins > (1 << 14)) {
+            std::this_thread::yield();
+            spins = 0;
+        }
+    }
+}
+
+void round_bf16_serial(const float* src, uint16_t* dst, size_t n) { pick_cast()(src, dst, n); }
+
+void shutdown() {
+    if (!try_acquire()) {
+        if (configured_threads() == 0) return;
+        return;  // another thread is mid-call: leave its pool alone
+    }
+    Pool& p = pool();
+    if (!p.workers.empty()) p.join_all();
+    release();
+}
+
+}  // namespace hostcast
+}  // namespace rf

@@ -195,3 +195,33 @@ def test_classifier_session_fails_loudly_without_gpu(lib):
         blob = (C.c_float * n)()
         assert lib.rf_clf_create(C.byref(c), blob, n, 0, C.byref(h)) == capi.RF_ERR_CUDA
         assert not h.value
+
+
+def test_host_rounding_is_round_to_nearest_even_bit_for_bit(lib):
+    """rf_host_round_bf16 (the rounding rf_fa_fwd_host applies to Q, K, V on the host cores before they cross the link):
+    identical to torch's f32 -> bf16 conversion, which is what the device cast gives -- ties, subnormals, infinities,
+    NaN (stays NaN), negative zero; through the thread pool (large n) and on the calling thread (small n)."""
+    import torch
+    from paper_2603_12646_b200 import capi
+    rng = np.random.default_rng(5)
+    special = np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 1e-40, -1e-40, 3.3895314e38, 65504.0, 1.00390625,
+                        1.01171875, 1.005859375, 0.99609375], np.float32)
+    ties = (np.arange(1, 4097, dtype=np.uint32) << 15).view(np.float32)   # every pattern that ends in ...1000 0000 0000 0000 or 0
+    for n in (special.size + ties.size + 1000, 3 * 12 * 4096 * 64 + 7):
+        x = rng.standard_normal(n).astype(np.float32) * np.float32(10.0) ** rng.integers(-6, 6, n).astype(np.float32)
+        x[:special.size] = special
+        x[special.size:special.size + ties.size] = ties
+        bits = rng.integers(0, 2 ** 32, 4096, dtype=np.uint64).astype(np.uint32).view(np.float32)  # raw bit patterns
+        x[-bits.size:] = bits
+        out = np.empty(n, np.uint16)
+        rc = lib.rf_host_round_bf16(x.ctypes.data_as(C.POINTER(C.c_float)), out.ctypes.data_as(C.POINTER(C.c_uint16)), n)
+        assert rc == capi.RF_OK
+        want = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+        nan = np.isnan(x)
+        assert np.array_equal(out[~nan], want[~nan])
+        assert np.all((out[nan] & 0x7fff) > 0x7f80)          # still NaN (payloads may differ between converters)
+    lib.rf_fa_host_release()                                  # joins the pool; a later call restarts it
+    x = np.linspace(-3, 3, 1 << 17, dtype=np.float32)
+    out = np.empty(x.size, np.uint16)
+    assert lib.rf_host_round_bf16(x.ctypes.data_as(C.POINTER(C.c_float)), out.ctypes.data_as(C.POINTER(C.c_uint16)), x.size) == capi.RF_OK
+    assert np.array_equal(out, torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16))

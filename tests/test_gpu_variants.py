@@ -54,3 +54,53 @@ def test_kernel_selector_variants(env):
     res = subprocess.run([sys.executable, "-c", SNIPPET], cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
     print(env, res.stdout[-500:], res.stderr[-1500:])
     assert res.returncode == 0 and "variant ok" in res.stdout
+
+
+HOST_SNIPPET = r"""
+import hashlib, os, sys
+import numpy as np
+sys.path.insert(0, os.getcwd())
+import paper_2603_12646_b200 as P
+from paper_2603_12646_b200 import capi
+rng = np.random.default_rng(17)
+digest = hashlib.sha256()
+for (B, H, S, wl, wr, pad) in ((1, 12, 4096, -1, -1, False), (2, 6, 2048, 63, 64, True), (1, 12, 8192, -1, -1, False)):
+    q, k, v = [rng.standard_normal((B, H, S, 64)).astype(np.float32) for _ in range(3)]   # NOT pre-rounded to bf16
+    pb = None
+    if pad:
+        pb = np.zeros((B, 1, 1, S), np.float32)
+        pb[-1, 0, 0, S - 333:] = -65504.0
+    x0 = capi.host_transfer_counters()
+    for _ in range(8):                      # default mode: three host-rounded calls, three device-rounded, then the faster
+        out = P.flash_attention(q, k, v, P.AttentionSpec(0.0, wl, wr, pb), device=0)
+        assert np.isfinite(out).all()
+        digest.update(out.tobytes())
+    x1 = capi.host_transfer_counters()
+    assert x1[2] - x0[2] == 8 and x1[1] - x0[1] == 8 * out.nbytes
+    per_call = (x1[0] - x0[0]) / 8
+    print("h2d per call / f32 input bytes: %.2f" % (per_call / (3 * q.nbytes)))
+print("host digest", digest.hexdigest())
+"""
+
+
+def _host_run(env):
+    e = dict(os.environ)
+    e.update(env)
+    res = subprocess.run([sys.executable, "-c", HOST_SNIPPET], cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    print(env, res.stdout[-800:], res.stderr[-1500:])
+    assert res.returncode == 0 and "host digest" in res.stdout
+    return res.stdout
+
+
+def test_host_entry_rounds_on_host_or_device_with_the_same_bits():
+    """rf_fa_fwd_host rounds Q, K, V to bf16 either on a pool of host threads (half the bytes on the link) or on the
+    device, whichever it measures to be faster on this host; every call of either kind gives the same output bits (the
+    two roundings are the same function), and the transfer counters say how many bytes actually crossed."""
+    outs = {name: _host_run(env) for name, env in (("device", {"RF_FA_HOST_CAST": "0"}), ("host", {"RF_FA_HOST_CAST": "1"}),
+                                                   ("auto", {}))}
+    digests = {name: [ln for ln in o.splitlines() if ln.startswith("host digest")][0] for name, o in outs.items()}
+    assert digests["device"] == digests["host"] == digests["auto"]
+    ratios = {name: [float(ln.split(":")[1]) for ln in o.splitlines() if ln.startswith("h2d per call")] for name, o in outs.items()}
+    assert all(abs(r - 1.0) < 0.02 for r in ratios["device"])            # f32 over the link (+ the pad bias)
+    # large calls go as bf16 (the 2048-token call is below the 16 MiB threshold only if 3 * 4 * B*H*S*64 < 16 MiB)
+    assert abs(ratios["host"][0] - 0.5) < 0.02 and abs(ratios["host"][2] - 0.5) < 0.02
