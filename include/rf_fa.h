@@ -209,7 +209,7 @@ int rf_fa_fwd_host(const float* q, const float* k, const float* v, float* out, i
 void rf_fa_host_release(void);
 
 /* The rounding rf_fa_fwd_host applies to Q, K, V before they cross the link: f32 -> bf16, round to nearest even (NaN
- * stays NaN), on a small pool of host threads (RF_FA_HOST_CAST_THREADS, default min(16, cores - 1); RF_FA_HOST_CAST=0
+ * stays NaN), on a small pool of host threads (RF_FA_HOST_CAST_THREADS, default min(16, cores - 2); RF_FA_HOST_CAST=0
  * keeps the rounding on the device).  Bit-identical to the device cast.  No CUDA call; exposed for tests and for
  * callers that keep their own 16-bit copies.  The reference has no counterpart (its Tensor is f32 only,
  * proj/core/include/routefast/tensor.hpp). */

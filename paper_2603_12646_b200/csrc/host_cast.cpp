@@ -40,9 +40,25 @@ __attribute__((target("avx2"))) void cast_range_avx2(const float* src, uint16_t*
 }
 #endif
 
+#if defined(__x86_64__) && defined(__GNUC__)
+// ... and for AVX-512 (16 lanes, vpmovdw packs).  The integer formulation is kept on purpose: AVX512-BF16's
+// vcvtneps2bf16 flushes subnormals, the device cast does not.
+__attribute__((target("avx512f,avx512bw,avx512vl,prefer-vector-width=512"))) void cast_range_avx512(const float* src, uint16_t* dst,
+                                                                                                    size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t x;
+        std::memcpy(&x, src + i, 4);
+        dst[i] = bf16_rne(x);
+    }
+}
+#endif
+
 using CastFn = void (*)(const float*, uint16_t*, size_t);
 CastFn pick_cast() {
 #if defined(__x86_64__) && defined(__GNUC__)
+    const char* isa = std::getenv("RF_FA_HOST_CAST_ISA");  // developer knob: "avx2" keeps the 256-bit path
+    const bool allow512 = isa == nullptr || std::strcmp(isa, "avx2") != 0;
+    if (allow512 && __builtin_cpu_supports("avx512bw") && __builtin_cpu_supports("avx512vl")) return cast_range_avx512;
     if (__builtin_cpu_supports("avx2")) return cast_range_avx2;
 #endif
     return cast_range_generic;
@@ -137,7 +153,7 @@ int configured_threads() {
             const int ranks = std::atoi(lw);
             if (ranks > 1) hw /= ranks;
         }
-        int t = std::min(16, hw - 1);  // leave a core to the thread that drives the copies
+        int t = std::min(16, hw - 2);  // leave cores to the thread that drives the copies and to the driver's own threads
         if (const char* env = std::getenv("RF_FA_HOST_CAST_THREADS")) t = std::atoi(env);
         return t < 2 ? 0 : std::min(t, 64);
     }();

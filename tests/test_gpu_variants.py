@@ -104,3 +104,12 @@ def test_host_entry_rounds_on_host_or_device_with_the_same_bits():
     assert all(abs(r - 1.0) < 0.02 for r in ratios["device"])            # f32 over the link (+ the pad bias)
     # large calls go as bf16 (the 2048-token call is below the 16 MiB threshold only if 3 * 4 * B*H*S*64 < 16 MiB)
     assert abs(ratios["host"][0] - 0.5) < 0.02 and abs(ratios["host"][2] - 0.5) < 0.02
+
+
+def test_host_rounding_on_the_gpu_box_cpu():
+    """The host rounding picks its widest vector path at run time (AVX-512 on the GPU boxes, AVX2 on the CPU-only dev
+    container): run the bit-for-bit check of tests/test_capi_cpu.py on this machine's path too."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import test_capi_cpu as T
+    from paper_2603_12646_b200 import capi
+    T.test_host_rounding_is_round_to_nearest_even_bit_for_bit(capi.load())
