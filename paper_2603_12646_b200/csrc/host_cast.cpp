@@ -73,23 +73,53 @@ inline void cpu_relax() {
 // Jobs of one call arrive every ~0.2 ms; a futex wake-up of fifteen sleeping workers costs about as much as the job
 // itself.  So a worker that ran out of work polls the job counter for a while (kSpinUs) before it goes to sleep on the
 // condition variable, and the thread that waits for a job polls the completion counter.
+//
+// Work is handed out in blocks through an atomic counter, and the posting thread takes blocks too while it waits:
+// a worker that the hypervisor parks for a millisecond then costs one block, not 1/T of the job (the bench boxes are
+// VMs; with fixed shares the same call took 1.5 or 2.1 ms depending on the minute).  A job is complete when all its
+// blocks are, not when every worker has looked at it; the two job slots alternate, and a slot is only rewritten once
+// no worker is inside it (active == 0) -- a latecomer finds the slot's generation changed and leaves.
 constexpr int kSpinUs = 400;
+constexpr size_t kBlockElems = 8192;  // per tensor: 32 KiB read, 16 KiB written
+
+struct Job {
+    const float* src[3] = {nullptr, nullptr, nullptr};
+    uint16_t* dst = nullptr;
+    size_t ne = 0, n_blocks = 0;
+    int arrays = 3;
+    std::atomic<uint64_t> gen{0};      // sequence number of the job in this slot, 0 while it is being rewritten
+    std::atomic<size_t> next{0};       // next block to hand out
+    std::atomic<size_t> done{0};       // blocks finished
+    std::atomic<int> active{0};        // threads inside the slot
+};
 
 struct Pool {
     std::mutex m;
     std::condition_variable cv_work;
     std::vector<std::thread> workers;
-    const float* src[3] = {nullptr, nullptr, nullptr};
-    uint16_t* dst = nullptr;
-    size_t ne = 0;
-    int arrays = 3;
-    std::atomic<uint64_t> posted{0};  // jobs posted so far (release: the fields above are written first)
-    std::atomic<int> remaining{0};    // workers still busy with the current job
+    Job jobs[2];
+    std::atomic<uint64_t> posted{0};  // sequence number of the newest job
     std::atomic<bool> stop{false};
     int sleepers = 0;                 // workers blocked on cv_work (under m)
     CastFn fn = nullptr;
 
-    void worker(int index, int count) {
+    // takes blocks of job `seq` until none is left; returns at once if the slot holds another job by now
+    void help(uint64_t seq) {
+        Job& j = jobs[seq & 1];
+        j.active.fetch_add(1, std::memory_order_acq_rel);
+        if (j.gen.load(std::memory_order_acquire) == seq) {
+            for (;;) {
+                const size_t b = j.next.fetch_add(1, std::memory_order_relaxed);
+                if (b >= j.n_blocks) break;
+                const size_t e0 = b * kBlockElems, e1 = std::min(j.ne, e0 + kBlockElems);
+                for (int t = 0; t < j.arrays; ++t) fn(j.src[t] + e0, j.dst + static_cast<size_t>(t) * j.ne + e0, e1 - e0);
+                j.done.fetch_add(1, std::memory_order_release);
+            }
+        }
+        j.active.fetch_sub(1, std::memory_order_release);
+    }
+
+    void worker() {
         uint64_t seen = 0;
         for (;;) {
             // poll, then sleep
@@ -106,24 +136,14 @@ struct Pool {
             }
             if (stop.load(std::memory_order_relaxed)) return;
             seen = posted.load(std::memory_order_acquire);
-            const float* s[3] = {src[0], src[1], src[2]};
-            uint16_t* d = dst;
-            const size_t n = ne;
-            const int na = arrays;
-            // this worker's slice of each tensor (64-element granules: whole cache lines of output)
-            const size_t granules = (n + 63) / 64;
-            const size_t g0 = granules * index / count, g1 = granules * (index + 1) / count;
-            const size_t e0 = std::min(n, g0 * 64), e1 = std::min(n, g1 * 64);
-            if (e1 > e0)
-                for (int t = 0; t < na; ++t) fn(s[t] + e0, d + static_cast<size_t>(t) * n + e0, e1 - e0);
-            remaining.fetch_sub(1, std::memory_order_acq_rel);
+            help(seen);
         }
     }
     void ensure_started(int count) {
         if (!workers.empty()) return;
         fn = pick_cast();
         stop.store(false);
-        for (int i = 0; i < count; ++i) workers.emplace_back([this, i, count] { worker(i, count); });
+        for (int i = 0; i < count; ++i) workers.emplace_back([this] { worker(); });
     }
     void join_all() {
         {
@@ -133,8 +153,7 @@ struct Pool {
         cv_work.notify_all();
         for (auto& t : workers) t.join();
         workers.clear();
-        posted.store(0);
-        remaining.store(0);
+        // (sequence numbers keep counting: a restarted pool's workers start from seen = 0 and simply find the newest job)
     }
 };
 
@@ -174,14 +193,20 @@ void release() { g_busy.store(false, std::memory_order_release); }
 
 void start(const float* const src[3], uint16_t* dst, size_t ne, int arrays) {
     Pool& p = pool();
-    const int count = configured_threads();
-    p.ensure_started(count);  // (one caller at a time: try_acquire)
-    p.src[0] = src[0]; p.src[1] = arrays > 1 ? src[1] : nullptr; p.src[2] = arrays > 2 ? src[2] : nullptr;
-    p.dst = dst;
-    p.ne = ne;
-    p.arrays = arrays;
-    p.remaining.store(count, std::memory_order_relaxed);
-    p.posted.fetch_add(1, std::memory_order_release);
+    p.ensure_started(configured_threads());  // (one caller at a time: try_acquire)
+    const uint64_t seq = p.posted.load(std::memory_order_relaxed) + 1;
+    Job& j = p.jobs[seq & 1];
+    j.gen.store(0, std::memory_order_release);                          // nobody may enter the slot any more ...
+    while (j.active.load(std::memory_order_acquire) != 0) cpu_relax();  // ... and whoever is inside leaves (its job is long done)
+    j.src[0] = src[0]; j.src[1] = arrays > 1 ? src[1] : nullptr; j.src[2] = arrays > 2 ? src[2] : nullptr;
+    j.dst = dst;
+    j.ne = ne;
+    j.arrays = arrays;
+    j.n_blocks = (ne + kBlockElems - 1) / kBlockElems;
+    j.next.store(0, std::memory_order_relaxed);
+    j.done.store(0, std::memory_order_relaxed);
+    j.gen.store(seq, std::memory_order_release);
+    p.posted.store(seq, std::memory_order_release);
     bool wake;
     {
         std::lock_guard<std::mutex> lk(p.m);
@@ -192,8 +217,12 @@ void start(const float* const src[3], uint16_t* dst, size_t ne, int arrays) {
 
 void wait() {
     Pool& p = pool();
+    const uint64_t seq = p.posted.load(std::memory_order_acquire);
+    if (seq == 0) return;
+    p.help(seq);  // the waiting thread takes blocks too
+    Job& j = p.jobs[seq & 1];
     int spins = 0;
-    while (p.remaining.load(std::memory_order_acquire) != 0) {
+    while (j.done.load(std::memory_order_acquire) != j.n_blocks) {
         cpu_relax();
         if (++spins > (1 << 14)) {
             std::this_thread::yield();
