@@ -9,12 +9,20 @@
 #include "ptx.cuh"
 using namespace rfptx;
 
-enum Mode { kLd32 = 0, kLd16, kSt32, kSt16, kLd32Mufu, kLd32St16, kNumModes };
+enum Mode { kLd32 = 0, kLd16, kSt32, kSt16, kLd32Mufu, kLd32St16, kTryWait, kNumModes };
 
 template <int kMode>
 __global__ void __launch_bounds__(512, 1) probe(int iters, long long* clk_out, uint32_t* sink) {
     __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t mbar;
     const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&mbar), 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) mbar_arrive(smem_u32(&mbar));  // phase 0 completes: a wait for parity 0 is satisfied from now on
+    __syncthreads();
     if (warp == 0) {
         tmem_alloc(smem_u32(&tmem_slot), 512);
         tmem_relinquish();
@@ -58,6 +66,9 @@ __global__ void __launch_bounds__(512, 1) probe(int iters, long long* clk_out, u
         } else if (kMode == kSt32) {
             tmem_st32(base + col, r);
             tc_wait_st();
+        } else if (kMode == kTryWait) {
+            // a phase check of a barrier that completed long ago, result consumed (dependent chain: latency)
+            r[0] += mbar_try_wait(smem_u32(&mbar), 0);
         } else if (kMode == kSt16) {
             tmem_st16(base + col, reinterpret_cast<uint32_t(&)[16]>(r[0]));
             tc_wait_st();
@@ -108,5 +119,6 @@ int main() {
     run<kSt16>("tcgen05.st 32x32b.x16 (2 KiB per warp)", 2048);
     run<kLd32Mufu>("tcgen05.ld x32 + 24 MUFU.EX2 (ld bytes counted)", 4096);
     run<kLd32St16>("tcgen05.ld x32 + tcgen05.st x16 (ld bytes counted)", 4096);
+    run<kTryWait>("mbarrier.try_wait on a completed phase (clk_per_round = latency per check; bytes n/a)", 0);
     return 0;
 }
