@@ -100,6 +100,12 @@ constexpr bool kPingPong = RF_FA_PINGPONG != 0;
 #endif
 // Developer build only (-DRF_FA_MMAONLY=1): the softmax warps skip their work (results are garbage);
 // what remains is the TMA + UMMA pipeline, i.e. the tensor-pipe floor of this tiling.
+// Developer build only (-DRF_FA_NOEXP=1, results are garbage): the softmax warps keep their TMEM traffic (S loads, P
+// stores), barriers and the scale / sum / pack instructions but take no exponential -- what the kernel would cost
+// if exponentials were free (171 us at 8K against 124 us for RF_FA_MMAONLY and 207 us shipped).
+#ifndef RF_FA_NOEXP
+#define RF_FA_NOEXP 0
+#endif
 #ifndef RF_FA_MMAONLY
 #define RF_FA_MMAONLY 0
 #endif
@@ -841,7 +847,9 @@ fa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                                                  __uint_as_float(su[cb * 32 + 2 * u + 1])),
                                              mul2, negm2),
                                       p0, p1);
-                                if (kEmu && (u % (kEmuEvery > 0 ? kEmuEvery : 1)) == (kEmuEvery > 0 ? kEmuEvery - 1 : 0)) {
+                                if (RF_FA_NOEXP) {
+                                    // (developer build: no exponential)
+                                } else if (kEmu && (u % (kEmuEvery > 0 ? kEmuEvery : 1)) == (kEmuEvery > 0 ? kEmuEvery - 1 : 0)) {
                                     exp2_poly2(p0, p1);
                                 } else {
                                     p0 = ex2(p0);
