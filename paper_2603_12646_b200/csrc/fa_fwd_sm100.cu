@@ -73,7 +73,7 @@ constexpr int kThreads = 640;        // 5 warpgroups: 4 softmax + 1 (producer, M
 constexpr int kHalfN = kBlockN / 2;  // key columns per softmax thread
 constexpr int kRegsSoftmax = 112;
 #ifndef RF_FA_EMU_EVERY
-#define RF_FA_EMU_EVERY 4
+#define RF_FA_EMU_EVERY 5  // 3 of a block's 16 pairs; 4 (a quarter) is 0.8 % slower at 8K, 3 and 6 slower still (same-box A/B)
 #endif
 constexpr int kEmuEvery = RF_FA_EMU_EVERY;  // every n-th element pair uses the FMA-pipe exp2 (0 = MUFU only)
 constexpr int kRegsOther = 32;       // 128*32 + 512*112 == 640*96: the CTA register pool balances exactly
