@@ -325,7 +325,14 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         // dense batches, where the gain is L2 locality, at most 10 % for padded ones, where lengths differ)
         const int64_t rounds = (pl.total_pairs + sms - 1) / sms;
         const double waste = static_cast<double>(rounds * sms) / static_cast<double>(pl.total_pairs) - 1.0;
-        const bool want2 = p->B > 1 && pl.total_pairs >= 4ll * sms && waste <= (p->pad_bias != nullptr ? 0.10 : 0.05);
+        // A single long sequence also goes round-robin once its K/V no longer sit in the L2 next to each other: with
+        // contiguous slices all H heads are in flight at once (S = 32K: 100 MB of K/V on a 126 MB L2), round-robin
+        // keeps the 148 CTAs on one or two heads (S = 32K: 3.24 vs 3.32-3.39 ms although its last round idles 6 %;
+        // at 16K, 50 MB, contiguous slices stay ahead: 0.79 vs 0.90 ms).
+        const double kv_bytes = 4.0 * static_cast<double>(p->B) * p->H * p->S * p->d;  // K and V, 16-bit
+        const bool kv_beyond_l2 = kv_bytes > 64.0e6;
+        const bool want2 = (p->B > 1 || kv_beyond_l2) && pl.total_pairs >= 4ll * sms &&
+                           waste <= ((p->pad_bias != nullptr || (p->B == 1 && kv_beyond_l2)) ? 0.10 : 0.05);
         if (forced == 2 || (forced == 0 && want2)) {
             pl.sched_mode = 2;
             pl.part_bytes = 0;

@@ -103,15 +103,17 @@ def test_workspace_is_linear_in_S(lib):
     assert sizes[16384] - sizes[8192] <= 8192 * per_key + 1024 and sizes[32768] - sizes[16384] <= 16384 * per_key + 1024
     assert sizes[32768] < 11 * 1024 * 1024
     # dense global attention over more query-tile pairs than SMs runs the persistent balanced schedule: its
-    # split-pair workspace is a constant (per-SM); only the key norms grow, linearly
+    # split-pair workspace is a constant (per-SM); only the key norms grow, linearly.  A single sequence whose K/V
+    # outgrow the L2 (32K tokens: 100 MB) is dealt round-robin as whole pairs instead: no split-pair block at all.
     p.pad_bias = None
     dense = []
-    for S in (8192, 32768):
+    for S in (8192, 16384, 32768):
         p.S = S
         assert lib.rf_fa_fwd_workspace_bytes(C.byref(p), C.byref(n)) == capi.RF_OK
         dense.append(n.value)
     assert 0 < dense[0] < dense[1] < 11 * 1024 * 1024
-    assert dense[1] - dense[0] <= (32768 - 8192) * (4 * 12 / 128.0) + 1024
+    assert dense[1] - dense[0] <= (16384 - 8192) * (4 * 12 / 128.0) + 1024
+    assert 0 < dense[2] < 64 * 1024                      # status block + flag block + 12 KiB of key norms
     p.S = 512  # 24 pairs fit one wave: one pair per CTA, nothing but the 256-byte launch-status block
     assert lib.rf_fa_fwd_workspace_bytes(C.byref(p), C.byref(n)) == capi.RF_OK and n.value == 256
 
