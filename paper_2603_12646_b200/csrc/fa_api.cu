@@ -292,22 +292,13 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         const char* env = std::getenv("RF_FA_SKIP_MAX");
         return env == nullptr || env[0] != '0';
     }();
-    if (p->d == 128) {
-        // head_dim 128: whole pairs only -- one per CTA while they fit a wave (and for split-KV partials),
-        // else dealt round-robin over a persistent grid
-        pl.d128 = true;
-        if (!r.partial && pl.total_pairs > sms) {
-            pl.sched_mode = 2;
-            pl.grid = sms;
-        }
-        return pl;
-    }
-    if (skip_max_enabled && p->S >= 1024)
+    if (p->d == 128) pl.d128 = true;  // own kernel (fa_fwd_sm100_d128.cu): same schedules, no row-max skip
+    if (skip_max_enabled && p->S >= 1024 && !pl.d128)
         pl.kmax_bytes = align_up(static_cast<size_t>(p->B) * p->H * n_kv_tiles(p->S) * sizeof(float), 256);
     if (!r.partial && pl.total_pairs > sms) {
         pl.sched_mode = 1;
         pl.grid = sms;
-        pl.part_bytes = align_up(rf::fa_fwd_sm100_partial_bytes(pl.grid), 256);
+        pl.part_bytes = align_up(rf::fa_fwd_sm100_partial_bytes(pl.grid, pl.d128 ? 128 : 64), 256);
         // Batches with many pairs per SM are dealt round-robin as whole pairs instead (mode 2), for two reasons.
         // (i) CTAs that run at the same time work on neighbouring pairs, i.e. on a handful of heads whose K/V
         // stay in L2; contiguous slices put the 148 CTAs on as many different heads at once, and with B*H*S*256 B
@@ -493,7 +484,7 @@ int build_launch(const rf_fa_params* p, void* workspace, size_t workspace_bytes,
     f.pairs_per_head = static_cast<int>(pl.pairs_per_head);
     f.tiles_per_pair = static_cast<int>(pl.tiles_per_pair);
     if (pl.sched_mode == 1) {
-        rf::fa_fwd_sm100_partial_carve(ws + pl.bias_bytes + pl.flag_bytes_bias, sched_flags, pl.grid, &f);
+        rf::fa_fwd_sm100_partial_carve(ws + pl.bias_bytes + pl.flag_bytes_bias, sched_flags, pl.grid, pl.d128 ? 128 : 64, &f);
         L->memset_ptr = sched_flags;
         L->memset_bytes = rf::fa_fwd_sm100_flag_bytes(pl.grid);
     }

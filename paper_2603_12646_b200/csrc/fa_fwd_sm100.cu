@@ -1072,9 +1072,9 @@ size_t fa_fwd_sm100_smem_bytes() {
     return Smem::xchg + Smem::xchg_bytes + 1024;  // + alignment slack
 }
 
-size_t fa_fwd_sm100_partial_bytes(int grid) {
-    // per CTA: O partial [2][128][64] f32, (m, l) [2][128][2] f32
-    return static_cast<size_t>(grid) * (2 * kBlockM * kHeadDim * 4 + 2 * kBlockM * 2 * 4);
+size_t fa_fwd_sm100_partial_bytes(int grid, int head_dim) {
+    // per CTA: O partial [2][128][head_dim] f32 (head_dim 64 here, 128 in fa_fwd_sm100_d128.cu), (m, l) [2][128][2] f32
+    return static_cast<size_t>(grid) * (2 * kBlockM * static_cast<size_t>(head_dim) * 4 + 2 * kBlockM * 2 * 4);
 }
 
 size_t fa_fwd_sm100_flag_bytes(int grid) {
@@ -1083,10 +1083,10 @@ size_t fa_fwd_sm100_flag_bytes(int grid) {
 
 // Carves the split-pair workspace.  `flags` (fa_fwd_sm100_flag_bytes) must be zero when the kernel starts; the
 // kernel leaves it zero.
-void fa_fwd_sm100_partial_carve(void* base, void* flags, int grid, FaParams* p) {
+void fa_fwd_sm100_partial_carve(void* base, void* flags, int grid, int head_dim, FaParams* p) {
     uint8_t* b = static_cast<uint8_t*>(base);
     p->part_o = reinterpret_cast<float*>(b);
-    b += static_cast<size_t>(grid) * 2 * kBlockM * kHeadDim * 4;
+    b += static_cast<size_t>(grid) * 2 * kBlockM * static_cast<size_t>(head_dim) * 4;
     p->part_ml = reinterpret_cast<float*>(b);
     p->part_flag = static_cast<int*>(flags);
 }

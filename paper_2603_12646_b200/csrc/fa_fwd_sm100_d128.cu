@@ -18,7 +18,11 @@
 //                          P (16-bit) written over the thread's own S columns, lazy rescale of O
 // TMEM: S_A [0,128)  S_B [128,256)  O_A [256,384)  O_B [384,512).
 // Work distribution: whole query-tile pairs -- one per CTA (sched_mode 0: a single wave, split-KV partials) or
-// dealt round-robin over a persistent grid (sched_mode 2).
+// dealt round-robin over a persistent grid (sched_mode 2) -- or, as in fa_fwd_sm100.cu, statically balanced slices of
+// the flat (pair x key tile) space (sched_mode 1): a pair cut between CTA c (leading key tiles, its FIRST item) and CTA
+// c + 1 (trailing key tiles, its LAST item) is merged in-kernel from the partial c published; a CTA only ever waits
+// for a lower-indexed CTA.  (384 pairs on 148 SMs are three rounds of which the last is 60 % full: 13.5 % of the
+// SM time idle with whole pairs.)
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -83,21 +87,49 @@ struct Item {
     int b, h, q0;
     int n0, n1;    // key tiles [n0, n1)
     int num_live;  // tiles in the range that are not fully padded
+    int kind;      // kItemFull / kItemPublish (leading key tiles of a cut pair) / kItemMerge (its trailing key tiles)
     bool has_b;
 };
+enum : int { kItemFull = 0, kItemPublish = 1, kItemMerge = 2 };
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
 
 template <bool kHasBias>
 __device__ __forceinline__ bool tile_live(const FaParams& p, int b, int n) {
     return !kHasBias || p.tile_flags[b * p.n_kv_tiles + n] != kTileSkip;
 }
 
-// i-th item of this CTA (i = 0, 1, ...): pair blockIdx.x + i * gridDim.x (sched_mode 2) or blockIdx.x (mode 0)
+// i-th item of this CTA (i = 0, 1, ...): pair blockIdx.x + i * gridDim.x (sched_mode 2), blockIdx.x (mode 0), or the
+// i-th pair from the END of the CTA's slice of the flat (pair x key tile) space, cut to the slice (mode 1)
 template <bool kHasBias>
 __device__ __forceinline__ bool get_item(const FaParams& p, int i, Item& it) {
-    const long long lin = p.sched_mode == 2 ? blockIdx.x + static_cast<long long>(i) * gridDim.x
-                                            : (i == 0 ? static_cast<long long>(blockIdx.x) : p.total_pairs);
-    if (lin >= p.total_pairs) return false;
-    const int pair_lin = static_cast<int>(lin);
+    int pair_lin, k0 = 0, k1 = 0x7fffffff;
+    it.kind = kItemFull;
+    if (p.sched_mode == 1) {
+        const long long K = p.tiles_per_pair;
+        const long long total = static_cast<long long>(p.total_pairs) * K;
+        const long long t0 = total * blockIdx.x / gridDim.x, t1 = total * (blockIdx.x + 1) / gridDim.x;
+        if (t1 <= t0) return false;
+        const long long pl = (t1 - 1) / K - i;
+        if (pl < t0 / K) return false;
+        const long long pair_start = pl * K;
+        pair_lin = static_cast<int>(pl);
+        k0 = static_cast<int>(max(t0, pair_start) - pair_start);
+        k1 = static_cast<int>(min(t1, pair_start + K) - pair_start);
+        it.kind = k0 > 0 ? kItemMerge : (k1 < K ? kItemPublish : kItemFull);
+    } else {
+        const long long lin = p.sched_mode == 2 ? blockIdx.x + static_cast<long long>(i) * gridDim.x
+                                                : (i == 0 ? static_cast<long long>(blockIdx.x) : p.total_pairs);
+        if (lin >= p.total_pairs) return false;
+        pair_lin = static_cast<int>(lin);
+    }
     const int px = pair_lin % p.pairs_per_head;
     const int bh = pair_lin / p.pairs_per_head;
     it.h = bh % p.H;
@@ -108,8 +140,11 @@ __device__ __forceinline__ bool get_item(const FaParams& p, int i, Item& it) {
     int j_lo = p.kv_begin, j_hi = p.kv_end;
     if (p.wl >= 0) j_lo = max(j_lo, it.q0 - p.wl);
     if (p.wr >= 0) j_hi = min(j_hi, rows_end + p.wr);
-    it.n0 = j_lo >> 7;
-    it.n1 = (j_hi > j_lo) ? ((j_hi + kBlockN - 1) >> 7) : it.n0;
+    const int pn0 = j_lo >> 7;
+    const int pn1 = (j_hi > j_lo) ? ((j_hi + kBlockN - 1) >> 7) : pn0;
+    // the item's slice of the pair's key tiles (mode 1: virtual tile v is real tile pn0 + v; past the last tile: empty)
+    it.n0 = min(pn0 + k0, pn1);
+    it.n1 = (k1 >= pn1 - pn0) ? pn1 : pn0 + k1;
     it.num_live = 0;
     for (int n = it.n0; n < it.n1; ++n) it.num_live += tile_live<kHasBias>(p, it.b, n) ? 1 : 0;
     return true;
@@ -502,53 +537,117 @@ fa_fwd_sm100_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 named_bar_sync(bar_id, kPairThreads);
                 const float l_tot = l_run + lrow[(hf ^ 1) * kBlockM];
                 named_bar_sync(bar_id, kPairThreads);  // reads done before the next item reuses the slot
-                const float inv = l_tot > 0.f ? 1.0f / l_tot : 0.f;
                 if (num_live > 0) {
                     mbar_wait(bar(kBarOFull + x), oi & 1u, wctx);
                     tc_fence_after();
                 }
                 const size_t ridx = (static_cast<size_t>(b) * p.H + h) * p.S + row;
-                if (p.o_partial != nullptr && hf == 0 && row < p.S) {
-                    p.m_partial[ridx] = m_ref;
-                    p.l_partial[ridx] = l_tot;
-                }
+                if (item.kind == kItemPublish) {
+                    // this CTA owns only the leading key tiles of the pair: un-normalised partial for CTA blockIdx.x + 1
+                    const size_t slot = (static_cast<size_t>(blockIdx.x) * 2 + x) * kBlockM + r;
 #pragma unroll
-                for (int cb = 0; cb < 2; ++cb) {
-                    const int col0 = hf * (kD / 2) + cb * 32;
-                    float o[32];
-                    if (num_live > 0) {
-                        tmem_ld32(t_o + cb * 32, reinterpret_cast<uint32_t(&)[32]>(o));
-                        tc_wait_ld();
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < 32; ++u) o[u] = 0.f;
-                    }
-                    if (row >= p.S) continue;
-                    if (p.o_partial != nullptr) {
-                        float4* dst = reinterpret_cast<float4*>(p.o_partial + ridx * kD + col0);
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) dst[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
-                    } else {
-                        const size_t off = static_cast<size_t>(b) * p.o_sb + static_cast<size_t>(h) * p.o_sh +
-                                           static_cast<size_t>(row) * p.o_ss + col0;
-                        if (p.out_dtype == 2) {
-                            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
-#pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                dst[u] = make_float4(o[4 * u] * inv, o[4 * u + 1] * inv, o[4 * u + 2] * inv, o[4 * u + 3] * inv);
+                    for (int cb = 0; cb < 2; ++cb) {
+                        uint32_t o[32];
+                        if (num_live > 0) {
+                            tmem_ld32(t_o + cb * 32, o);
+                            tc_wait_ld();
                         } else {
-                            uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + off);
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                uint32_t w[4];
+                            for (int u = 0; u < 32; ++u) o[u] = 0u;
+                        }
+                        float* dst = p.part_o + slot * kD + hf * (kD / 2) + cb * 32;  // 128-byte aligned
 #pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    const float a0 = o[8 * u + 2 * e] * inv, a1 = o[8 * u + 2 * e + 1] * inv;
-                                    w[e] = (p.out_dtype == 0) ? pack2<true>(a0, a1) : pack2<false>(a0, a1);
-                                }
-                                dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+                        for (int u = 0; u < 4; ++u) st_global_v8(dst + 8 * u, reinterpret_cast<const uint32_t(&)[8]>(o[8 * u]));
+                    }
+                    if (hf == 0) {
+                        p.part_ml[slot * 2] = m_ref;
+                        p.part_ml[slot * 2 + 1] = l_tot;
+                    }
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) st_release_gpu(p.part_flag + blockIdx.x * kNumSoftmaxWarps + warp, 1);
+                } else {
+                    float l_fin = l_tot, w1 = 1.0f, w2 = 0.0f;
+                    const float* part_src = nullptr;
+                    if (item.kind == kItemMerge) {
+                        // the partial CTA blockIdx.x - 1 published for the same rows at the START of its slice (its
+                        // half-0 warp of the same quadrant wrote m and l, this warp's twin wrote the columns); own part
+                        // first: fixed order, deterministic.  Only ever a wait for a lower-indexed CTA.
+                        const int* flag_o = p.part_flag + (blockIdx.x - 1) * kNumSoftmaxWarps + warp;
+                        const int* flag_ml = p.part_flag + (blockIdx.x - 1) * kNumSoftmaxWarps + (warp & ~4);
+                        uint32_t spins = 0;
+                        while (ld_acquire_gpu(flag_o) == 0 || ld_acquire_gpu(flag_ml) == 0) {
+                            if (!wait_slow_path(spins, wctx, kStatusPeerTimeout)) break;
+                        }
+                        const size_t slot = (static_cast<size_t>(blockIdx.x - 1) * 2 + x) * kBlockM + r;
+                        const float m2 = __ldcg(p.part_ml + slot * 2);
+                        const float l2 = __ldcg(p.part_ml + slot * 2 + 1);
+                        const float ms = fmaxf(m_ref, m2);
+                        w1 = (m_ref == -CUDART_INF_F) ? 0.f : ex2(m_ref - ms);
+                        w2 = (m2 == -CUDART_INF_F) ? 0.f : ex2(m2 - ms);
+                        l_fin = l_tot * w1 + l2 * w2;
+                        m_ref = ms;
+                        part_src = p.part_o + slot * kD + hf * (kD / 2);
+                    }
+                    const float inv = l_fin > 0.f ? 1.0f / l_fin : 0.f;
+                    if (p.o_partial != nullptr && hf == 0 && row < p.S) {
+                        p.m_partial[ridx] = m_ref;
+                        p.l_partial[ridx] = l_fin;
+                    }
+#pragma unroll
+                    for (int cb = 0; cb < 2; ++cb) {
+                        const int col0 = hf * (kD / 2) + cb * 32;
+                        float o[32];
+                        if (num_live > 0) {
+                            tmem_ld32(t_o + cb * 32, reinterpret_cast<uint32_t(&)[32]>(o));
+                            tc_wait_ld();
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 32; ++u) o[u] = 0.f;
+                        }
+                        if (part_src != nullptr) {
+                            const float4* src = reinterpret_cast<const float4*>(part_src + cb * 32);
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const float4 t = __ldcg(src + u);
+                                o[4 * u] = o[4 * u] * w1 + t.x * w2;
+                                o[4 * u + 1] = o[4 * u + 1] * w1 + t.y * w2;
+                                o[4 * u + 2] = o[4 * u + 2] * w1 + t.z * w2;
+                                o[4 * u + 3] = o[4 * u + 3] * w1 + t.w * w2;
                             }
                         }
+                        if (row >= p.S) continue;
+                        if (p.o_partial != nullptr) {
+                            float4* dst = reinterpret_cast<float4*>(p.o_partial + ridx * kD + col0);
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) dst[u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+                        } else {
+                            const size_t off = static_cast<size_t>(b) * p.o_sb + static_cast<size_t>(h) * p.o_sh +
+                                               static_cast<size_t>(row) * p.o_ss + col0;
+                            if (p.out_dtype == 2) {
+                                float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+#pragma unroll
+                                for (int u = 0; u < 8; ++u)
+                                    dst[u] = make_float4(o[4 * u] * inv, o[4 * u + 1] * inv, o[4 * u + 2] * inv, o[4 * u + 3] * inv);
+                            } else {
+                                uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + off);
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    uint32_t w[4];
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        const float a0 = o[8 * u + 2 * e] * inv, a1 = o[8 * u + 2 * e + 1] * inv;
+                                        w[e] = (p.out_dtype == 0) ? pack2<true>(a0, a1) : pack2<false>(a0, a1);
+                                    }
+                                    dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+                                }
+                            }
+                        }
+                    }
+                    if (item.kind == kItemMerge) {
+                        // the flags are left as they were found (zero): this warp and its twin are their only readers
+                        named_bar_sync(bar_id, kPairThreads);
+                        if (lane == 0) p.part_flag[(blockIdx.x - 1) * kNumSoftmaxWarps + warp] = 0;
                     }
                 }
                 if (num_live > 0) {

@@ -87,15 +87,15 @@ size_t fa_fwd_sm100_local_smem_bytes();
 cudaError_t launch_fa_fwd_sm100_local(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
                                       const FaParams& p, const float* pad_bias, bool bf16, int grid,
                                       cudaStream_t stream);
-// head_dim 128 kernel (fa_fwd_sm100_d128.cu): whole query-tile pairs, sched_mode 0 or 2
+// head_dim 128 kernel (fa_fwd_sm100_d128.cu): sched_mode 0, 1 or 2 as the head_dim-64 kernel
 cudaError_t launch_fa_fwd_sm100_d128(const CUtensorMap& tmq, const CUtensorMap& tmk, const CUtensorMap& tmv,
                                      const FaParams& p, bool bf16, int grid, cudaStream_t stream);
 size_t fa_fwd_sm100_d128_smem_bytes();
 bool fa_fwd_sm100_d128_available();
 size_t fa_fwd_sm100_smem_bytes();
-size_t fa_fwd_sm100_partial_bytes(int grid);
+size_t fa_fwd_sm100_partial_bytes(int grid, int head_dim);  // head_dim 64 (also for 32, zero-padded) or 128
 size_t fa_fwd_sm100_flag_bytes(int grid);
-void fa_fwd_sm100_partial_carve(void* base, void* flags, int grid, FaParams* p);
+void fa_fwd_sm100_partial_carve(void* base, void* flags, int grid, int head_dim, FaParams* p);
 cudaError_t launch_fa_fwd_simt(const SimtParams& p, cudaStream_t stream, int* grid_ctas);
 
 cudaError_t launch_bias_prepare(const float* pad_bias, int B, int S, float* bias2, uint8_t* tile_flags,

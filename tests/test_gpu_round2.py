@@ -178,6 +178,39 @@ def test_head_dims_32_128_long_sequence_and_split_kv(torch_mod, P, oracle, d):
     assert (merged - full).abs().max().item() <= 2e-3
 
 
+def test_head_dim_128_balanced_schedule_split_pairs(torch_mod, P, oracle):
+    """head_dim 128 over more query-tile pairs than SMs runs the balanced schedule of the head_dim-64 kernel (slices of
+    the flat (pair x key tile) space, cut pairs merged in-kernel): 384 pairs on 148 SMs, every CTA publishes and merges.
+    Checked against the CUDA-core kernel on every head, against the oracle on one, bit-identical from launch to launch
+    (plan relaunches on one workspace: the flags are left zero), and with ragged lengths."""
+    torch = torch_mod
+    from paper_2603_12646_b200 import capi
+    from paper_2603_12646_b200.attention import FaPlan
+    for (B, H, S, lens) in ((1, 12, 8192, None), (3, 4, 5000, [5000, 1234, 4097])):
+        g = torch.Generator(device="cuda").manual_seed(128 + S)
+        q, k, v = [(torch.rand((B, H, S, 128), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(3)]
+        pb = torch.from_numpy(tail_pad(B, S, lens)).cuda() if lens else None
+        spec = P.AttentionSpec(0.0, -1, -1, pb)
+        st = P.FlashStats()
+        out = P.flash_attention(q, k, v, spec, stats=st, out_dtype=torch.float32)
+        ref = P.flash_attention(q, k, v, spec, kernel="simt", out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert st.kernel == "tcgen05" and st.grid_ctas == torch.cuda.get_device_properties(0).multi_processor_count
+        assert (out - ref).abs().max().item() <= 5e-3
+        if S <= 5000:   # the oracle on one (batch, head) slice (a few seconds of scalar C)
+            b, h = 1, H - 1
+            want = oracle.flash_attention(*[t[b:b + 1, h:h + 1].float().cpu().numpy() for t in (q, k, v)], 0.0, -1, -1,
+                                          pb[b:b + 1].cpu().numpy() if pb is not None else None)
+            assert np.abs(out[b:b + 1, h:h + 1].cpu().numpy() - want).max() <= TOL
+        o2 = torch.empty_like(out)
+        plan = FaPlan(q, k, v, spec, out=o2)
+        for _ in range(5):
+            plan.launch()
+        torch.cuda.synchronize()
+        assert plan.status() == capi.RF_OK and torch.equal(o2, out)
+        plan.close()
+
+
 # ------------------------------------------------------------------ plan object
 def test_plan_launch_equals_direct_call_and_reports_status(torch_mod, P, oracle):
     """rf_fa_plan_create / rf_fa_plan_launch: same result bit for bit as rf_fa_fwd, relaunchable after the
