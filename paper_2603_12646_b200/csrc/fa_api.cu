@@ -292,8 +292,8 @@ Plan make_plan(const rf_fa_params* p, const Resolved& r, int kernel) {
         const char* env = std::getenv("RF_FA_SKIP_MAX");
         return env == nullptr || env[0] != '0';
     }();
-    if (p->d == 128) pl.d128 = true;  // own kernel (fa_fwd_sm100_d128.cu): same schedules, no row-max skip
-    if (skip_max_enabled && p->S >= 1024 && !pl.d128)
+    if (p->d == 128) pl.d128 = true;  // own kernel (fa_fwd_sm100_d128.cu): same schedules, same row-max skip
+    if (skip_max_enabled && p->S >= 1024)
         pl.kmax_bytes = align_up(static_cast<size_t>(p->B) * p->H * n_kv_tiles(p->S) * sizeof(float), 256);
     if (!r.partial && pl.total_pairs > sms) {
         pl.sched_mode = 1;

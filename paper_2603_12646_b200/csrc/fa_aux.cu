@@ -75,18 +75,21 @@ __global__ void __launch_bounds__(128) k_tile_norms_kernel(const uint16_t* __res
     const int rgrp = threadIdx.x >> 3;  // row inside a pass of 16 rows
     const uint16_t* kb = k + b * k_sb + h * k_sh + sub * 8;
     constexpr int kPasses = kBlockN / 16;
-    uint4 kv[kPasses];
+    // head_dim 128: rows are sixteen chunks, a thread takes chunks sub and sub + 8
+    uint4 kv[kPasses], kw[kPasses];
 #pragma unroll
     for (int pass = 0; pass < kPasses; ++pass) {
         const int row = n * kBlockN + pass * 16 + rgrp;
-        kv[pass] = make_uint4(0u, 0u, 0u, 0u);
+        kv[pass] = kw[pass] = make_uint4(0u, 0u, 0u, 0u);
         if (row < S && sub * 8 < d)  // head_dim 32: rows are four 16-byte chunks
             kv[pass] = __ldg(reinterpret_cast<const uint4*>(kb + row * k_ss));
+        if (row < S && 64 + sub * 8 < d) kw[pass] = __ldg(reinterpret_cast<const uint4*>(kb + row * k_ss + 64));
     }
     float kn_max = 0.f;
 #pragma unroll
     for (int pass = 0; pass < kPasses; ++pass) {
         float ks = sumsq8_bound<kBf16>(kv[pass]);
+        if (d > 64) ks += sumsq8_bound<kBf16>(kw[pass]);
 #pragma unroll
         for (int o = 4; o > 0; o >>= 1) ks += __shfl_xor_sync(0xffffffffu, ks, o);
         kn_max = fmaxf(kn_max, ks);

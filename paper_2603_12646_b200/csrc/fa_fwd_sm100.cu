@@ -155,57 +155,6 @@ constexpr uint32_t kTmemSlotOff = kNumBars * 8;                     // u32: TMEM
 constexpr uint32_t kWaitBlockOff = (kTmemSlotOff + 8 + 15) & ~15u;  // 16 bytes: abort word + status pointer (ptx.cuh)
 static_assert(kWaitBlockOff + 16 <= Smem::bar_bytes, "barrier block too small");
 
-// An UPPER bound (within 1.6 %) of the sum of squares of the eight 16-bit values of a 16-byte chunk, added to two
-// independent accumulators.  bf16: the odd element of a word is used as it sits in the word -- the even element's
-// bits below it only lengthen the mantissa, |w| >= |hi| and at most 2^-7 larger -- which saves the mask; the skip test
-// needs a bound, not the norm.
-template <bool kBf16>
-__device__ __forceinline__ void sumsq_chunk(const uint4& v, float& a0, float& a1) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        float lo, hi;
-        if (kBf16) {
-            lo = __uint_as_float(w[e] << 16);
-            hi = __uint_as_float(w[e]);
-        } else {
-            const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
-            lo = f2.x;
-            hi = f2.y;
-        }
-        a0 = fmaf(lo, lo, a0);
-        a1 = fmaf(hi, hi, a1);
-    }
-}
-__device__ __forceinline__ uint4 lds128(uint32_t addr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-    return v;
-}
-// Bound of |row|^2 for kRows 128-byte rows (kStride bytes apart) of a 128B-swizzled tile at once.  The swizzle
-// permutes a row's eight chunks, which a sum does not care about; lane l starts at chunk l mod 8 so that the warp's
-// 32 rows hit all banks (4 wavefronts per LDS.128).  Loads go out in batches, and every row has two accumulators.
-template <bool kBf16, int kRows, uint32_t kStride>
-__device__ __forceinline__ void rows_sumsq(uint32_t row_addr, int lane, float (&out)[kRows]) {
-    float a0[kRows], a1[kRows];
-#pragma unroll
-    for (int r = 0; r < kRows; ++r) a0[r] = a1[r] = 0.f;
-#pragma unroll
-    for (int c = 0; c < 8; c += 2) {
-        uint4 v[kRows][2];
-#pragma unroll
-        for (int r = 0; r < kRows; ++r)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) v[r][u] = lds128(row_addr + r * kStride + (((c + u + lane) & 7) << 4));
-#pragma unroll
-        for (int r = 0; r < kRows; ++r)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) sumsq_chunk<kBf16>(v[r][u], a0[r], a1[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < kRows; ++r) out[r] = a0[r] + a1[r];
-}
-
 // kItemPublish: the CTA owns the LEADING key tiles of a pair cut at the end of its slice: processed first, partial
 // published for the next CTA.  kItemMerge: it owns the TRAILING key tiles of the pair its slice starts in:
 // processed last, merged with the partial of the previous CTA.

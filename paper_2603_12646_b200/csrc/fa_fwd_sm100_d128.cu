@@ -51,7 +51,10 @@ constexpr int kThreads = 640;
 constexpr int kHalfN = kBlockN / 2;
 constexpr int kRegsSoftmax = 112;
 constexpr int kRegsOther = 32;
-constexpr int kEmuEvery = 8;                  // every 8th element pair of a full tile: FMA-pipe exp2
+#ifndef RF_FA_D128_EMU_EVERY
+#define RF_FA_D128_EMU_EVERY 5  // 326 us at 8K; 8: 328, 16: 329, 4: 334 (same-box sweep)
+#endif
+constexpr int kEmuEvery = RF_FA_D128_EMU_EVERY;  // every n-th element pair of a full tile: FMA-pipe exp2
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;                 // + 128 * X
 constexpr uint32_t kColO = 256;               // + 128 * X
@@ -189,7 +192,7 @@ fa_fwd_sm100_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         prefetch_tensormap(&tm_k);
         prefetch_tensormap(&tm_v);
         mbar_init(bar(kBarQFull), 1);
-        mbar_init(bar(kBarQEmpty), 1);
+        mbar_init(bar(kBarQEmpty), 1 + kNumSoftmaxWarps);  // the UMMA commit and every softmax warp (row norms from the Q tile)
         for (int s = 0; s < kStages; ++s) {
             mbar_init(bar(kBarKFull + s), 1);
             mbar_init(bar(kBarKEmpty + s), 1);
@@ -390,6 +393,7 @@ fa_fwd_sm100_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         constexpr float kThreshold = kBf16 ? kRescaleThresholdBf16 : kRescaleThresholdF16;
 
         uint32_t oi = 0;    // items with work so far (O-full phase)
+        uint32_t qn = 0;    // items with live key tiles so far, whether this tile took part or not (Q-full phase)
         uint32_t sp = 0;    // phase parity of the next S-full wait
         uint32_t xpar = 0;  // exchange double buffer
 
@@ -402,6 +406,23 @@ fa_fwd_sm100_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             const int row = tile_r_lo + r;
             float m_ref = -CUDART_INF_F;
             float l_run = 0.f;
+            // Row-max skip (fa_fwd_sm100.cu): c |q_row| max_j |k_j| bounds every score of the row in a key tile; |q_row|
+            // from the Q tile in shared memory (two 64-column boxes), the key-tile norms from k_tile_norms_kernel.
+            float qn_c = CUDART_INF_F;
+            const float* kmax_row = nullptr;
+            if (num_live > 0) {
+                mbar_wait(bar(kBarQFull), qn & 1u, wctx);
+                if (active && p.kmax != nullptr) {
+                    kmax_row = p.kmax + (static_cast<size_t>(b) * p.H + h) * p.n_kv_tiles;
+                    const uint32_t qrow = smem_base + Smem::q + x * kTileBytes + static_cast<uint32_t>(r) * 128u;
+                    float sq[2];
+                    rows_sumsq<kBf16, 2, static_cast<uint32_t>(kBoxBytes)>(qrow, lane, sq);
+                    qn_c = sqrtf(sq[0] + sq[1]) * c * 1.001f;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar(kBarQEmpty));
+                ++qn;
+            }
 
             if (active && num_live > 0) {
                 // key tiles [nf0, nf1) need no window / range predicate for any row of this query tile
@@ -422,6 +443,7 @@ fa_fwd_sm100_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                         if (flag == kTileSkip) continue;
                     }
                     const int kv0 = n * kBlockN;
+                    const float kmax_n = kmax_row != nullptr ? __ldg(kmax_row + n) : CUDART_INF_F;  // back before S is
                     mbar_wait(bar(kBarSFull + x), sp, wctx);
                     tc_fence_after();
                     uint32_t su[kHalfN];
@@ -431,8 +453,12 @@ fa_fwd_sm100_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     tc_wait_ld();
 
                     const bool full = (n >= nf0) && (n < nf1) && (flag == kTileFull);
-                    float my_max, mul;
-                    if (full) {
+                    // no score of this tile can move the reference max (warp-uniform; both halves decide alike)
+                    const bool skip_max = full && !__any_sync(0xffffffffu, !(qn_c * kmax_n <= m_ref + kThreshold));
+                    float my_max = 0.f, mul;
+                    if (skip_max) {
+                        mul = c;
+                    } else if (full) {
                         float mx[4];
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4) mx[q4] = __uint_as_float(su[q4]);
@@ -475,13 +501,16 @@ fa_fwd_sm100_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                         mul = 1.0f;
                     }
                     // row max over both halves (smem, double-buffered); lazy running max
-                    float* xrow = xrow_base + xpar * (4 * kBlockM);
-                    xrow[hf * kBlockM] = my_max;
-                    named_bar_sync(bar_id, kPairThreads);
-                    const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
-                    xpar ^= 1u;
-                    const float m_new = (tile_max > m_ref + kThreshold) ? tile_max : m_ref;
-                    const float alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
+                    float m_new = m_ref, alpha = 1.0f;
+                    if (!skip_max) {
+                        float* xrow = xrow_base + xpar * (4 * kBlockM);
+                        xrow[hf * kBlockM] = my_max;
+                        named_bar_sync(bar_id, kPairThreads);
+                        const float tile_max = fmaxf(my_max, xrow[(hf ^ 1) * kBlockM]);
+                        xpar ^= 1u;
+                        m_new = (tile_max > m_ref + kThreshold) ? tile_max : m_ref;
+                        alpha = (m_new == m_ref) ? 1.0f : ex2(m_ref - m_new);
+                    }
                     const float neg_m = (m_new == -CUDART_INF_F) ? 0.f : -m_new;
 
                     // P = 2^(s*mul - m); on full tiles every kEmuEvery-th pair takes the FMA-pipe polynomial
@@ -520,7 +549,7 @@ fa_fwd_sm100_d128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     m_ref = m_new;
                     // O_X *= alpha where the reference max moved.  S-full of this tile was committed after P V of
                     // the previous one (in-order pipe), so O is stable until this tile's P is published.
-                    if (it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o_rows_d128(t_o, alpha);
+                    if (!skip_max && it > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o_rows_d128(t_o, alpha);
                     tc_wait_st();
                     tc_fence_before();
                     mbar_arrive(bar(kBarPFull + x));
