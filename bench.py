@@ -388,6 +388,13 @@ def run_ours(args):
                 extra[f"S8192_d{d2}"] = {"ms": ms_d, "tflops": f_d / ms_d / 1e9, "frac_of_peak": f_d / ms_d / 1e9 / peaks["bf16"],
                                          "kernel": "fa_fwd_sm100_kernel (zero-padded to 64)" if d2 == 32 else "fa_fwd_sm100_d128_kernel"}
                 del sets_d, outs_d
+            # head_dim 128 at 16K tokens (the tensor-bound case of the contract's head dims)
+            sets_d, outs_d = make_sets(torch, B, H, 16384, 128, 2, seed=13)
+            ms_d = time_op(torch, P, sets_d, spec, 10, 3, outs_d, settle_s=0.5)
+            f_d = flops_global(B, H, 16384, 128)
+            extra["S16384_d128"] = {"ms": ms_d, "tflops": f_d / ms_d / 1e9, "frac_of_peak": f_d / ms_d / 1e9 / peaks["bf16"],
+                                    "kernel": "fa_fwd_sm100_d128_kernel"}
+            del sets_d, outs_d
             wl, wr = P.local_window_attrs()
             msl = time_op_graph(torch, P, sets, P.AttentionSpec(0.0, wl, wr), 20, outs)
             bytes_l = 4.0 * B * H * S * D * 2
